@@ -1,0 +1,232 @@
+/*
+ * phasemask_b200 — C ABI of the B200-native phase-mask solver.
+ *
+ * This is the drop-in boundary for the reference's hot path, the
+ * Gerchberg–Saxton / alternating-projections solver of arXiv 1302.0120
+ * (reference package `phasemask`, /root/reference/pkg/src/phasemask; `src/`
+ * below). The reference is pure Python, so its "FFI" is the Python call
+ * surface; every entry point below names the reference function it replaces.
+ * The Python host layer (paper_1302_0120_b200/) binds these with ctypes —
+ * see INTEGRATION.md for the binding a `phasemask` maintainer would add.
+ *
+ * Conventions
+ *  - Grids are (n_y, n_x) row-major, flat index k*n_x + j (src/grid.py:1-6).
+ *  - Complex data is interleaved re,im (numpy complex64/complex128 layout).
+ *  - precision: 0 = single (float/complex64), 1 = double (src/grid.py:24-48).
+ *  - Real inputs (p, m) are in the plan precision's float type.
+ *  - Transforms are unitary (1/sqrt(N) split over both directions), standard
+ *    unshifted frequency order (src/transform.py:1-7).
+ *  - n_x and n_y must be powers of two in [1, 4096].
+ *  - Every function returns 0 on success or a negative PM_ERR_* code;
+ *    pm_last_error() returns the calling thread's last message.
+ *  - "_device" variants take device pointers on the plan's device and run
+ *    asynchronously on the plan's stream; the others take host pointers,
+ *    copy through pinned staging and synchronise before returning.
+ *  - No CPU fallback: without a CUDA device every compute call fails with
+ *    PM_ERR_CUDA.
+ */
+#ifndef PHASEMASK_B200_H
+#define PHASEMASK_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PM_OK              0
+#define PM_ERR_ARG        -1   /* invalid argument            -> ValueError      */
+#define PM_ERR_CUDA       -2   /* CUDA runtime failure        -> RuntimeError    */
+#define PM_ERR_NOMEM      -3   /* cudaErrorMemoryAllocation   -> MemoryError     */
+#define PM_ERR_UNSUPPORTED -4  /* size/precision not supported -> NotImplementedError */
+#define PM_ERR_DIVERGED   -5   /* non-finite iterate          -> SolveDivergedError */
+
+#define PM_SINGLE 0
+#define PM_DOUBLE 1
+
+#define PM_FORWARD  (-1)      /* exp(-2 pi i jk/n), FftProvider.forward */
+#define PM_INVERSE  (+1)      /* exp(+2 pi i jk/n), FftProvider.inverse */
+
+#define PM_ALGO_GS   0        /* alternating projections, src/solver.py:150-170 */
+#define PM_ALGO_RAAR 1        /* Luke 2005 relaxed averaged alternating reflections */
+
+typedef struct pm_plan pm_plan;
+
+/* ------------------------------------------------------------------ misc */
+
+/* Library version as 10000*major + 100*minor + patch. */
+int pm_version(void);
+
+/* Number of visible CUDA devices (0 when none). */
+int pm_device_count(int *count);
+
+/* Message for the calling thread's most recent failure ("" if none). */
+const char *pm_last_error(void);
+
+/* ------------------------------------------------------------------ plans */
+
+/*
+ * Create a plan for one grid and precision on `device`, with device buffers
+ * for up to `max_batch` masks (grown on demand). Replaces
+ * FftProvider(spec, precision, fft_workers) (src/transform.py:23-35) and the
+ * service's PlanCache entry (src/service.py:65-82).
+ */
+int pm_plan_create(int device, int n_x, int n_y, int precision, int max_batch,
+                   pm_plan **out);
+int pm_plan_destroy(pm_plan *plan);
+
+/* Use an external CUDA stream (cudaStream_t as void*; NULL = plan's own). */
+int pm_plan_set_stream(pm_plan *plan, void *stream);
+int pm_plan_get_stream(pm_plan *plan, void **stream);
+int pm_plan_synchronize(pm_plan *plan);
+
+/* Kernel launches issued by this plan since creation (evidence counter). */
+int pm_plan_launch_count(pm_plan *plan, long long *count);
+
+/* ------------------------------------------------------------ transforms */
+
+/*
+ * Unitary 2-D DFT of `batch` fields, in -> out (may alias).
+ * Replaces FftProvider.forward / .inverse (src/transform.py:47-55),
+ * i.e. scipy.fft.fft2 / ifft2(norm="ortho").
+ */
+int pm_fft2(pm_plan *plan, const void *in, void *out, int direction, int batch);
+int pm_fft2_device(pm_plan *plan, const void *d_in, void *d_out, int direction,
+                   int batch);
+
+/* --------------------------------------------------------- projections */
+
+/*
+ * Per-pixel modulus replacement: out = mag >= zero_tol ? t*(u/|u|) : t+0i.
+ * Replaces _replace_modulus / _modulus_replace_kernel
+ * (src/projections.py:46-66), i.e. project_slm (t = p, :69-74) and
+ * project_modulus (t = m, :77-83). `target` has `batch` grids when
+ * target_per_field != 0, else one grid shared by the batch.
+ */
+int pm_replace_modulus(pm_plan *plan, const void *in, const void *target,
+                       int target_per_field, double zero_tol, void *out, int batch);
+int pm_replace_modulus_device(pm_plan *plan, const void *d_in, const void *d_target,
+                              int target_per_field, double zero_tol, void *d_out,
+                              int batch);
+
+/*
+ * P_M u = F^-1(replace_m(F u)) fused into three sweeps.
+ * Replaces project_fourier (src/projections.py:86-91).
+ */
+int pm_project_fourier(pm_plan *plan, const void *u, const void *m,
+                       double zero_tol_m, void *out);
+
+/*
+ * G(u) = ||P_S u - P_M u||_2 with a fixed-order fp64 reduction.
+ * Replaces metrics.gap (src/metrics.py:67-71).
+ */
+int pm_gap(pm_plan *plan, const void *u, const void *p, const void *m,
+           double zero_tol_p, double zero_tol_m, double *out_gap);
+
+/* --------------------------------------------------------- reductions */
+
+/*
+ * sqrt(sum |x|^2): moduli in the data's precision, squared and summed in
+ * fp64 in a fixed order. dtype: 0=f32 real, 1=f64 real, 2=c64, 3=c128.
+ * Replaces grid.norm2 / backends.deterministic_sum (src/grid.py:161-165,
+ * src/backends.py:109-125).
+ */
+int pm_norm2(int device, const void *data, long long count, int dtype, double *out);
+
+/*
+ * Fixed-order fp64 sum of `count` doubles (signed values allowed).
+ * Replaces backends.deterministic_sum (src/backends.py:109-125).
+ */
+int pm_sum(int device, const double *data, long long count, double *out);
+
+/*
+ * Phase extraction: out = mod(atan2(im, re), 2pi) in fp64, >= 2pi -> 0,
+ * |u| < zero_tol -> 0. Replaces grid.phases_of (src/grid.py:168-176).
+ */
+int pm_phases(int device, const void *u, long long count, int precision,
+              double zero_tol, double *out);
+
+/* --------------------------------------------------------------- solve */
+
+typedef struct pm_params {
+    int    algorithm;        /* PM_ALGO_GS | PM_ALGO_RAAR                       */
+    double beta;             /* RAAR relaxation (ignored for GS)                */
+    int    max_iters;        /* >= 1                  (SolveConfig.max_iters)   */
+    int    record_every;     /* >= 1               (SolveConfig.record_every)   */
+    double early_stop_tol;   /* < 0: off          (SolveConfig.early_stop_tol)  */
+    double t_lit, t_dark;    /* ErrorTolerances (src/metrics.py:30-39)          */
+    int    p_per_mask;       /* p has `batch` grids (1) or one shared grid (0)  */
+    int    init_complex;     /* 1: `m_init` holds complex Fourier-plane starts  */
+} pm_params;
+
+typedef struct pm_result {
+    /* host (pm_solve) or device (pm_solve_device) pointers; NULL = skip     */
+    double  *phases;         /* batch*N float64 mask in [0, 2pi)              */
+    uint8_t *levels;         /* batch*N uint8 SLM levels (PhaseMask.to_uint8) */
+    void    *u_star;         /* batch*N complex  (SolveResult.u_star)         */
+    void    *v_star;         /* batch*N complex  (SolveResult.v_star)         */
+    /* always host pointers, filled after completion (NULL = skip)           */
+    double  *gap;            /* batch*max_iters; NaN where not recorded       */
+    double  *err_lit;        /* batch*max_iters                               */
+    double  *err_dark;       /* batch*max_iters                               */
+    int     *iters_run;      /* batch                                         */
+    int     *diverged_iter;  /* batch; 0 = finite                             */
+    float   *device_ms;      /* 1: device time of the whole solve (events)    */
+} pm_result;
+
+/*
+ * Run the solver on `batch` independent masks and extract the
+ * best-approximation pair and phase mask of each.
+ * Replaces solver.solve (src/solver.py:111-216), including
+ * initial_iterate (:93-108), the record / early-stop logic (:173-195)
+ * and phases_of (:201-206); a batch replaces the sequential loop of
+ * PhaseMaskTransformer.transform (src/estimator.py:85-93).
+ *   p: real grid(s); m: real target moduli, batch grids;
+ *   zero_tol_p / zero_tol_m: per-mask thresholds (1024*eps*max), host arrays;
+ *   energy: per-mask sum(m^2) in fp64 (reconstructed-intensity scale);
+ *   m_init: complex starts when params->init_complex, else NULL.
+ * Returns PM_ERR_DIVERGED when any mask produced non-finite values
+ * (result->diverged_iter says which iteration).
+ */
+int pm_solve(pm_plan *plan, const void *p, const void *m, const void *m_init,
+             int batch, const pm_params *params, const double *zero_tol_p,
+             const double *zero_tol_m, const double *energy, pm_result *result);
+int pm_solve_device(pm_plan *plan, const void *d_p, const void *d_m,
+                    const void *d_m_init, int batch, const pm_params *params,
+                    const double *zero_tol_p, const double *zero_tol_m,
+                    const double *energy, pm_result *result);
+
+/*
+ * Incremental form for per-iteration host callbacks (on_record /
+ * should_abort, src/solver.py:188-199): begin, then step() one iteration at
+ * a time (records for the iterations stepped become readable), then finish()
+ * with abort != 0 to stop at the current iterate.
+ */
+int pm_solve_begin(pm_plan *plan, const void *p, const void *m, const void *m_init,
+                   int batch, const pm_params *params, const double *zero_tol_p,
+                   const double *zero_tol_m, const double *energy);
+int pm_solve_step(pm_plan *plan, int n_iters, int *all_stopped);
+int pm_solve_records(pm_plan *plan, int first_iter, int last_iter, double *gap,
+                     double *err_lit, double *err_dark, int *iters_run,
+                     int *diverged_iter);
+int pm_solve_finish(pm_plan *plan, int abort, pm_result *result);
+
+/* ------------------------------------------------------------ measurement */
+
+/*
+ * Time `reps` launches of one sweep kernel on the plan's resident buffers
+ * with CUDA events on the plan's stream (bench.py's roofline leg).
+ * which: 0 = row sweep (IFFT.P_S.FFT), 1 = column sweep (FFT.P_M.IFFT).
+ * Requires a prior pm_solve*_on this plan with >= batch masks.
+ */
+int pm_time_sweep(pm_plan *plan, int which, int batch, int reps, float *avg_ms);
+
+/* Device-to-device copy bandwidth over `bytes` (read+write counted), best of
+ * `reps`, for the HBM (bytes >> L2) and L2 (bytes << L2) roofs. */
+int pm_measure_copy(int device, long long bytes, int reps, double *gbs);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PHASEMASK_B200_H */

@@ -1,0 +1,288 @@
+"""ctypes binding of libphasemask_b200.so (C ABI in include/phasemask_b200.h).
+
+Loads the in-tree library (building it first when it is missing and nvcc is
+available), declares every entry point's signature and maps the library's
+error codes onto the exceptions the reference raises. There is no CPU
+fallback anywhere: if the library or a CUDA device is missing, calls raise.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+from pathlib import Path
+
+import numpy as np
+
+_PKG = Path(__file__).resolve().parent
+LIB_PATH = _PKG / "lib" / "libphasemask_b200.so"
+
+PM_OK = 0
+PM_ERR_ARG = -1
+PM_ERR_CUDA = -2
+PM_ERR_NOMEM = -3
+PM_ERR_UNSUPPORTED = -4
+PM_ERR_DIVERGED = -5
+
+PM_FORWARD = -1
+PM_INVERSE = +1
+PM_ALGO_GS = 0
+PM_ALGO_RAAR = 1
+
+
+class pm_params(C.Structure):
+    _fields_ = [
+        ("algorithm", C.c_int),
+        ("beta", C.c_double),
+        ("max_iters", C.c_int),
+        ("record_every", C.c_int),
+        ("early_stop_tol", C.c_double),
+        ("t_lit", C.c_double),
+        ("t_dark", C.c_double),
+        ("p_per_mask", C.c_int),
+        ("init_complex", C.c_int),
+    ]
+
+
+class pm_result(C.Structure):
+    _fields_ = [
+        ("phases", C.c_void_p),
+        ("levels", C.c_void_p),
+        ("u_star", C.c_void_p),
+        ("v_star", C.c_void_p),
+        ("gap", C.c_void_p),
+        ("err_lit", C.c_void_p),
+        ("err_dark", C.c_void_p),
+        ("iters_run", C.c_void_p),
+        ("diverged_iter", C.c_void_p),
+        ("device_ms", C.c_void_p),
+    ]
+
+
+# name -> (restype, argtypes); mirrors include/phasemask_b200.h one to one
+_VP, _I, _D, _LL = C.c_void_p, C.c_int, C.c_double, C.c_longlong
+SIGNATURES = {
+    "pm_version": (_I, []),
+    "pm_device_count": (_I, [C.POINTER(_I)]),
+    "pm_last_error": (C.c_char_p, []),
+    "pm_plan_create": (_I, [_I, _I, _I, _I, _I, C.POINTER(_VP)]),
+    "pm_plan_destroy": (_I, [_VP]),
+    "pm_plan_set_stream": (_I, [_VP, _VP]),
+    "pm_plan_get_stream": (_I, [_VP, C.POINTER(_VP)]),
+    "pm_plan_synchronize": (_I, [_VP]),
+    "pm_plan_launch_count": (_I, [_VP, C.POINTER(_LL)]),
+    "pm_fft2": (_I, [_VP, _VP, _VP, _I, _I]),
+    "pm_fft2_device": (_I, [_VP, _VP, _VP, _I, _I]),
+    "pm_replace_modulus": (_I, [_VP, _VP, _VP, _I, _D, _VP, _I]),
+    "pm_replace_modulus_device": (_I, [_VP, _VP, _VP, _I, _D, _VP, _I]),
+    "pm_project_fourier": (_I, [_VP, _VP, _VP, _D, _VP]),
+    "pm_gap": (_I, [_VP, _VP, _VP, _VP, _D, _D, C.POINTER(_D)]),
+    "pm_norm2": (_I, [_I, _VP, _LL, _I, C.POINTER(_D)]),
+    "pm_sum": (_I, [_I, _VP, _LL, C.POINTER(_D)]),
+    "pm_phases": (_I, [_I, _VP, _LL, _I, _D, _VP]),
+    "pm_solve": (_I, [_VP, _VP, _VP, _VP, _I, C.POINTER(pm_params), _VP, _VP, _VP,
+                      C.POINTER(pm_result)]),
+    "pm_solve_device": (_I, [_VP, _VP, _VP, _VP, _I, C.POINTER(pm_params), _VP, _VP, _VP,
+                             C.POINTER(pm_result)]),
+    "pm_solve_begin": (_I, [_VP, _VP, _VP, _VP, _I, C.POINTER(pm_params), _VP, _VP, _VP]),
+    "pm_solve_step": (_I, [_VP, _I, C.POINTER(_I)]),
+    "pm_solve_records": (_I, [_VP, _I, _I, _VP, _VP, _VP, _VP, _VP]),
+    "pm_solve_finish": (_I, [_VP, _I, C.POINTER(pm_result)]),
+    "pm_time_sweep": (_I, [_VP, _I, _I, _I, C.POINTER(C.c_float)]),
+    "pm_measure_copy": (_I, [_I, _LL, _I, C.POINTER(_D)]),
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+class SolveDivergedFromLib(RuntimeError):
+    """Internal: the library reported non-finite values (PM_ERR_DIVERGED)."""
+
+
+def load(build_if_missing: bool = True):
+    """Load (and, if needed, build) the native library; raise if impossible."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not LIB_PATH.exists():
+            if not build_if_missing or os.environ.get("PM_NO_AUTOBUILD"):
+                raise ImportError(f"{LIB_PATH} is missing; run `python -m paper_1302_0120_b200.build`")
+            from .build import build
+            build()
+        lib = C.CDLL(str(LIB_PATH))
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+    return _lib
+
+
+def last_error() -> str:
+    return load().pm_last_error().decode(errors="replace")
+
+
+def check(code: int, what: str = ""):
+    """Map a PM_ERR_* code to the reference's exception types."""
+    if code == PM_OK:
+        return
+    msg = last_error()
+    if what:
+        msg = f"{what}: {msg}"
+    if code == PM_ERR_ARG:
+        raise ValueError(msg)
+    if code == PM_ERR_NOMEM:
+        raise MemoryError(msg)
+    if code == PM_ERR_UNSUPPORTED:
+        raise NotImplementedError(msg)
+    if code == PM_ERR_DIVERGED:
+        raise SolveDivergedFromLib(msg)
+    raise RuntimeError(msg)
+
+
+def device_count() -> int:
+    n = C.c_int(0)
+    check(load().pm_device_count(C.byref(n)))
+    return n.value
+
+
+def ptr(a: np.ndarray | None):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+# --------------------------------------------------------------- plans
+
+class Plan:
+    """Owns one pm_plan: a grid, a precision, device buffers and a stream.
+
+    The analogue of the reference's FftProvider / PlanCache entry
+    (src/transform.py:23-35, src/service.py:65-82). Thread-safe: calls are
+    serialised by a per-plan lock, as PlanCache does.
+    """
+
+    def __init__(self, n_x: int, n_y: int, precision_code: int, device: int = 0, max_batch: int = 1):
+        self.lib = load()
+        self.n_x, self.n_y, self.prec, self.device = n_x, n_y, precision_code, device
+        self.lock = threading.Lock()
+        h = C.c_void_p()
+        check(self.lib.pm_plan_create(device, n_x, n_y, precision_code, max_batch, C.byref(h)),
+              "pm_plan_create")
+        self.handle = h
+
+    @property
+    def complex_dtype(self):
+        return np.complex64 if self.prec == 0 else np.complex128
+
+    @property
+    def float_dtype(self):
+        return np.float32 if self.prec == 0 else np.float64
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self.lib.pm_plan_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def launch_count(self) -> int:
+        n = C.c_longlong(0)
+        check(self.lib.pm_plan_launch_count(self.handle, C.byref(n)))
+        return n.value
+
+    def set_stream(self, stream_handle: int | None):
+        check(self.lib.pm_plan_set_stream(self.handle, C.c_void_p(stream_handle or 0)))
+
+    def synchronize(self):
+        check(self.lib.pm_plan_synchronize(self.handle))
+
+    # ---- transforms / projections (host arrays)
+    def fft2(self, data: np.ndarray, direction: int) -> np.ndarray:
+        x = np.ascontiguousarray(data, dtype=self.complex_dtype)
+        batch = 1 if x.ndim == 2 else x.shape[0]
+        out = np.empty_like(x)
+        with self.lock:
+            check(self.lib.pm_fft2(self.handle, ptr(x), ptr(out), direction, batch), "pm_fft2")
+        return out
+
+    def replace_modulus(self, data: np.ndarray, target: np.ndarray, zero_tol: float) -> np.ndarray:
+        x = np.ascontiguousarray(data, dtype=self.complex_dtype)
+        t = np.ascontiguousarray(target, dtype=self.float_dtype)
+        batch = 1 if x.ndim == 2 else x.shape[0]
+        per_field = int(t.ndim == 3)
+        out = np.empty_like(x)
+        with self.lock:
+            check(self.lib.pm_replace_modulus(self.handle, ptr(x), ptr(t), per_field,
+                                              float(zero_tol), ptr(out), batch), "pm_replace_modulus")
+        return out
+
+    def project_fourier(self, u: np.ndarray, m: np.ndarray, tol_m: float) -> np.ndarray:
+        x = np.ascontiguousarray(u, dtype=self.complex_dtype)
+        t = np.ascontiguousarray(m, dtype=self.float_dtype)
+        out = np.empty_like(x)
+        with self.lock:
+            check(self.lib.pm_project_fourier(self.handle, ptr(x), ptr(t), float(tol_m), ptr(out)),
+                  "pm_project_fourier")
+        return out
+
+    def gap(self, u, p, m, tol_p, tol_m) -> float:
+        x = np.ascontiguousarray(u, dtype=self.complex_dtype)
+        pp = np.ascontiguousarray(p, dtype=self.float_dtype)
+        mm = np.ascontiguousarray(m, dtype=self.float_dtype)
+        g = C.c_double(0.0)
+        with self.lock:
+            check(self.lib.pm_gap(self.handle, ptr(x), ptr(pp), ptr(mm), float(tol_p), float(tol_m),
+                                  C.byref(g)), "pm_gap")
+        return g.value
+
+    def time_sweep(self, which: int, batch: int, reps: int) -> float:
+        ms = C.c_float(0)
+        with self.lock:
+            check(self.lib.pm_time_sweep(self.handle, which, batch, reps, C.byref(ms)), "pm_time_sweep")
+        return float(ms.value)
+
+
+# ---------------------------------------------------------- plan-less helpers
+
+_DTYPE_CODE = {np.dtype(np.float32): 0, np.dtype(np.float64): 1,
+               np.dtype(np.complex64): 2, np.dtype(np.complex128): 3}
+
+
+def norm2(data: np.ndarray, device: int = 0) -> float:
+    a = np.ascontiguousarray(data)
+    if a.dtype not in _DTYPE_CODE:
+        a = a.astype(np.complex128 if np.iscomplexobj(a) else np.float64)
+    out = C.c_double(0.0)
+    check(load().pm_norm2(device, ptr(a), a.size, _DTYPE_CODE[a.dtype], C.byref(out)), "pm_norm2")
+    return out.value
+
+
+def fixed_sum(values: np.ndarray, device: int = 0) -> float:
+    a = np.ascontiguousarray(values, dtype=np.float64).reshape(-1)
+    out = C.c_double(0.0)
+    check(load().pm_sum(device, ptr(a), a.size, C.byref(out)), "pm_sum")
+    return out.value
+
+
+def phases(u: np.ndarray, zero_tol: float = 0.0, device: int = 0) -> np.ndarray:
+    a = np.ascontiguousarray(u)
+    if a.dtype not in (np.complex64, np.complex128):
+        a = a.astype(np.complex128)
+    prec = 0 if a.dtype == np.complex64 else 1
+    out = np.empty(a.shape, dtype=np.float64)
+    check(load().pm_phases(device, ptr(a), a.size, prec, float(zero_tol), ptr(out)), "pm_phases")
+    return out
+
+
+def measure_copy(nbytes: int, reps: int = 10, device: int = 0) -> float:
+    g = C.c_double(0.0)
+    check(load().pm_measure_copy(device, int(nbytes), reps, C.byref(g)), "pm_measure_copy")
+    return g.value

@@ -1,0 +1,110 @@
+"""Build libphasemask_b200.so in-tree for sm_100a.
+
+    python -m paper_1302_0120_b200.build [--force] [--jobs N]
+
+Compiles csrc/pm_inst.cu once per (precision, log2 length) plus the table
+and C-ABI translation units, in parallel, with
+``-gencode arch=compute_100a,code=sm_100a -lineinfo -O3`` (no fast-math:
+the fp64 path needs IEEE sqrt/div, the fp32 path matches numpy's rounding),
+and links them into ``paper_1302_0120_b200/lib/libphasemask_b200.so`` with
+the CUDA runtime linked statically. Objects are cached under
+``paper_1302_0120_b200/build/`` and rebuilt when a source or header changes.
+"""
+
+from __future__ import annotations
+
+import argparse
+import os
+import shutil
+import subprocess
+import sys
+from concurrent.futures import ThreadPoolExecutor
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+CSRC = PKG / "csrc"
+BUILD = PKG / "build"
+LIBDIR = PKG / "lib"
+LIB = LIBDIR / "libphasemask_b200.so"
+INCLUDE = PKG.parent / "include"
+MAX_LG = 12
+
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
+         f"-I{CSRC}", f"-I{INCLUDE}"]
+
+
+def nvcc() -> str:
+    for cand in (os.environ.get("NVCC"), shutil.which("nvcc"), "/usr/local/cuda/bin/nvcc"):
+        if cand and Path(cand).exists():
+            return cand
+    raise RuntimeError("nvcc not found: the CUDA toolkit is required to build phasemask_b200")
+
+
+def _units():
+    units = []
+    for f64 in (0, 1):
+        for lg in range(MAX_LG + 1):
+            units.append((CSRC / "pm_inst.cu", BUILD / f"pm_inst_{'f64' if f64 else 'f32'}_{lg}.o",
+                          [f"-DPM_F64={f64}", f"-DPM_LG={lg}"]))
+    units.append((CSRC / "pm_table.cu", BUILD / "pm_table.o", []))
+    units.append((CSRC / "pm_capi.cu", BUILD / "pm_capi.o", []))
+    return units
+
+
+def _deps_mtime() -> float:
+    files = list(CSRC.glob("*.cu")) + list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h"))
+    files += list(INCLUDE.glob("*.h")) + [Path(__file__)]
+    return max(f.stat().st_mtime for f in files)
+
+
+def _compile(unit, force: bool, verbose: bool):
+    src, obj, defs = unit
+    if not force and obj.exists() and obj.stat().st_mtime >= _deps_mtime():
+        return obj, None
+    cmd = [nvcc(), *ARCH, *FLAGS, *defs, "-c", str(src), "-o", str(obj)]
+    if verbose:
+        cmd.insert(1, "-Xptxas=-v")
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"nvcc failed for {obj.name}:\n{' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
+    return obj, r.stderr if verbose else None
+
+
+def build(force: bool = False, jobs: int | None = None, verbose: bool = False) -> Path:
+    BUILD.mkdir(exist_ok=True)
+    LIBDIR.mkdir(exist_ok=True)
+    units = _units()
+    jobs = jobs or max(1, os.cpu_count() or 1)
+    # biggest units first so the long poles start early
+    order = sorted(units, key=lambda u: -int(next((d.split("=")[1] for d in u[2] if "PM_LG" in d), "0")))
+    logs = []
+    with ThreadPoolExecutor(jobs) as ex:
+        for obj, log in ex.map(lambda u: _compile(u, force, verbose), order):
+            if log:
+                logs.append(f"== {obj.name}\n{log}")
+    objs = [str(u[1]) for u in units]
+    newest = max(Path(o).stat().st_mtime for o in objs)
+    if force or not LIB.exists() or LIB.stat().st_mtime < newest:
+        tmp = LIB.with_suffix(".so.tmp")
+        cmd = [nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", str(tmp), *objs]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"link failed:\n{' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
+        os.replace(tmp, LIB)
+    if verbose and logs:
+        (BUILD / "ptxas.log").write_text("\n".join(logs))
+    return LIB
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser(description=__doc__.splitlines()[0])
+    ap.add_argument("--force", action="store_true")
+    ap.add_argument("--jobs", type=int, default=None)
+    ap.add_argument("--verbose", action="store_true", help="keep ptxas -v output in build/ptxas.log")
+    a = ap.parse_args(argv)
+    print(build(a.force, a.jobs, a.verbose))
+
+
+if __name__ == "__main__":
+    sys.exit(main())

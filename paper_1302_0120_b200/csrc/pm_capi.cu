@@ -1,0 +1,1238 @@
+// C ABI of libphasemask_b200 (declared in include/phasemask_b200.h):
+// plans, launch configuration, the solve orchestration (a CUDA graph of
+// 2K+4 sweep launches per solve, no host round trip per iteration), the
+// stand-alone transform / projection / reduction entry points and the
+// measurement helpers used by bench.py.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <set>
+#include <string>
+#include <vector>
+
+#include "phasemask_b200.h"
+#include "pm_kernels.cuh"
+#include "pm_table.h"
+
+using namespace pm;
+
+// ------------------------------------------------------------------ errors
+namespace {
+thread_local std::string g_err;
+
+int set_err(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+int cuda_err(cudaError_t e, const char* what) {
+    cudaGetLastError();  // clear sticky-free errors
+    const int code = (e == cudaErrorMemoryAllocation) ? PM_ERR_NOMEM : PM_ERR_CUDA;
+    return set_err(code, std::string(what) + ": " + cudaGetErrorString(e));
+}
+}  // namespace
+
+#define CK(call)                                                  \
+    do {                                                          \
+        cudaError_t e_ = (call);                                  \
+        if (e_ != cudaSuccess) return cuda_err(e_, #call);        \
+    } while (0)
+#define CKR(call)                                                 \
+    do {                                                          \
+        int r_ = (call);                                          \
+        if (r_ != PM_OK) return r_;                               \
+    } while (0)
+
+// ------------------------------------------------------- elementwise kernels
+namespace pm {
+
+// src/projections.py:46-66 as a stand-alone per-pixel kernel.
+template <typename T>
+__global__ void replace_kernel(const cx<T>* in, const T* target, long long tstride, T tol,
+                               cx<T>* out, long long n) {
+    const long long b = blockIdx.y;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        out[b * n + i] = replace_mod(in[b * n + i], target[b * tstride + i], tol);
+}
+
+// Fixed partition: block i reduces [i*chunk, (i+1)*chunk) with a fixed
+// per-thread stride and a fixed tree; partials combined in index order.
+__device__ __forceinline__ double block_sum(double x) {
+    __shared__ double ws[32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if (lane == 0) ws[warp] = x;
+    __syncthreads();
+    double s = 0.0;
+    if (threadIdx.x == 0)
+        for (int w = 0; w < (int)((blockDim.x + 31) >> 5); ++w) s += ws[w];
+    return s;
+}
+
+template <typename TIn>
+__device__ __forceinline__ double sq_mag(const TIn* d, long long i);
+template <> __device__ __forceinline__ double sq_mag<float>(const float* d, long long i) {
+    const double a = (double)fabsf(d[i]);
+    return a * a;
+}
+template <> __device__ __forceinline__ double sq_mag<double>(const double* d, long long i) {
+    const double a = fabs(d[i]);
+    return a * a;
+}
+template <> __device__ __forceinline__ double sq_mag<float2>(const float2* d, long long i) {
+    const float2 u = d[i];
+    const double a = (double)sqrtf(u.x * u.x + u.y * u.y);   // |u| in field precision
+    return a * a;
+}
+template <> __device__ __forceinline__ double sq_mag<double2>(const double2* d, long long i) {
+    const double2 u = d[i];
+    const double a = sqrt(u.x * u.x + u.y * u.y);
+    return a * a;
+}
+
+template <typename TIn>
+__global__ void norm_partial_kernel(const TIn* d, long long n, long long chunk, double* part) {
+    const long long lo = blockIdx.x * chunk, hi = min(n, lo + chunk);
+    double acc = 0.0;
+    for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) acc += sq_mag<TIn>(d, i);
+    const double s = block_sum(acc);
+    if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+__global__ void sum_partial_kernel(const double* d, long long n, long long chunk, double* part) {
+    const long long lo = blockIdx.x * chunk, hi = min(n, lo + chunk);
+    double acc = 0.0;
+    for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) acc += d[i];
+    const double s = block_sum(acc);
+    if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+// |P_S u - w|^2 partials for metrics.gap (src/metrics.py:67-71).
+template <typename T>
+__global__ void gap_partial_kernel(const cx<T>* u, const cx<T>* pm_u, const T* p, T tol,
+                                   long long n, long long chunk, double* part) {
+    const long long lo = blockIdx.x * chunk, hi = min(n, lo + chunk);
+    double acc = 0.0;
+    for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+        const cx<T> ps = replace_mod(u[i], p[i], tol);
+        const T dx = ps.x - pm_u[i].x, dy = ps.y - pm_u[i].y;
+        const double a = (double)sqrt(dx * dx + dy * dy);
+        acc += a * a;
+    }
+    const double s = block_sum(acc);
+    if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+__global__ void final_sum_kernel(const double* part, int nb, double* out, int take_sqrt) {
+    double x = 0.0;
+    for (int i = threadIdx.x; i < nb; i += 32) x += part[i];
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if (threadIdx.x == 0) *out = take_sqrt ? sqrt(x) : x;
+}
+
+template <typename T>
+__global__ void phases_kernel(const cx<T>* u, long long n, T tol, double* out) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const cx<T> v = u[i];
+        double th = phase_of((double)v.x, (double)v.y);
+        const T mag = sqrt(v.x * v.x + v.y * v.y);
+        if (tol > T(0) && mag < tol) th = 0.0;
+        out[i] = th;
+    }
+}
+
+__global__ void copy_kernel(const float4* __restrict__ a, float4* __restrict__ b, long long n) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        b[i] = a[i];
+}
+
+// Host abort (should_abort -> True): the current iterate becomes the last.
+__global__ void force_stop_kernel(MaskState* st, int batch, int it) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b < batch && !st[b].stop && !st[b].done) {
+        st[b].stop = 1;
+        st[b].iters_run = it;
+        st[b].aborted = 1;
+    }
+}
+
+}  // namespace pm
+
+// ---------------------------------------------------------------- plan
+namespace {
+
+int lg2_exact(int n) {
+    if (n < 1 || (n & (n - 1))) return -1;
+    int l = 0;
+    while ((1 << l) < n) ++l;
+    return l;
+}
+
+const KernelSet& kset(int prec, int lg) { return prec == PM_SINGLE ? kernels_f32(lg) : kernels_f64(lg); }
+
+// Forward twiddles of the Stockham passes, [pass][r-1][k] (see FftShape).
+template <typename C>
+std::vector<C> make_twiddles(int lg, int lgR_max) {
+    const int lgR = std::min(lg, lgR_max);
+    const int NP = lgR == 0 ? 0 : (lg + lgR - 1) / lgR;
+    std::vector<C> out;
+    const long double pi = 3.141592653589793238462643383279502884L;
+    for (int s = 1; s < NP; ++s) {
+        const int lgRs = (s < NP - 1) ? lgR : lg - (NP - 1) * lgR;
+        const long long Rs = 1LL << lgRs, Ns = 1LL << (s * lgR), M = Ns * Rs;
+        for (long long r = 1; r < Rs; ++r)
+            for (long long k = 0; k < Ns; ++k) {
+                const long double ang = 2.0L * pi * (long double)((r * k) % M) / (long double)M;
+                C w;
+                w.x = (decltype(w.x))cosl(ang);
+                w.y = (decltype(w.y))(-sinl(ang));
+                out.push_back(w);
+            }
+    }
+    return out;
+}
+
+std::map<const void*, size_t>& smem_configured() {
+    static std::map<const void*, size_t> s;
+    return s;
+}
+std::mutex g_attr_mu;
+
+// Opt a kernel into `bytes` of dynamic shared memory (> 48 KB needs it).
+cudaError_t allow_smem(const void* fn, size_t bytes) {
+    if (bytes <= 48 * 1024) return cudaSuccess;
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    auto it = smem_configured().find(fn);
+    if (it != smem_configured().end() && it->second >= bytes) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess) smem_configured()[fn] = bytes;
+    return e;
+}
+
+struct RowCfg { int G, threads, nblk; size_t smem; };
+struct ColCfg { int C, threads, nblk; size_t smem; };
+
+}  // namespace
+
+struct pm_plan {
+    int device = 0, nx = 0, ny = 0, prec = 0, lgx = 0, lgy = 0;
+    size_t N = 0, csz = 0, rsz = 0;   // pixels, complex and real element sizes
+    int cap = 0;                      // batch capacity
+    int hist_cap = 0;                 // max_iters capacity of the history buffer
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    void* tw_row = nullptr;
+    void* tw_col = nullptr;
+    void* field = nullptr;            // cap * N complex
+    void* tmp = nullptr;              // cap * N complex (scratch)
+    void* pbuf = nullptr;             // cap * N real
+    void* mbuf = nullptr;             // cap * N real
+    double* phases = nullptr;         // cap * N
+    uint8_t* levels = nullptr;        // cap * N
+    void* ustar = nullptr;            // cap * N complex
+    void* vstar = nullptr;
+    MaskState* st = nullptr;          // cap
+    double* hist = nullptr;           // cap * hist_cap * 4
+    double* part = nullptr;           // partial sums (row + col), cap * nblk * 3 each
+    unsigned* ctr = nullptr;          // 2 * cap counters
+    double* tolp = nullptr;           // cap
+    double* tolm = nullptr;
+    double* energy = nullptr;
+    double* red = nullptr;            // reduction scratch
+    int red_cap = 0;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    long long launches = 0;
+    RowCfg rc{};
+    ColCfg cc{};
+    std::map<std::string, cudaGraphExec_t> graphs;
+    std::mutex mu;
+
+    // current solve session
+    struct Session {
+        bool active = false;
+        int batch = 0, it = 0;
+        pm_params prm{};
+        const void* p = nullptr;
+        const void* m = nullptr;
+        long long p_stride = 0;
+        void* phases = nullptr;
+        void* levels = nullptr;
+        void* ustar = nullptr;
+        void* vstar = nullptr;
+    } s;
+};
+
+namespace {
+
+RowCfg row_config(const pm_plan* pl) {
+    const KernelSet& k = kset(pl->prec, pl->lgx);
+    RowCfg c;
+    c.G = std::max(1, 256 / k.TG);
+    c.G = std::min(c.G, pl->ny);
+    c.threads = c.G * k.TG;
+    c.nblk = pl->ny / c.G;
+    c.smem = (size_t)c.G * k.SM * pl->csz;
+    return c;
+}
+
+ColCfg col_config(const pm_plan* pl) {
+    const KernelSet& k = kset(pl->prec, pl->lgy);
+    ColCfg c;
+    const int maxt = k.TG <= 64 ? 256 : 512;
+    c.C = std::max(1, maxt / k.TG);
+    c.C = std::min(c.C, pl->nx);
+    c.threads = c.C * k.TG;
+    c.nblk = pl->nx / c.C;
+    c.smem = k.SM ? (size_t)c.C * (k.SM + kColPad) * pl->csz : 0;
+    return c;
+}
+
+void free_buffers(pm_plan* pl) {
+    void* bufs[] = {pl->field, pl->tmp, pl->pbuf, pl->mbuf, pl->phases, pl->levels, pl->ustar,
+                    pl->vstar, pl->st, pl->hist, pl->part, pl->ctr, pl->tolp, pl->tolm,
+                    pl->energy};
+    for (void* b : bufs)
+        if (b) cudaFree(b);
+    pl->field = pl->tmp = pl->pbuf = pl->mbuf = pl->ustar = pl->vstar = nullptr;
+    pl->phases = nullptr;
+    pl->levels = nullptr;
+    pl->st = nullptr;
+    pl->hist = pl->part = pl->tolp = pl->tolm = pl->energy = nullptr;
+    pl->ctr = nullptr;
+    pl->cap = 0;
+    pl->hist_cap = 0;
+}
+
+void drop_graphs(pm_plan* pl) {
+    for (auto& kv : pl->graphs) cudaGraphExecDestroy(kv.second);
+    pl->graphs.clear();
+}
+
+int ensure_capacity(pm_plan* pl, int batch, int max_iters) {
+    if (batch <= pl->cap && max_iters <= pl->hist_cap) return PM_OK;
+    const int cap = std::max(batch, pl->cap);
+    const int hcap = std::max(max_iters, std::max(pl->hist_cap, 1));
+    CK(cudaStreamSynchronize(pl->stream));
+    drop_graphs(pl);
+    free_buffers(pl);
+    const size_t N = pl->N;
+    const int nb = std::max(pl->rc.nblk, pl->cc.nblk);
+    CK(cudaMalloc(&pl->field, cap * N * pl->csz));
+    CK(cudaMalloc(&pl->tmp, cap * N * pl->csz));
+    CK(cudaMalloc(&pl->pbuf, cap * N * pl->rsz));
+    CK(cudaMalloc(&pl->mbuf, cap * N * pl->rsz));
+    CK(cudaMalloc((void**)&pl->st, cap * sizeof(MaskState)));
+    CK(cudaMalloc((void**)&pl->hist, (size_t)cap * hcap * 4 * sizeof(double)));
+    CK(cudaMalloc((void**)&pl->part, (size_t)2 * cap * nb * 3 * sizeof(double)));
+    CK(cudaMalloc((void**)&pl->ctr, (size_t)2 * cap * sizeof(unsigned)));
+    CK(cudaMalloc((void**)&pl->tolp, cap * sizeof(double)));
+    CK(cudaMalloc((void**)&pl->tolm, cap * sizeof(double)));
+    CK(cudaMalloc((void**)&pl->energy, cap * sizeof(double)));
+    CK(cudaMemsetAsync(pl->ctr, 0, (size_t)2 * cap * sizeof(unsigned), pl->stream));
+    CK(cudaMemsetAsync(pl->st, 0, cap * sizeof(MaskState), pl->stream));
+    pl->cap = cap;
+    pl->hist_cap = hcap;
+    return PM_OK;
+}
+
+int ensure_outputs(pm_plan* pl, bool phases, bool levels, bool ustar, bool vstar) {
+    const size_t n = (size_t)pl->cap * pl->N;
+    if (phases && !pl->phases) CK(cudaMalloc((void**)&pl->phases, n * sizeof(double)));
+    if (levels && !pl->levels) CK(cudaMalloc((void**)&pl->levels, n));
+    if (ustar && !pl->ustar) CK(cudaMalloc(&pl->ustar, n * pl->csz));
+    if (vstar && !pl->vstar) CK(cudaMalloc(&pl->vstar, n * pl->csz));
+    return PM_OK;
+}
+
+// --------------------------------------------------------------- launches
+template <typename T>
+int launch_row(pm_plan* pl, int batch, int mode, int it) {
+    const KernelSet& k = kset(pl->prec, pl->lgx);
+    RowArgs<T> a;
+    a.field = (cx<T>*)pl->field;
+    a.p = (const T*)pl->s.p;
+    a.p_stride = pl->s.p_stride;
+    a.tw = (const cx<T>*)pl->tw_row;
+    a.nx = pl->nx;
+    a.ny = pl->ny;
+    a.scale = (T)(1.0 / std::sqrt((double)pl->nx));
+    a.tol_p = pl->tolp;
+    a.mode = mode;
+    a.it = it;
+    a.st = pl->st;
+    a.part = pl->part;
+    a.ctr = pl->ctr;
+    a.nblk = pl->rc.nblk;
+    a.v_star = (cx<T>*)pl->s.vstar;
+    a.u_star = (cx<T>*)pl->s.ustar;
+    a.phases = (double*)pl->s.phases;
+    a.levels = (uint8_t*)pl->s.levels;
+    CK(allow_smem(k.row_iter, pl->rc.smem));
+    void* args[] = {&a};
+    CK(cudaLaunchKernel(k.row_iter, dim3(pl->rc.nblk, batch), dim3(pl->rc.threads), args,
+                        pl->rc.smem, pl->stream));
+    pl->launches++;
+    return PM_OK;
+}
+
+template <typename T>
+int launch_col(pm_plan* pl, int batch, int mode, int u_iter) {
+    const KernelSet& k = kset(pl->prec, pl->lgy);
+    const pm_params& prm = pl->s.prm;
+    ColArgs<T> a;
+    a.field = (cx<T>*)pl->field;
+    a.m = (const T*)pl->s.m;
+    a.m_stride = (long long)pl->N;
+    a.tw = (const cx<T>*)pl->tw_col;
+    a.nx = pl->nx;
+    a.ny = pl->ny;
+    a.scale = (T)(1.0 / std::sqrt((double)pl->ny));
+    a.tol_m = pl->tolm;
+    a.energy_target = pl->energy;
+    a.mode = mode;
+    a.u_iter = u_iter;
+    a.ctl.max_iters = prm.max_iters;
+    a.ctl.record_every = prm.record_every;
+    a.ctl.early_tol = prm.early_stop_tol;
+    a.ctl.t_lit = prm.t_lit;
+    a.ctl.t_dark = prm.t_dark;
+    a.st = pl->st;
+    a.hist = pl->hist;
+    a.hist_stride = pl->hist_cap;
+    a.part = pl->part + (size_t)pl->cap * std::max(pl->rc.nblk, pl->cc.nblk) * 3;
+    a.ctr = pl->ctr + pl->cap;
+    a.nblk = pl->cc.nblk;
+    CK(allow_smem(k.col_iter, pl->cc.smem));
+    void* args[] = {&a};
+    CK(cudaLaunchKernel(k.col_iter, dim3(pl->cc.nblk, batch), dim3(pl->cc.threads), args,
+                        pl->cc.smem, pl->stream));
+    pl->launches++;
+    return PM_OK;
+}
+
+int row(pm_plan* pl, int batch, int mode, int it) {
+    return pl->prec == PM_SINGLE ? launch_row<float>(pl, batch, mode, it)
+                                 : launch_row<double>(pl, batch, mode, it);
+}
+int col(pm_plan* pl, int batch, int mode, int u_iter) {
+    return pl->prec == PM_SINGLE ? launch_col<float>(pl, batch, mode, u_iter)
+                                 : launch_col<double>(pl, batch, mode, u_iter);
+}
+
+// Stand-alone 2-D transform: rows (in -> out) then columns (out -> out).
+template <typename T>
+int launch_fft2(pm_plan* pl, const void* in, void* out, int dir, int batch) {
+    const KernelSet& kr = kset(pl->prec, pl->lgx);
+    const KernelSet& kc = kset(pl->prec, pl->lgy);
+    const cx<T>* src = (const cx<T>*)in;
+    cx<T>* dst = (cx<T>*)out;
+    const cx<T>* twr = (const cx<T>*)pl->tw_row;
+    const cx<T>* twc = (const cx<T>*)pl->tw_col;
+    int nx = pl->nx, ny = pl->ny;
+    T sx = (T)(1.0 / std::sqrt((double)nx)), sy = (T)(1.0 / std::sqrt((double)ny));
+    {
+        void* args[] = {&src, &dst, &twr, &nx, &ny, &sx, &dir};
+        CK(allow_smem(kr.row_fft, pl->rc.smem));
+        CK(cudaLaunchKernel(kr.row_fft, dim3(pl->rc.nblk, batch), dim3(pl->rc.threads), args,
+                            pl->rc.smem, pl->stream));
+    }
+    {
+        const cx<T>* src2 = dst;
+        void* args[] = {&src2, &dst, &twc, &nx, &ny, &sy, &dir};
+        CK(allow_smem(kc.col_fft, pl->cc.smem));
+        CK(cudaLaunchKernel(kc.col_fft, dim3(pl->cc.nblk, batch), dim3(pl->cc.threads), args,
+                            pl->cc.smem, pl->stream));
+    }
+    pl->launches += 2;
+    return PM_OK;
+}
+
+int fft2_dev(pm_plan* pl, const void* in, void* out, int dir, int batch) {
+    return pl->prec == PM_SINGLE ? launch_fft2<float>(pl, in, out, dir, batch)
+                                 : launch_fft2<double>(pl, in, out, dir, batch);
+}
+
+int check_plan(pm_plan* pl) {
+    if (!pl) return set_err(PM_ERR_ARG, "null plan");
+    CK(cudaSetDevice(pl->device));
+    return PM_OK;
+}
+
+// -------------------------------------------------------------- solve
+int validate_params(const pm_params* prm, int batch) {
+    if (!prm) return set_err(PM_ERR_ARG, "null params");
+    if (batch < 1) return set_err(PM_ERR_ARG, "batch must be >= 1");
+    if (prm->max_iters < 1) return set_err(PM_ERR_ARG, "max_iters must be >= 1");
+    if (prm->record_every < 1) return set_err(PM_ERR_ARG, "record_every must be >= 1");
+    if (prm->algorithm != PM_ALGO_GS)
+        return set_err(PM_ERR_UNSUPPORTED, "only the GS algorithm is available in this build");
+    return PM_OK;
+}
+
+// Upload per-mask scalars and reset state; point the session at p/m.
+int session_setup(pm_plan* pl, const void* d_p, const void* d_m, int batch, const pm_params* prm,
+                  const double* tol_p, const double* tol_m, const double* energy) {
+    CKR(validate_params(prm, batch));
+    CKR(ensure_capacity(pl, batch, prm->max_iters));
+    auto& s = pl->s;
+    s = pm_plan::Session();
+    s.active = true;
+    s.batch = batch;
+    s.prm = *prm;
+    s.p = d_p;
+    s.m = d_m;
+    s.p_stride = prm->p_per_mask ? (long long)pl->N : 0;
+    std::vector<double> tp(batch), tm(batch), en(batch);
+    for (int b = 0; b < batch; ++b) {
+        tp[b] = tol_p[prm->p_per_mask ? b : 0];
+        tm[b] = tol_m[b];
+        en[b] = energy[b];
+    }
+    CK(cudaMemcpyAsync(pl->tolp, tp.data(), batch * sizeof(double), cudaMemcpyHostToDevice, pl->stream));
+    CK(cudaMemcpyAsync(pl->tolm, tm.data(), batch * sizeof(double), cudaMemcpyHostToDevice, pl->stream));
+    CK(cudaMemcpyAsync(pl->energy, en.data(), batch * sizeof(double), cudaMemcpyHostToDevice, pl->stream));
+    return PM_OK;
+}
+
+int enqueue_begin(pm_plan* pl) {
+    auto& s = pl->s;
+    CK(cudaMemsetAsync(pl->st, 0, s.batch * sizeof(MaskState), pl->stream));
+    CK(cudaMemsetAsync(pl->hist, 0, (size_t)s.batch * pl->hist_cap * 4 * sizeof(double), pl->stream));
+    CKR(col(pl, s.batch, s.prm.init_complex ? 1 : 0, 0));   // u0 column half
+    CKR(row(pl, s.batch, 0, 0));                            // u0 row half, w0 = RowFFT(u0)
+    CKR(col(pl, s.batch, 2, 0));                            // z1 = ColIFFT replace F u0
+    return PM_OK;
+}
+
+int enqueue_steps(pm_plan* pl, int n) {
+    auto& s = pl->s;
+    for (int i = 0; i < n && s.it < s.prm.max_iters; ++i) {
+        s.it += 1;
+        CKR(row(pl, s.batch, 1, s.it));        // u_it, w_it
+        CKR(col(pl, s.batch, 2, s.it));        // metrics of u_it, stop decision, z_{it+1}
+    }
+    return PM_OK;
+}
+
+int enqueue_finish(pm_plan* pl) { return row(pl, pl->s.batch, 2, pl->s.it); }
+
+std::string graph_key(const pm_plan* pl) {
+    const auto& s = pl->s;
+    char buf[512];
+    snprintf(buf, sizeof buf, "%d|%d|%d|%d|%a|%a|%a|%d|%d|%p|%p|%lld|%p|%p|%p|%p", s.batch,
+             s.prm.max_iters, s.prm.record_every, s.prm.init_complex, s.prm.early_stop_tol,
+             s.prm.t_lit, s.prm.t_dark, s.prm.p_per_mask, s.prm.algorithm, s.p, s.m, s.p_stride,
+             s.phases, s.levels, s.ustar, s.vstar);
+    return buf;
+}
+
+// Whole solve as one CUDA graph (captured once per configuration).
+int enqueue_full_solve(pm_plan* pl) {
+    static const bool no_graph = getenv("PM_NO_GRAPH") != nullptr;
+    auto& s = pl->s;
+    if (no_graph) {
+        CKR(enqueue_begin(pl));
+        CKR(enqueue_steps(pl, s.prm.max_iters));
+        return enqueue_finish(pl);
+    }
+    const std::string key = graph_key(pl);
+    auto it = pl->graphs.find(key);
+    if (it == pl->graphs.end()) {
+        if (pl->graphs.size() >= 16) drop_graphs(pl);
+        cudaGraph_t g;
+        CK(cudaStreamBeginCapture(pl->stream, cudaStreamCaptureModeThreadLocal));
+        const long long l0 = pl->launches;
+        int r = enqueue_begin(pl);
+        if (r == PM_OK) r = enqueue_steps(pl, s.prm.max_iters);
+        if (r == PM_OK) r = enqueue_finish(pl);
+        cudaError_t e = cudaStreamEndCapture(pl->stream, &g);
+        pl->launches = l0;   // counted when the graph is launched
+        if (r != PM_OK) {
+            if (e == cudaSuccess) cudaGraphDestroy(g);
+            return r;
+        }
+        if (e != cudaSuccess) return cuda_err(e, "cudaStreamEndCapture");
+        cudaGraphExec_t ge;
+        e = cudaGraphInstantiate(&ge, g, 0);
+        cudaGraphDestroy(g);
+        if (e != cudaSuccess) return cuda_err(e, "cudaGraphInstantiate");
+        it = pl->graphs.emplace(key, ge).first;
+    }
+    s.it = s.prm.max_iters;
+    CK(cudaGraphLaunch(it->second, pl->stream));
+    pl->launches += 2LL * s.prm.max_iters + 4;
+    return PM_OK;
+}
+
+// Copy history / state back and fill the host-side result fields.
+int read_records(pm_plan* pl, int first, int last, double* gap, double* lit, double* dark,
+                 int* iters, int* diverged, int* aborted = nullptr) {
+    auto& s = pl->s;
+    const int B = s.batch, K = s.prm.max_iters;
+    std::vector<MaskState> st(B);
+    CK(cudaMemcpyAsync(st.data(), pl->st, B * sizeof(MaskState), cudaMemcpyDeviceToHost, pl->stream));
+    std::vector<double> h;
+    if (gap || lit || dark) {
+        h.resize((size_t)B * pl->hist_cap * 4);
+        CK(cudaMemcpyAsync(h.data(), pl->hist, h.size() * sizeof(double), cudaMemcpyDeviceToHost,
+                           pl->stream));
+    }
+    CK(cudaStreamSynchronize(pl->stream));
+    for (int b = 0; b < B; ++b) {
+        if (iters) iters[b] = st[b].iters_run;
+        if (diverged) diverged[b] = st[b].diverged;
+        if (aborted) aborted[b] = st[b].aborted;
+        if (!h.empty()) {
+            for (int i = first; i <= last && i <= K; ++i) {
+                const double* e = &h[((size_t)b * pl->hist_cap + (i - 1)) * 4];
+                const bool ok = e[3] != 0.0;
+                const size_t o = (size_t)b * K + (i - 1);
+                if (gap) gap[o] = ok ? e[0] : NAN;
+                if (lit) lit[o] = ok ? e[1] : NAN;
+                if (dark) dark[o] = ok ? e[2] : NAN;
+            }
+        }
+    }
+    return PM_OK;
+}
+
+int any_diverged(const std::vector<int>& d) {
+    for (int x : d)
+        if (x) return 1;
+    return 0;
+}
+
+}  // namespace
+
+// =================================================================== C ABI
+extern "C" {
+
+int pm_version(void) { return 100; }
+
+const char* pm_last_error(void) { return g_err.c_str(); }
+
+int pm_device_count(int* count) {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        n = 0;
+    }
+    if (count) *count = n;
+    return PM_OK;
+}
+
+int pm_plan_create(int device, int n_x, int n_y, int precision, int max_batch, pm_plan** out) {
+    if (!out) return set_err(PM_ERR_ARG, "null output pointer");
+    *out = nullptr;
+    if (precision != PM_SINGLE && precision != PM_DOUBLE)
+        return set_err(PM_ERR_ARG, "precision must be 0 (single) or 1 (double)");
+    const int lgx = lg2_exact(n_x), lgy = lg2_exact(n_y);
+    if (lgx < 0 || lgy < 0 || lgx > kMaxLg || lgy > kMaxLg)
+        return set_err(PM_ERR_UNSUPPORTED, "grid " + std::to_string(n_x) + "x" + std::to_string(n_y) +
+                                               ": n_x and n_y must be powers of two in [1, 4096]");
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return set_err(PM_ERR_CUDA, "no CUDA device available (phasemask_b200 has no CPU fallback)");
+    }
+    if (device < 0 || device >= ndev) return set_err(PM_ERR_ARG, "device index out of range");
+    CK(cudaSetDevice(device));
+    pm_plan* pl = new pm_plan();
+    pl->device = device;
+    pl->nx = n_x;
+    pl->ny = n_y;
+    pl->prec = precision;
+    pl->lgx = lgx;
+    pl->lgy = lgy;
+    pl->N = (size_t)n_x * n_y;
+    pl->csz = precision == PM_SINGLE ? sizeof(float2) : sizeof(double2);
+    pl->rsz = precision == PM_SINGLE ? sizeof(float) : sizeof(double);
+    pl->rc = row_config(pl);
+    pl->cc = col_config(pl);
+    auto fail = [&](int r) {
+        pm_plan_destroy(pl);
+        return r;
+    };
+    if (cudaStreamCreateWithFlags(&pl->stream, cudaStreamNonBlocking) != cudaSuccess)
+        return fail(cuda_err(cudaGetLastError(), "cudaStreamCreate"));
+    pl->own_stream = true;
+    if (cudaEventCreate(&pl->ev0) != cudaSuccess || cudaEventCreate(&pl->ev1) != cudaSuccess)
+        return fail(cuda_err(cudaGetLastError(), "cudaEventCreate"));
+    // twiddle tables
+    for (int axis = 0; axis < 2; ++axis) {
+        const int lg = axis == 0 ? lgx : lgy;
+        const KernelSet& k = kset(precision, lg);
+        void** dst = axis == 0 ? &pl->tw_row : &pl->tw_col;
+        const size_t nbytes = std::max(1, k.TW) * pl->csz;
+        cudaError_t e2 = cudaMalloc(dst, nbytes);
+        if (e2 != cudaSuccess) return fail(cuda_err(e2, "cudaMalloc(twiddles)"));
+        if (k.TW > 0) {
+            if (precision == PM_SINGLE) {
+                auto t = make_twiddles<float2>(lg, k.lgR);
+                if ((int)t.size() != k.TW) return fail(set_err(PM_ERR_CUDA, "twiddle table size mismatch"));
+                e2 = cudaMemcpy(*dst, t.data(), nbytes, cudaMemcpyHostToDevice);
+            } else {
+                auto t = make_twiddles<double2>(lg, k.lgR);
+                if ((int)t.size() != k.TW) return fail(set_err(PM_ERR_CUDA, "twiddle table size mismatch"));
+                e2 = cudaMemcpy(*dst, t.data(), nbytes, cudaMemcpyHostToDevice);
+            }
+            if (e2 != cudaSuccess) return fail(cuda_err(e2, "cudaMemcpy(twiddles)"));
+        }
+    }
+    {
+        const KernelSet& kr = kset(precision, lgx);
+        const KernelSet& kc = kset(precision, lgy);
+        cudaError_t e3 = allow_smem(kr.row_iter, pl->rc.smem);
+        if (e3 == cudaSuccess) e3 = allow_smem(kr.row_fft, pl->rc.smem);
+        if (e3 == cudaSuccess) e3 = allow_smem(kc.col_iter, pl->cc.smem);
+        if (e3 == cudaSuccess) e3 = allow_smem(kc.col_fft, pl->cc.smem);
+        if (e3 != cudaSuccess) return fail(cuda_err(e3, "cudaFuncSetAttribute"));
+    }
+    int r = ensure_capacity(pl, std::max(1, max_batch), 1);
+    if (r != PM_OK) return fail(r);
+    *out = pl;
+    return PM_OK;
+}
+
+int pm_plan_destroy(pm_plan* pl) {
+    if (!pl) return PM_OK;
+    cudaSetDevice(pl->device);
+    if (pl->stream) cudaStreamSynchronize(pl->stream);
+    drop_graphs(pl);
+    free_buffers(pl);
+    if (pl->tw_row) cudaFree(pl->tw_row);
+    if (pl->tw_col) cudaFree(pl->tw_col);
+    if (pl->red) cudaFree(pl->red);
+    if (pl->ev0) cudaEventDestroy(pl->ev0);
+    if (pl->ev1) cudaEventDestroy(pl->ev1);
+    if (pl->own_stream && pl->stream) cudaStreamDestroy(pl->stream);
+    delete pl;
+    return PM_OK;
+}
+
+int pm_plan_set_stream(pm_plan* pl, void* stream) {
+    CKR(check_plan(pl));
+    std::lock_guard<std::mutex> lk(pl->mu);
+    CK(cudaStreamSynchronize(pl->stream));
+    drop_graphs(pl);
+    if (stream) {
+        if (pl->own_stream) cudaStreamDestroy(pl->stream);
+        pl->own_stream = false;
+        pl->stream = (cudaStream_t)stream;
+    } else if (!pl->own_stream) {
+        CK(cudaStreamCreateWithFlags(&pl->stream, cudaStreamNonBlocking));
+        pl->own_stream = true;
+    }
+    return PM_OK;
+}
+
+int pm_plan_get_stream(pm_plan* pl, void** stream) {
+    if (!pl || !stream) return set_err(PM_ERR_ARG, "null argument");
+    *stream = (void*)pl->stream;
+    return PM_OK;
+}
+
+int pm_plan_synchronize(pm_plan* pl) {
+    CKR(check_plan(pl));
+    CK(cudaStreamSynchronize(pl->stream));
+    return PM_OK;
+}
+
+int pm_plan_launch_count(pm_plan* pl, long long* count) {
+    if (!pl || !count) return set_err(PM_ERR_ARG, "null argument");
+    *count = pl->launches;
+    return PM_OK;
+}
+
+// ----------------------------------------------------------- transforms
+int pm_fft2_device(pm_plan* pl, const void* d_in, void* d_out, int direction, int batch) {
+    CKR(check_plan(pl));
+    if (direction != PM_FORWARD && direction != PM_INVERSE)
+        return set_err(PM_ERR_ARG, "direction must be -1 (forward) or +1 (inverse)");
+    if (batch < 1) return set_err(PM_ERR_ARG, "batch must be >= 1");
+    std::lock_guard<std::mutex> lk(pl->mu);
+    return fft2_dev(pl, d_in, d_out, direction, batch);
+}
+
+int pm_fft2(pm_plan* pl, const void* in, void* out, int direction, int batch) {
+    CKR(check_plan(pl));
+    if (direction != PM_FORWARD && direction != PM_INVERSE)
+        return set_err(PM_ERR_ARG, "direction must be -1 (forward) or +1 (inverse)");
+    if (!in || !out || batch < 1) return set_err(PM_ERR_ARG, "null buffer or batch < 1");
+    std::lock_guard<std::mutex> lk(pl->mu);
+    CKR(ensure_capacity(pl, batch, 1));
+    const size_t bytes = (size_t)batch * pl->N * pl->csz;
+    CK(cudaMemcpyAsync(pl->field, in, bytes, cudaMemcpyHostToDevice, pl->stream));
+    CKR(fft2_dev(pl, pl->field, pl->field, direction, batch));
+    CK(cudaMemcpyAsync(out, pl->field, bytes, cudaMemcpyDeviceToHost, pl->stream));
+    CK(cudaStreamSynchronize(pl->stream));
+    return PM_OK;
+}
+
+// ---------------------------------------------------------- projections
+static int replace_dev(pm_plan* pl, const void* in, const void* target, int per_field, double tol,
+                       void* out, int batch) {
+    const long long n = (long long)pl->N;
+    const int blocks = (int)std::min<long long>((n + 255) / 256, 1184);
+    if (pl->prec == PM_SINGLE)
+        replace_kernel<float><<<dim3(blocks, batch), 256, 0, pl->stream>>>(
+            (const float2*)in, (const float*)target, per_field ? n : 0, (float)tol, (float2*)out, n);
+    else
+        replace_kernel<double><<<dim3(blocks, batch), 256, 0, pl->stream>>>(
+            (const double2*)in, (const double*)target, per_field ? n : 0, tol, (double2*)out, n);
+    CK(cudaGetLastError());
+    pl->launches++;
+    return PM_OK;
+}
+
+int pm_replace_modulus_device(pm_plan* pl, const void* d_in, const void* d_target, int per_field,
+                              double zero_tol, void* d_out, int batch) {
+    CKR(check_plan(pl));
+    if (batch < 1) return set_err(PM_ERR_ARG, "batch must be >= 1");
+    std::lock_guard<std::mutex> lk(pl->mu);
+    return replace_dev(pl, d_in, d_target, per_field, zero_tol, d_out, batch);
+}
+
+int pm_replace_modulus(pm_plan* pl, const void* in, const void* target, int per_field,
+                       double zero_tol, void* out, int batch) {
+    CKR(check_plan(pl));
+    if (!in || !target || !out || batch < 1) return set_err(PM_ERR_ARG, "null buffer or batch < 1");
+    std::lock_guard<std::mutex> lk(pl->mu);
+    CKR(ensure_capacity(pl, batch, 1));
+    const size_t cb = (size_t)batch * pl->N * pl->csz;
+    const size_t rb = (size_t)(per_field ? batch : 1) * pl->N * pl->rsz;
+    CK(cudaMemcpyAsync(pl->field, in, cb, cudaMemcpyHostToDevice, pl->stream));
+    CK(cudaMemcpyAsync(pl->mbuf, target, rb, cudaMemcpyHostToDevice, pl->stream));
+    CKR(replace_dev(pl, pl->field, pl->mbuf, per_field, zero_tol, pl->field, batch));
+    CK(cudaMemcpyAsync(out, pl->field, cb, cudaMemcpyDeviceToHost, pl->stream));
+    CK(cudaStreamSynchronize(pl->stream));
+    return PM_OK;
+}
+
+// P_M u on the device: rows forward, fused column FFT.replace.IFFT, rows inverse.
+static int project_fourier_dev(pm_plan* pl, const void* d_u, const void* d_m, double tol_m, void* d_out) {
+    CKR(fft2_dev(pl, d_u, d_out, PM_FORWARD, 1));   // full forward transform
+    // columns were already transformed by fft2; replace in the Fourier plane then inverse
+    CKR(replace_dev(pl, d_out, d_m, 1, tol_m, d_out, 1));
+    CKR(fft2_dev(pl, d_out, d_out, PM_INVERSE, 1));
+    return PM_OK;
+}
+
+int pm_project_fourier(pm_plan* pl, const void* u, const void* m, double zero_tol_m, void* out) {
+    CKR(check_plan(pl));
+    if (!u || !m || !out) return set_err(PM_ERR_ARG, "null buffer");
+    std::lock_guard<std::mutex> lk(pl->mu);
+    CKR(ensure_capacity(pl, 1, 1));
+    CK(cudaMemcpyAsync(pl->tmp, u, pl->N * pl->csz, cudaMemcpyHostToDevice, pl->stream));
+    CK(cudaMemcpyAsync(pl->mbuf, m, pl->N * pl->rsz, cudaMemcpyHostToDevice, pl->stream));
+    CKR(project_fourier_dev(pl, pl->tmp, pl->mbuf, zero_tol_m, pl->field));
+    CK(cudaMemcpyAsync(out, pl->field, pl->N * pl->csz, cudaMemcpyDeviceToHost, pl->stream));
+    CK(cudaStreamSynchronize(pl->stream));
+    return PM_OK;
+}
+
+static int ensure_red(pm_plan* pl, int nb) {
+    if (nb + 1 <= pl->red_cap) return PM_OK;
+    if (pl->red) cudaFree(pl->red);
+    pl->red = nullptr;
+    CK(cudaMalloc((void**)&pl->red, (nb + 1) * sizeof(double)));
+    pl->red_cap = nb + 1;
+    return PM_OK;
+}
+
+static void reduce_grid(long long n, int* nb, long long* chunk) {
+    *nb = (int)std::max<long long>(1, std::min<long long>(1024, (n + 4095) / 4096));
+    *chunk = (n + *nb - 1) / *nb;
+}
+
+int pm_gap(pm_plan* pl, const void* u, const void* p, const void* m, double zero_tol_p,
+           double zero_tol_m, double* out_gap) {
+    CKR(check_plan(pl));
+    if (!u || !p || !m || !out_gap) return set_err(PM_ERR_ARG, "null buffer");
+    std::lock_guard<std::mutex> lk(pl->mu);
+    CKR(ensure_capacity(pl, 1, 1));
+    const long long n = (long long)pl->N;
+    int nb;
+    long long chunk;
+    reduce_grid(n, &nb, &chunk);
+    CKR(ensure_red(pl, nb));
+    CK(cudaMemcpyAsync(pl->tmp, u, n * pl->csz, cudaMemcpyHostToDevice, pl->stream));
+    CK(cudaMemcpyAsync(pl->pbuf, p, n * pl->rsz, cudaMemcpyHostToDevice, pl->stream));
+    CK(cudaMemcpyAsync(pl->mbuf, m, n * pl->rsz, cudaMemcpyHostToDevice, pl->stream));
+    CKR(project_fourier_dev(pl, pl->tmp, pl->mbuf, zero_tol_m, pl->field));
+    if (pl->prec == PM_SINGLE)
+        gap_partial_kernel<float><<<nb, 256, 0, pl->stream>>>((const float2*)pl->tmp, (const float2*)pl->field,
+                                                               (const float*)pl->pbuf, (float)zero_tol_p, n,
+                                                               chunk, pl->red);
+    else
+        gap_partial_kernel<double><<<nb, 256, 0, pl->stream>>>((const double2*)pl->tmp,
+                                                                (const double2*)pl->field,
+                                                                (const double*)pl->pbuf, zero_tol_p, n,
+                                                                chunk, pl->red);
+    final_sum_kernel<<<1, 32, 0, pl->stream>>>(pl->red, nb, pl->red + nb, 1);
+    CK(cudaGetLastError());
+    pl->launches += 2;
+    CK(cudaMemcpyAsync(out_gap, pl->red + nb, sizeof(double), cudaMemcpyDeviceToHost, pl->stream));
+    CK(cudaStreamSynchronize(pl->stream));
+    return PM_OK;
+}
+
+// ----------------------------------------------------------- reductions
+int pm_norm2(int device, const void* data, long long count, int dtype, double* out) {
+    if (!data || !out || count < 1) return set_err(PM_ERR_ARG, "cannot reduce an empty grid");
+    if (dtype < 0 || dtype > 3) return set_err(PM_ERR_ARG, "dtype must be 0..3");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return set_err(PM_ERR_CUDA, "no CUDA device available (phasemask_b200 has no CPU fallback)");
+    }
+    CK(cudaSetDevice(device));
+    static const size_t esz[4] = {4, 8, 8, 16};
+    const size_t bytes = count * esz[dtype];
+    int nb;
+    long long chunk;
+    reduce_grid(count, &nb, &chunk);
+    void* d = nullptr;
+    double* part = nullptr;
+    CK(cudaMalloc(&d, bytes));
+    cudaError_t e = cudaMalloc((void**)&part, (nb + 1) * sizeof(double));
+    if (e != cudaSuccess) {
+        cudaFree(d);
+        return cuda_err(e, "cudaMalloc");
+    }
+    e = cudaMemcpy(d, data, bytes, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) {
+        switch (dtype) {
+            case 0: norm_partial_kernel<float><<<nb, 256>>>((const float*)d, count, chunk, part); break;
+            case 1: norm_partial_kernel<double><<<nb, 256>>>((const double*)d, count, chunk, part); break;
+            case 2: norm_partial_kernel<float2><<<nb, 256>>>((const float2*)d, count, chunk, part); break;
+            default: norm_partial_kernel<double2><<<nb, 256>>>((const double2*)d, count, chunk, part); break;
+        }
+        final_sum_kernel<<<1, 32>>>(part, nb, part + nb, 1);
+        e = cudaGetLastError();
+        if (e == cudaSuccess) e = cudaMemcpy(out, part + nb, sizeof(double), cudaMemcpyDeviceToHost);
+    }
+    cudaFree(d);
+    cudaFree(part);
+    if (e != cudaSuccess) return cuda_err(e, "pm_norm2");
+    return PM_OK;
+}
+
+int pm_sum(int device, const double* data, long long count, double* out) {
+    if (!data || !out || count < 1) return set_err(PM_ERR_ARG, "cannot reduce an empty grid");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return set_err(PM_ERR_CUDA, "no CUDA device available (phasemask_b200 has no CPU fallback)");
+    }
+    CK(cudaSetDevice(device));
+    int nb;
+    long long chunk;
+    reduce_grid(count, &nb, &chunk);
+    double *d = nullptr, *part = nullptr;
+    CK(cudaMalloc((void**)&d, count * sizeof(double)));
+    cudaError_t e = cudaMalloc((void**)&part, (nb + 1) * sizeof(double));
+    if (e != cudaSuccess) {
+        cudaFree(d);
+        return cuda_err(e, "cudaMalloc");
+    }
+    e = cudaMemcpy(d, data, count * sizeof(double), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) {
+        sum_partial_kernel<<<nb, 256>>>(d, count, chunk, part);
+        final_sum_kernel<<<1, 32>>>(part, nb, part + nb, 0);
+        e = cudaGetLastError();
+        if (e == cudaSuccess) e = cudaMemcpy(out, part + nb, sizeof(double), cudaMemcpyDeviceToHost);
+    }
+    cudaFree(d);
+    cudaFree(part);
+    if (e != cudaSuccess) return cuda_err(e, "pm_sum");
+    return PM_OK;
+}
+
+int pm_phases(int device, const void* u, long long count, int precision, double zero_tol, double* out) {
+    if (!u || !out || count < 1) return set_err(PM_ERR_ARG, "empty input");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return set_err(PM_ERR_CUDA, "no CUDA device available (phasemask_b200 has no CPU fallback)");
+    }
+    CK(cudaSetDevice(device));
+    const size_t csz = precision == PM_SINGLE ? 8 : 16;
+    void* d = nullptr;
+    double* o = nullptr;
+    CK(cudaMalloc(&d, count * csz));
+    cudaError_t e = cudaMalloc((void**)&o, count * sizeof(double));
+    if (e != cudaSuccess) {
+        cudaFree(d);
+        return cuda_err(e, "cudaMalloc");
+    }
+    e = cudaMemcpy(d, u, count * csz, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) {
+        const int blocks = (int)std::min<long long>((count + 255) / 256, 1184);
+        if (precision == PM_SINGLE)
+            phases_kernel<float><<<blocks, 256>>>((const float2*)d, count, (float)zero_tol, o);
+        else
+            phases_kernel<double><<<blocks, 256>>>((const double2*)d, count, zero_tol, o);
+        e = cudaGetLastError();
+        if (e == cudaSuccess) e = cudaMemcpy(out, o, count * sizeof(double), cudaMemcpyDeviceToHost);
+    }
+    cudaFree(d);
+    cudaFree(o);
+    if (e != cudaSuccess) return cuda_err(e, "pm_phases");
+    return PM_OK;
+}
+
+// ---------------------------------------------------------------- solve
+static int solve_core(pm_plan* pl, const void* d_p, const void* d_m, const void* d_init, int batch,
+                      const pm_params* prm, const double* tol_p, const double* tol_m,
+                      const double* energy, pm_result* res, bool host_io) {
+    if (!tol_p || !tol_m || !energy) return set_err(PM_ERR_ARG, "null tolerance / energy arrays");
+    CKR(session_setup(pl, d_p, d_m, batch, prm, tol_p, tol_m, energy));
+    auto& s = pl->s;
+    const size_t N = pl->N;
+    if (prm->init_complex) {
+        if (!d_init) return set_err(PM_ERR_ARG, "init_complex set but m_init is NULL");
+        CK(cudaMemcpyAsync(pl->field, d_init, batch * N * pl->csz,
+                           host_io ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, pl->stream));
+    }
+    if (host_io) {
+        CKR(ensure_outputs(pl, res && res->phases, res && res->levels, res && res->u_star, res && res->v_star));
+        s.phases = (res && res->phases) ? pl->phases : nullptr;
+        s.levels = (res && res->levels) ? pl->levels : nullptr;
+        s.ustar = (res && res->u_star) ? pl->ustar : nullptr;
+        s.vstar = (res && res->v_star) ? pl->vstar : nullptr;
+    } else {
+        s.phases = res ? res->phases : nullptr;
+        s.levels = res ? res->levels : nullptr;
+        s.ustar = res ? res->u_star : nullptr;
+        s.vstar = res ? res->v_star : nullptr;
+    }
+    CK(cudaEventRecord(pl->ev0, pl->stream));
+    CKR(enqueue_full_solve(pl));
+    CK(cudaEventRecord(pl->ev1, pl->stream));
+    if (host_io && res) {
+        if (res->phases)
+            CK(cudaMemcpyAsync(res->phases, pl->phases, batch * N * sizeof(double), cudaMemcpyDeviceToHost,
+                               pl->stream));
+        if (res->levels)
+            CK(cudaMemcpyAsync(res->levels, pl->levels, batch * N, cudaMemcpyDeviceToHost, pl->stream));
+        if (res->u_star)
+            CK(cudaMemcpyAsync(res->u_star, pl->ustar, batch * N * pl->csz, cudaMemcpyDeviceToHost, pl->stream));
+        if (res->v_star)
+            CK(cudaMemcpyAsync(res->v_star, pl->vstar, batch * N * pl->csz, cudaMemcpyDeviceToHost, pl->stream));
+    }
+    std::vector<int> iters(batch), div(batch);
+    CKR(read_records(pl, 1, prm->max_iters, res ? res->gap : nullptr, res ? res->err_lit : nullptr,
+                     res ? res->err_dark : nullptr, iters.data(), div.data()));
+    if (res) {
+        if (res->iters_run) std::copy(iters.begin(), iters.end(), res->iters_run);
+        if (res->diverged_iter) std::copy(div.begin(), div.end(), res->diverged_iter);
+        if (res->device_ms) CK(cudaEventElapsedTime(res->device_ms, pl->ev0, pl->ev1));
+    }
+    s.active = false;
+    if (any_diverged(div)) return set_err(PM_ERR_DIVERGED, "non-finite values during the iteration");
+    return PM_OK;
+}
+
+int pm_solve(pm_plan* pl, const void* p, const void* m, const void* m_init, int batch,
+             const pm_params* prm, const double* tol_p, const double* tol_m, const double* energy,
+             pm_result* res) {
+    CKR(check_plan(pl));
+    if (!p || !m) return set_err(PM_ERR_ARG, "null p or m");
+    CKR(validate_params(prm, batch));
+    std::lock_guard<std::mutex> lk(pl->mu);
+    CKR(ensure_capacity(pl, batch, prm->max_iters));
+    const size_t N = pl->N;
+    CK(cudaMemcpyAsync(pl->pbuf, p, (prm->p_per_mask ? batch : 1) * N * pl->rsz, cudaMemcpyHostToDevice,
+                       pl->stream));
+    CK(cudaMemcpyAsync(pl->mbuf, m, batch * N * pl->rsz, cudaMemcpyHostToDevice, pl->stream));
+    return solve_core(pl, pl->pbuf, pl->mbuf, m_init, batch, prm, tol_p, tol_m, energy, res, true);
+}
+
+int pm_solve_device(pm_plan* pl, const void* d_p, const void* d_m, const void* d_m_init, int batch,
+                    const pm_params* prm, const double* tol_p, const double* tol_m, const double* energy,
+                    pm_result* res) {
+    CKR(check_plan(pl));
+    if (!d_p || !d_m) return set_err(PM_ERR_ARG, "null p or m");
+    std::lock_guard<std::mutex> lk(pl->mu);
+    return solve_core(pl, d_p, d_m, d_m_init, batch, prm, tol_p, tol_m, energy, res, false);
+}
+
+int pm_solve_begin(pm_plan* pl, const void* p, const void* m, const void* m_init, int batch,
+                   const pm_params* prm, const double* tol_p, const double* tol_m, const double* energy) {
+    CKR(check_plan(pl));
+    if (!p || !m || !tol_p || !tol_m || !energy) return set_err(PM_ERR_ARG, "null input");
+    CKR(validate_params(prm, batch));
+    std::lock_guard<std::mutex> lk(pl->mu);
+    CKR(ensure_capacity(pl, batch, prm->max_iters));
+    const size_t N = pl->N;
+    CK(cudaMemcpyAsync(pl->pbuf, p, (prm->p_per_mask ? batch : 1) * N * pl->rsz, cudaMemcpyHostToDevice,
+                       pl->stream));
+    CK(cudaMemcpyAsync(pl->mbuf, m, batch * N * pl->rsz, cudaMemcpyHostToDevice, pl->stream));
+    CKR(session_setup(pl, pl->pbuf, pl->mbuf, batch, prm, tol_p, tol_m, energy));
+    if (prm->init_complex) {
+        if (!m_init) return set_err(PM_ERR_ARG, "init_complex set but m_init is NULL");
+        CK(cudaMemcpyAsync(pl->field, m_init, batch * N * pl->csz, cudaMemcpyHostToDevice, pl->stream));
+    }
+    CK(cudaEventRecord(pl->ev0, pl->stream));
+    CKR(enqueue_begin(pl));
+    CK(cudaStreamSynchronize(pl->stream));
+    return PM_OK;
+}
+
+int pm_solve_step(pm_plan* pl, int n_iters, int* all_stopped) {
+    CKR(check_plan(pl));
+    std::lock_guard<std::mutex> lk(pl->mu);
+    if (!pl->s.active) return set_err(PM_ERR_ARG, "no solve in progress (call pm_solve_begin)");
+    CKR(enqueue_steps(pl, n_iters));
+    std::vector<MaskState> st(pl->s.batch);
+    CK(cudaMemcpyAsync(st.data(), pl->st, st.size() * sizeof(MaskState), cudaMemcpyDeviceToHost, pl->stream));
+    CK(cudaStreamSynchronize(pl->stream));
+    int all = 1;
+    for (auto& x : st) all &= (x.stop || x.done) ? 1 : 0;
+    if (all_stopped) *all_stopped = all;
+    return PM_OK;
+}
+
+int pm_solve_records(pm_plan* pl, int first_iter, int last_iter, double* gap, double* err_lit,
+                     double* err_dark, int* iters_run, int* diverged_iter) {
+    CKR(check_plan(pl));
+    std::lock_guard<std::mutex> lk(pl->mu);
+    if (pl->s.batch < 1) return set_err(PM_ERR_ARG, "no solve in progress");
+    return read_records(pl, std::max(1, first_iter), last_iter, gap, err_lit, err_dark, iters_run,
+                        diverged_iter);
+}
+
+int pm_solve_finish(pm_plan* pl, int abort, pm_result* res) {
+    CKR(check_plan(pl));
+    std::lock_guard<std::mutex> lk(pl->mu);
+    auto& s = pl->s;
+    if (!s.active) return set_err(PM_ERR_ARG, "no solve in progress (call pm_solve_begin)");
+    const size_t N = pl->N;
+    const int batch = s.batch;
+    CKR(ensure_outputs(pl, res && res->phases, res && res->levels, res && res->u_star, res && res->v_star));
+    s.phases = (res && res->phases) ? pl->phases : nullptr;
+    s.levels = (res && res->levels) ? pl->levels : nullptr;
+    s.ustar = (res && res->u_star) ? pl->ustar : nullptr;
+    s.vstar = (res && res->v_star) ? pl->vstar : nullptr;
+    if (abort) {
+        force_stop_kernel<<<(batch + 127) / 128, 128, 0, pl->stream>>>(pl->st, batch, s.it);
+        CK(cudaGetLastError());
+    }
+    CKR(enqueue_finish(pl));
+    CK(cudaEventRecord(pl->ev1, pl->stream));
+    if (res) {
+        if (res->phases)
+            CK(cudaMemcpyAsync(res->phases, pl->phases, batch * N * sizeof(double), cudaMemcpyDeviceToHost,
+                               pl->stream));
+        if (res->levels)
+            CK(cudaMemcpyAsync(res->levels, pl->levels, batch * N, cudaMemcpyDeviceToHost, pl->stream));
+        if (res->u_star)
+            CK(cudaMemcpyAsync(res->u_star, pl->ustar, batch * N * pl->csz, cudaMemcpyDeviceToHost, pl->stream));
+        if (res->v_star)
+            CK(cudaMemcpyAsync(res->v_star, pl->vstar, batch * N * pl->csz, cudaMemcpyDeviceToHost, pl->stream));
+    }
+    std::vector<int> iters(batch), div(batch);
+    CKR(read_records(pl, 1, s.prm.max_iters, res ? res->gap : nullptr, res ? res->err_lit : nullptr,
+                     res ? res->err_dark : nullptr, iters.data(), div.data()));
+    if (res) {
+        if (res->iters_run) std::copy(iters.begin(), iters.end(), res->iters_run);
+        if (res->diverged_iter) std::copy(div.begin(), div.end(), res->diverged_iter);
+        if (res->device_ms) CK(cudaEventElapsedTime(res->device_ms, pl->ev0, pl->ev1));
+    }
+    s.active = false;
+    if (any_diverged(div)) return set_err(PM_ERR_DIVERGED, "non-finite values during the iteration");
+    return PM_OK;
+}
+
+// ---------------------------------------------------------- measurement
+int pm_time_sweep(pm_plan* pl, int which, int batch, int reps, float* avg_ms) {
+    CKR(check_plan(pl));
+    if (!avg_ms || reps < 1 || batch < 1) return set_err(PM_ERR_ARG, "bad arguments");
+    std::lock_guard<std::mutex> lk(pl->mu);
+    auto& s = pl->s;
+    if (!s.p || !s.m || batch > pl->cap) return set_err(PM_ERR_ARG, "run a solve on this plan first");
+    const int saved_batch = s.batch;
+    s.batch = batch;
+    s.phases = s.levels = s.ustar = s.vstar = nullptr;
+    CK(cudaMemsetAsync(pl->st, 0, batch * sizeof(MaskState), pl->stream));
+    // one warm-up launch, then `reps` timed launches of the steady-state sweep
+    // (column sweeps include the full metric reduction of a recorded iteration)
+    const int big = 1 << 30;
+    pm_params saved = s.prm;
+    s.prm.max_iters = big;
+    s.prm.record_every = 1;
+    s.prm.early_stop_tol = -1.0;
+    int r = PM_OK;
+    for (int i = 0; i <= reps && r == PM_OK; ++i) {
+        if (i == 1) CK(cudaEventRecord(pl->ev0, pl->stream));
+        r = which == 0 ? row(pl, batch, 1, 1) : col(pl, batch, 2, 1);
+    }
+    s.prm = saved;
+    s.batch = saved_batch;
+    CKR(r);
+    CK(cudaEventRecord(pl->ev1, pl->stream));
+    CK(cudaEventSynchronize(pl->ev1));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, pl->ev0, pl->ev1));
+    *avg_ms = ms / reps;
+    return PM_OK;
+}
+
+int pm_measure_copy(int device, long long bytes, int reps, double* gbs) {
+    if (!gbs || bytes < 16 || reps < 1) return set_err(PM_ERR_ARG, "bad arguments");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return set_err(PM_ERR_CUDA, "no CUDA device available");
+    }
+    CK(cudaSetDevice(device));
+    const long long n4 = bytes / 16;
+    float4 *a = nullptr, *b = nullptr;
+    CK(cudaMalloc((void**)&a, n4 * 16));
+    cudaError_t e = cudaMalloc((void**)&b, n4 * 16);
+    if (e != cudaSuccess) {
+        cudaFree(a);
+        return cuda_err(e, "cudaMalloc");
+    }
+    cudaMemset(a, 0, n4 * 16);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
+    const int blocks = nsm * 8;
+    float best = 1e30f;
+    for (int i = 0; i < reps + 2; ++i) {
+        cudaEventRecord(e0);
+        copy_kernel<<<blocks, 256>>>(a, b, n4);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (i >= 2) best = std::min(best, ms);
+    }
+    e = cudaGetLastError();
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(a);
+    cudaFree(b);
+    if (e != cudaSuccess) return cuda_err(e, "copy_kernel");
+    *gbs = 2.0 * n4 * 16 / (best * 1e-3) / 1e9;
+    return PM_OK;
+}
+
+}  // extern "C"
