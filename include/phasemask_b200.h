@@ -222,6 +222,10 @@ int pm_solve_finish(pm_plan *plan, int abort, pm_result *result);
  */
 int pm_time_sweep(pm_plan *plan, int which, int batch, int reps, float *avg_ms);
 
+/* Diagnostics: enable (1) per-phase %globaltimer stamps in the persistent
+ * solve kernel, or read (0) up to n of them into `out` (ns). */
+int pm_debug_phase_stamps(pm_plan *plan, int enable, unsigned long long *out, int n);
+
 /* Device-to-device copy bandwidth over `bytes` (read+write counted), best of
  * `reps`, for the HBM (bytes >> L2) and L2 (bytes << L2) roofs. */
 int pm_measure_copy(int device, long long bytes, int reps, double *gbs);

@@ -16,7 +16,7 @@ from pathlib import Path
 import numpy as np
 
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "lib" / "libphasemask_b200.so"
+LIB_PATH = Path(os.environ.get("PM_LIB", _PKG / "lib" / "libphasemask_b200.so"))
 
 PM_OK = 0
 PM_ERR_ARG = -1
@@ -91,6 +91,7 @@ SIGNATURES = {
     "pm_solve_finish": (_I, [_VP, _I, C.POINTER(pm_result)]),
     "pm_time_sweep": (_I, [_VP, _I, _I, _I, C.POINTER(C.c_float)]),
     "pm_measure_copy": (_I, [_I, _LL, _I, C.POINTER(_D)]),
+    "pm_debug_phase_stamps": (_I, [_VP, _I, _VP, _I]),
 }
 
 _lib = None

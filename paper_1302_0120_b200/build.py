@@ -41,14 +41,33 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found: the CUDA toolkit is required to build phasemask_b200")
 
 
-def _units():
+# log2 points per thread of the row / column kernels, per precision
+# (see DESIGN.md "Kernel configuration"); override for experiments with
+# PM_LGR="f32row,f32col,f64row,f64col".
+DEFAULT_LGR = {"f32": (4, 4), "f64": (4, 3)}
+
+
+def _lgr():
+    env = os.environ.get("PM_LGR")
+    if env:
+        a = [int(x) for x in env.split(",")]
+        return {"f32": (a[0], a[1]), "f64": (a[2], a[3])}
+    return DEFAULT_LGR
+
+
+def _units(build_dir):
     units = []
+    lgr = _lgr()
+    nt = int(os.environ.get("PM_SOLVE_NT", "512"))
     for f64 in (0, 1):
+        tag = "f64" if f64 else "f32"
+        row, col = lgr[tag]
         for lg in range(MAX_LG + 1):
-            units.append((CSRC / "pm_inst.cu", BUILD / f"pm_inst_{'f64' if f64 else 'f32'}_{lg}.o",
-                          [f"-DPM_F64={f64}", f"-DPM_LG={lg}"]))
-    units.append((CSRC / "pm_table.cu", BUILD / "pm_table.o", []))
-    units.append((CSRC / "pm_capi.cu", BUILD / "pm_capi.o", []))
+            units.append((CSRC / "pm_inst.cu", build_dir / f"pm_inst_{tag}_{lg}_{row}{col}_{nt}.o",
+                          [f"-DPM_F64={f64}", f"-DPM_LG={lg}", f"-DPM_LGR_ROW={row}", f"-DPM_LGR_COL={col}",
+                           f"-DPM_SOLVE_NT={nt}"]))
+    units.append((CSRC / "pm_table.cu", build_dir / "pm_table.o", []))
+    units.append((CSRC / "pm_capi.cu", build_dir / "pm_capi.o", []))
     return units
 
 
@@ -71,10 +90,12 @@ def _compile(unit, force: bool, verbose: bool):
     return obj, r.stderr if verbose else None
 
 
-def build(force: bool = False, jobs: int | None = None, verbose: bool = False) -> Path:
+def build(force: bool = False, jobs: int | None = None, verbose: bool = False,
+          out: Path | None = None) -> Path:
+    lib = Path(out) if out else LIB
     BUILD.mkdir(exist_ok=True)
-    LIBDIR.mkdir(exist_ok=True)
-    units = _units()
+    lib.parent.mkdir(parents=True, exist_ok=True)
+    units = _units(BUILD)
     jobs = jobs or max(1, os.cpu_count() or 1)
     # biggest units first so the long poles start early
     order = sorted(units, key=lambda u: -int(next((d.split("=")[1] for d in u[2] if "PM_LG" in d), "0")))
@@ -85,16 +106,16 @@ def build(force: bool = False, jobs: int | None = None, verbose: bool = False) -
                 logs.append(f"== {obj.name}\n{log}")
     objs = [str(u[1]) for u in units]
     newest = max(Path(o).stat().st_mtime for o in objs)
-    if force or not LIB.exists() or LIB.stat().st_mtime < newest:
-        tmp = LIB.with_suffix(".so.tmp")
+    if force or not lib.exists() or lib.stat().st_mtime < newest:
+        tmp = lib.with_suffix(".so.tmp")
         cmd = [nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", str(tmp), *objs]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
-        os.replace(tmp, LIB)
+        os.replace(tmp, lib)
     if verbose and logs:
         (BUILD / "ptxas.log").write_text("\n".join(logs))
-    return LIB
+    return lib
 
 
 def main(argv=None):
@@ -102,8 +123,9 @@ def main(argv=None):
     ap.add_argument("--force", action="store_true")
     ap.add_argument("--jobs", type=int, default=None)
     ap.add_argument("--verbose", action="store_true", help="keep ptxas -v output in build/ptxas.log")
+    ap.add_argument("--out", default=None, help="output .so path (default: lib/libphasemask_b200.so)")
     a = ap.parse_args(argv)
-    print(build(a.force, a.jobs, a.verbose))
+    print(build(a.force, a.jobs, a.verbose, a.out))
 
 
 if __name__ == "__main__":

@@ -157,6 +157,29 @@ __global__ void copy_kernel(const float4* __restrict__ a, float4* __restrict__ b
         b[i] = a[i];
 }
 
+// sum p^2 per amplitude grid (fixed partition) and the reconstructed-
+// intensity scale sum m^2 / sum p^2 per mask (sum |u|^2 = sum p^2 on S).
+template <typename T>
+__global__ void psum_partial_kernel(const T* p, long long n, long long chunk, long long pstride,
+                                    double* part, int nb) {
+    const T* q = p + blockIdx.y * pstride;
+    const long long lo = blockIdx.x * chunk, hi = min(n, lo + chunk);
+    double acc = 0.0;
+    for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) acc += (double)q[i] * (double)q[i];
+    const double s = block_sum(acc);
+    if (threadIdx.x == 0) part[blockIdx.y * nb + blockIdx.x] = s;
+}
+
+__global__ void escale_kernel(const double* part, int nb, int per_mask, const double* energy,
+                              double* escale, int batch) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= batch) return;
+    const double* q = part + (per_mask ? b : 0) * nb;
+    double s = 0.0;
+    for (int i = 0; i < nb; ++i) s += q[i];
+    escale[b] = energy[b] / s;
+}
+
 // Host abort (should_abort -> True): the current iterate becomes the last.
 __global__ void force_stop_kernel(MaskState* st, int batch, int it) {
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
@@ -181,12 +204,12 @@ int lg2_exact(int n) {
 
 const KernelSet& kset(int prec, int lg) { return prec == PM_SINGLE ? kernels_f32(lg) : kernels_f64(lg); }
 
-// Forward twiddles of the Stockham passes, [pass][r-1][k] (see FftShape).
-template <typename C>
-std::vector<C> make_twiddles(int lg, int lgR_max) {
+// Twiddles of the Stockham passes, [pass][r-1][k] (see FftShape), as
+// (cos, sin) of the angle DIR * 2 pi r k / (Ns Rs) in long double.
+std::vector<std::pair<double, double>> twiddle_angles(int lg, int lgR_max, int dir) {
     const int lgR = std::min(lg, lgR_max);
     const int NP = lgR == 0 ? 0 : (lg + lgR - 1) / lgR;
-    std::vector<C> out;
+    std::vector<std::pair<double, double>> out;
     const long double pi = 3.141592653589793238462643383279502884L;
     for (int s = 1; s < NP; ++s) {
         const int lgRs = (s < NP - 1) ? lgR : lg - (NP - 1) * lgR;
@@ -194,13 +217,47 @@ std::vector<C> make_twiddles(int lg, int lgR_max) {
         for (long long r = 1; r < Rs; ++r)
             for (long long k = 0; k < Ns; ++k) {
                 const long double ang = 2.0L * pi * (long double)((r * k) % M) / (long double)M;
-                C w;
-                w.x = (decltype(w.x))cosl(ang);
-                w.y = (decltype(w.y))(-sinl(ang));
-                out.push_back(w);
+                out.emplace_back((double)cosl(ang), (double)(dir * sinl(ang)));
             }
     }
     return out;
+}
+
+// Device twiddle tables for one axis: fp32 forward/inverse float4 entries
+// (c, s, -s, c) so a twiddle multiply is FMUL2 + FFMA2; fp64 one (c, s) table.
+int upload_twiddles(int prec, int lg, int lgR, int TW, void** fwd, void** inv) {
+    *fwd = *inv = nullptr;
+    if (prec == PM_SINGLE) {
+        for (int d = 0; d < 2; ++d) {
+            const int dir = d == 0 ? -1 : +1;
+            std::vector<float4> t;
+            for (auto& w : twiddle_angles(lg, lgR, dir))
+                t.push_back(make_float4((float)w.first, (float)w.second, -(float)w.second, (float)w.first));
+            if ((int)t.size() != TW) return set_err(PM_ERR_CUDA, "twiddle table size mismatch");
+            void** dst = d == 0 ? fwd : inv;
+            CK(cudaMalloc(dst, std::max<size_t>(1, t.size()) * sizeof(float4)));
+            if (!t.empty()) CK(cudaMemcpy(*dst, t.data(), t.size() * sizeof(float4), cudaMemcpyHostToDevice));
+        }
+    } else {
+        std::vector<double2> t;
+        for (auto& w : twiddle_angles(lg, lgR, -1)) t.push_back(make_double2(w.first, w.second));
+        if ((int)t.size() != TW) return set_err(PM_ERR_CUDA, "twiddle table size mismatch");
+        CK(cudaMalloc(fwd, std::max<size_t>(1, t.size()) * sizeof(double2)));
+        if (!t.empty()) CK(cudaMemcpy(*fwd, t.data(), t.size() * sizeof(double2), cudaMemcpyHostToDevice));
+        *inv = *fwd;
+    }
+    return PM_OK;
+}
+
+// fp32 zero-branch decision on s = |u|^2: the least float s with
+// sqrtf(s) >= (float)tol, so `s >= thr` <=> `sqrtf(s) >= tol` exactly.
+double fp32_sq_threshold(double tol) {
+    const float tf = (float)tol;
+    if (!(tf > 0.f)) return 0.0;
+    float s = tf * tf;
+    while (s > 0.f && sqrtf(s) >= tf) s = nextafterf(s, 0.f);
+    while (sqrtf(s) < tf) s = nextafterf(s, INFINITY);
+    return (double)s;
 }
 
 std::map<const void*, size_t>& smem_configured() {
@@ -232,8 +289,10 @@ struct pm_plan {
     int hist_cap = 0;                 // max_iters capacity of the history buffer
     cudaStream_t stream = nullptr;
     bool own_stream = false;
-    void* tw_row = nullptr;
+    void* tw_row = nullptr;           // forward twiddles, row axis
+    void* tw_row_i = nullptr;         // inverse (fp32; == tw_row for fp64)
     void* tw_col = nullptr;
+    void* tw_col_i = nullptr;
     void* field = nullptr;            // cap * N complex
     void* tmp = nullptr;              // cap * N complex (scratch)
     void* pbuf = nullptr;             // cap * N real
@@ -246,13 +305,19 @@ struct pm_plan {
     double* hist = nullptr;           // cap * hist_cap * 4
     double* part = nullptr;           // partial sums (row + col), cap * nblk * 3 each
     unsigned* ctr = nullptr;          // 2 * cap counters
-    double* tolp = nullptr;           // cap
-    double* tolm = nullptr;
-    double* energy = nullptr;
+    double* tolp = nullptr;           // cap: reference zero_tol of p
+    double* thrp = nullptr;           // cap: decision thresholds (fp32: on |u|^2)
+    double* thrm = nullptr;
+    double* escale = nullptr;         // cap: sum m^2 / sum p^2
+    double* energy = nullptr;         // cap: sum m^2 (host-provided)
+    double* psum = nullptr;           // cap * kPsumBlocks partial sums of p^2
     double* red = nullptr;            // reduction scratch
     int red_cap = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     long long launches = 0;
+    GridBar* bar = nullptr;           // grid barrier of the persistent kernel
+    unsigned long long* stamps = nullptr;  // optional phase timestamps (pm_debug_phase_stamps)
+    int solve_grid = 0;               // CTAs of the persistent kernel (0: not available)
     RowCfg rc{};
     ColCfg cc{};
     std::map<std::string, cudaGraphExec_t> graphs;
@@ -270,15 +335,16 @@ struct pm_plan {
         void* levels = nullptr;
         void* ustar = nullptr;
         void* vstar = nullptr;
+        std::vector<double> h_tolp, h_thrp, h_thrm, h_en;
     } s;
 };
 
 namespace {
 
 RowCfg row_config(const pm_plan* pl) {
-    const KernelSet& k = kset(pl->prec, pl->lgx);
+    const AxisShape& k = kset(pl->prec, pl->lgx).row;
     RowCfg c;
-    c.G = std::max(1, 256 / k.TG);
+    c.G = std::max(1, 128 / k.TG);
     c.G = std::min(c.G, pl->ny);
     c.threads = c.G * k.TG;
     c.nblk = pl->ny / c.G;
@@ -287,28 +353,29 @@ RowCfg row_config(const pm_plan* pl) {
 }
 
 ColCfg col_config(const pm_plan* pl) {
-    const KernelSet& k = kset(pl->prec, pl->lgy);
+    const AxisShape& k = kset(pl->prec, pl->lgy).col;
     ColCfg c;
     const int maxt = k.TG <= 64 ? 256 : 512;
     c.C = std::max(1, maxt / k.TG);
     c.C = std::min(c.C, pl->nx);
     c.threads = c.C * k.TG;
     c.nblk = pl->nx / c.C;
-    c.smem = k.SM ? (size_t)c.C * (k.SM + kColPad) * pl->csz : 0;
+    const int pad = std::max(1, (int)(128 / (pl->csz * c.C)));
+    c.smem = k.SM ? (size_t)c.C * (k.SM + pad) * pl->csz : 0;
     return c;
 }
 
 void free_buffers(pm_plan* pl) {
     void* bufs[] = {pl->field, pl->tmp, pl->pbuf, pl->mbuf, pl->phases, pl->levels, pl->ustar,
-                    pl->vstar, pl->st, pl->hist, pl->part, pl->ctr, pl->tolp, pl->tolm,
-                    pl->energy};
+                    pl->vstar, pl->st, pl->hist, pl->part, pl->ctr, pl->tolp, pl->thrp,
+                    pl->thrm, pl->escale, pl->energy, pl->psum};
     for (void* b : bufs)
         if (b) cudaFree(b);
     pl->field = pl->tmp = pl->pbuf = pl->mbuf = pl->ustar = pl->vstar = nullptr;
     pl->phases = nullptr;
     pl->levels = nullptr;
     pl->st = nullptr;
-    pl->hist = pl->part = pl->tolp = pl->tolm = pl->energy = nullptr;
+    pl->hist = pl->part = pl->tolp = pl->thrp = pl->thrm = pl->escale = pl->energy = pl->psum = nullptr;
     pl->ctr = nullptr;
     pl->cap = 0;
     pl->hist_cap = 0;
@@ -327,19 +394,22 @@ int ensure_capacity(pm_plan* pl, int batch, int max_iters) {
     drop_graphs(pl);
     free_buffers(pl);
     const size_t N = pl->N;
-    const int nb = std::max(pl->rc.nblk, pl->cc.nblk);
+    const int nb = std::max(pl->cc.nblk, pl->nx);   // >= tasks per mask of either path
     CK(cudaMalloc(&pl->field, cap * N * pl->csz));
     CK(cudaMalloc(&pl->tmp, cap * N * pl->csz));
     CK(cudaMalloc(&pl->pbuf, cap * N * pl->rsz));
     CK(cudaMalloc(&pl->mbuf, cap * N * pl->rsz));
     CK(cudaMalloc((void**)&pl->st, cap * sizeof(MaskState)));
     CK(cudaMalloc((void**)&pl->hist, (size_t)cap * hcap * 4 * sizeof(double)));
-    CK(cudaMalloc((void**)&pl->part, (size_t)2 * cap * nb * 3 * sizeof(double)));
-    CK(cudaMalloc((void**)&pl->ctr, (size_t)2 * cap * sizeof(unsigned)));
+    CK(cudaMalloc((void**)&pl->part, (size_t)cap * nb * 3 * sizeof(double)));
+    CK(cudaMalloc((void**)&pl->ctr, (size_t)cap * sizeof(unsigned)));
     CK(cudaMalloc((void**)&pl->tolp, cap * sizeof(double)));
-    CK(cudaMalloc((void**)&pl->tolm, cap * sizeof(double)));
+    CK(cudaMalloc((void**)&pl->thrp, cap * sizeof(double)));
+    CK(cudaMalloc((void**)&pl->thrm, cap * sizeof(double)));
+    CK(cudaMalloc((void**)&pl->escale, cap * sizeof(double)));
     CK(cudaMalloc((void**)&pl->energy, cap * sizeof(double)));
-    CK(cudaMemsetAsync(pl->ctr, 0, (size_t)2 * cap * sizeof(unsigned), pl->stream));
+    CK(cudaMalloc((void**)&pl->psum, (size_t)cap * 32 * sizeof(double)));
+    CK(cudaMemsetAsync(pl->ctr, 0, (size_t)cap * sizeof(unsigned), pl->stream));
     CK(cudaMemsetAsync(pl->st, 0, cap * sizeof(MaskState), pl->stream));
     pl->cap = cap;
     pl->hist_cap = hcap;
@@ -357,49 +427,56 @@ int ensure_outputs(pm_plan* pl, bool phases, bool levels, bool ustar, bool vstar
 
 // --------------------------------------------------------------- launches
 template <typename T>
-int launch_row(pm_plan* pl, int batch, int mode, int it) {
-    const KernelSet& k = kset(pl->prec, pl->lgx);
+RowArgs<T> row_args(pm_plan* pl, int mode, int it) {
     RowArgs<T> a;
     a.field = (cx<T>*)pl->field;
     a.p = (const T*)pl->s.p;
     a.p_stride = pl->s.p_stride;
-    a.tw = (const cx<T>*)pl->tw_row;
+    a.twf = (const twe<T>*)pl->tw_row;
+    a.twi = (const twe<T>*)pl->tw_row_i;
     a.nx = pl->nx;
     a.ny = pl->ny;
-    a.scale = (T)(1.0 / std::sqrt((double)pl->nx));
-    a.tol_p = pl->tolp;
+    a.scale = (T)(1.0 / std::sqrt((double)pl->N));
+    a.thr_p = pl->thrp;
     a.mode = mode;
     a.it = it;
     a.st = pl->st;
-    a.part = pl->part;
-    a.ctr = pl->ctr;
-    a.nblk = pl->rc.nblk;
+    return a;
+}
+
+template <typename T>
+FinalArgs<T> final_args(pm_plan* pl) {
+    FinalArgs<T> a;
+    a.field = (const cx<T>*)pl->field;
+    a.p = (const T*)pl->s.p;
+    a.p_stride = pl->s.p_stride;
+    a.twi = (const twe<T>*)pl->tw_row_i;
+    a.nx = pl->nx;
+    a.ny = pl->ny;
+    a.scale = (T)(1.0 / std::sqrt((double)pl->N));
+    a.tol_p = pl->tolp;
+    a.st = pl->st;
     a.v_star = (cx<T>*)pl->s.vstar;
     a.u_star = (cx<T>*)pl->s.ustar;
     a.phases = (double*)pl->s.phases;
     a.levels = (uint8_t*)pl->s.levels;
-    CK(allow_smem(k.row_iter, pl->rc.smem));
-    void* args[] = {&a};
-    CK(cudaLaunchKernel(k.row_iter, dim3(pl->rc.nblk, batch), dim3(pl->rc.threads), args,
-                        pl->rc.smem, pl->stream));
-    pl->launches++;
-    return PM_OK;
+    return a;
 }
 
 template <typename T>
-int launch_col(pm_plan* pl, int batch, int mode, int u_iter) {
-    const KernelSet& k = kset(pl->prec, pl->lgy);
+ColArgs<T> col_args(pm_plan* pl, int mode, int u_iter) {
     const pm_params& prm = pl->s.prm;
     ColArgs<T> a;
     a.field = (cx<T>*)pl->field;
     a.m = (const T*)pl->s.m;
     a.m_stride = (long long)pl->N;
-    a.tw = (const cx<T>*)pl->tw_col;
+    a.twf = (const twe<T>*)pl->tw_col;
+    a.twi = (const twe<T>*)pl->tw_col_i;
     a.nx = pl->nx;
     a.ny = pl->ny;
-    a.scale = (T)(1.0 / std::sqrt((double)pl->ny));
-    a.tol_m = pl->tolm;
-    a.energy_target = pl->energy;
+    a.scale = (T)(1.0 / std::sqrt((double)pl->N));
+    a.thr_m = pl->thrm;
+    a.escale = pl->escale;
     a.mode = mode;
     a.u_iter = u_iter;
     a.ctl.max_iters = prm.max_iters;
@@ -410,20 +487,87 @@ int launch_col(pm_plan* pl, int batch, int mode, int u_iter) {
     a.st = pl->st;
     a.hist = pl->hist;
     a.hist_stride = pl->hist_cap;
-    a.part = pl->part + (size_t)pl->cap * std::max(pl->rc.nblk, pl->cc.nblk) * 3;
-    a.ctr = pl->ctr + pl->cap;
+    a.part = pl->part;
+    a.ctr = pl->ctr;
     a.nblk = pl->cc.nblk;
-    CK(allow_smem(k.col_iter, pl->cc.smem));
+    return a;
+}
+
+template <typename T>
+int launch_row(pm_plan* pl, int batch, int mode, int it) {
+    RowArgs<T> a = row_args<T>(pl, mode, it);
     void* args[] = {&a};
-    CK(cudaLaunchKernel(k.col_iter, dim3(pl->cc.nblk, batch), dim3(pl->cc.threads), args,
-                        pl->cc.smem, pl->stream));
+    CK(cudaLaunchKernel(kset(pl->prec, pl->lgx).row_iter, dim3(pl->rc.nblk, batch), dim3(pl->rc.threads),
+                        args, pl->rc.smem, pl->stream));
     pl->launches++;
     return PM_OK;
+}
+
+template <typename T>
+int launch_final(pm_plan* pl, int batch) {
+    FinalArgs<T> a = final_args<T>(pl);
+    void* args[] = {&a};
+    CK(cudaLaunchKernel(kset(pl->prec, pl->lgx).row_final, dim3(pl->rc.nblk, batch), dim3(pl->rc.threads),
+                        args, pl->rc.smem, pl->stream));
+    pl->launches++;
+    return PM_OK;
+}
+
+template <typename T>
+int launch_col(pm_plan* pl, int batch, int mode, int u_iter) {
+    ColArgs<T> a = col_args<T>(pl, mode, u_iter);
+    void* args[] = {&a};
+    CK(cudaLaunchKernel(kset(pl->prec, pl->lgy).col_iter, dim3(pl->cc.nblk, batch), dim3(pl->cc.threads),
+                        args, pl->cc.smem, pl->stream));
+    pl->launches++;
+    return PM_OK;
+}
+
+// One cooperative launch of the persistent solve kernel: optional initial
+// iterate, iterations [it_begin, it_end), optional final pair.
+template <typename T>
+int launch_solve(pm_plan* pl, int do_init, int it_begin, int it_end, int do_final) {
+    const KernelSet& k = kset(pl->prec, pl->lgx);
+    SolveArgs<T> a;
+    a.row = row_args<T>(pl, 1, 0);
+    a.col = col_args<T>(pl, 2, 0);
+    a.fin = final_args<T>(pl);
+    a.bar = pl->bar;
+    a.batch = pl->s.batch;
+    a.it_begin = it_begin;
+    a.it_end = it_end;
+    a.do_init = do_init;
+    a.do_final = do_final;
+    a.init_mode = pl->s.prm.init_complex ? 1 : 0;
+    a.stamps = pl->stamps;
+    void* args[] = {&a};
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(pl->solve_grid);
+    cfg.blockDim = dim3(k.solve_threads);
+    cfg.dynamicSmemBytes = (size_t)k.solve_smem;
+    cfg.stream = pl->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CK(cudaMemsetAsync(pl->bar, 0, sizeof(GridBar), pl->stream));
+    CK(cudaLaunchKernelExC(&cfg, k.solve, args));
+    pl->launches++;
+    return PM_OK;
+}
+
+int solve_launch(pm_plan* pl, int do_init, int it_begin, int it_end, int do_final) {
+    return pl->prec == PM_SINGLE ? launch_solve<float>(pl, do_init, it_begin, it_end, do_final)
+                                 : launch_solve<double>(pl, do_init, it_begin, it_end, do_final);
 }
 
 int row(pm_plan* pl, int batch, int mode, int it) {
     return pl->prec == PM_SINGLE ? launch_row<float>(pl, batch, mode, it)
                                  : launch_row<double>(pl, batch, mode, it);
+}
+int final_pair(pm_plan* pl, int batch) {
+    return pl->prec == PM_SINGLE ? launch_final<float>(pl, batch) : launch_final<double>(pl, batch);
 }
 int col(pm_plan* pl, int batch, int mode, int u_iter) {
     return pl->prec == PM_SINGLE ? launch_col<float>(pl, batch, mode, u_iter)
@@ -437,20 +581,18 @@ int launch_fft2(pm_plan* pl, const void* in, void* out, int dir, int batch) {
     const KernelSet& kc = kset(pl->prec, pl->lgy);
     const cx<T>* src = (const cx<T>*)in;
     cx<T>* dst = (cx<T>*)out;
-    const cx<T>* twr = (const cx<T>*)pl->tw_row;
-    const cx<T>* twc = (const cx<T>*)pl->tw_col;
+    const twe<T>* twr = (const twe<T>*)(dir < 0 ? pl->tw_row : pl->tw_row_i);
+    const twe<T>* twc = (const twe<T>*)(dir < 0 ? pl->tw_col : pl->tw_col_i);
     int nx = pl->nx, ny = pl->ny;
     T sx = (T)(1.0 / std::sqrt((double)nx)), sy = (T)(1.0 / std::sqrt((double)ny));
     {
         void* args[] = {&src, &dst, &twr, &nx, &ny, &sx, &dir};
-        CK(allow_smem(kr.row_fft, pl->rc.smem));
         CK(cudaLaunchKernel(kr.row_fft, dim3(pl->rc.nblk, batch), dim3(pl->rc.threads), args,
                             pl->rc.smem, pl->stream));
     }
     {
         const cx<T>* src2 = dst;
         void* args[] = {&src2, &dst, &twc, &nx, &ny, &sy, &dir};
-        CK(allow_smem(kc.col_fft, pl->cc.smem));
         CK(cudaLaunchKernel(kc.col_fft, dim3(pl->cc.nblk, batch), dim3(pl->cc.threads), args,
                             pl->cc.smem, pl->stream));
     }
@@ -493,22 +635,60 @@ int session_setup(pm_plan* pl, const void* d_p, const void* d_m, int batch, cons
     s.p = d_p;
     s.m = d_m;
     s.p_stride = prm->p_per_mask ? (long long)pl->N : 0;
-    std::vector<double> tp(batch), tm(batch), en(batch);
+    // pinned-free small uploads: stage in the session's host vectors, which
+    // must outlive the async copies -> keep them in the plan
+    s.h_tolp.resize(batch);
+    s.h_thrp.resize(batch);
+    s.h_thrm.resize(batch);
+    s.h_en.resize(batch);
     for (int b = 0; b < batch; ++b) {
-        tp[b] = tol_p[prm->p_per_mask ? b : 0];
-        tm[b] = tol_m[b];
-        en[b] = energy[b];
+        const double tp = tol_p[prm->p_per_mask ? b : 0];
+        s.h_tolp[b] = tp;
+        // row projection runs on v' = v / S (S = 1/sqrt(N)): scale the threshold
+        s.h_thrp[b] = pl->prec == PM_SINGLE ? fp32_sq_threshold(tp) * (double)pl->N
+                                            : tp * std::sqrt((double)pl->N);
+        s.h_thrm[b] = pl->prec == PM_SINGLE ? fp32_sq_threshold(tol_m[b]) : tol_m[b];
+        s.h_en[b] = energy[b];
     }
-    CK(cudaMemcpyAsync(pl->tolp, tp.data(), batch * sizeof(double), cudaMemcpyHostToDevice, pl->stream));
-    CK(cudaMemcpyAsync(pl->tolm, tm.data(), batch * sizeof(double), cudaMemcpyHostToDevice, pl->stream));
-    CK(cudaMemcpyAsync(pl->energy, en.data(), batch * sizeof(double), cudaMemcpyHostToDevice, pl->stream));
+    CK(cudaMemcpyAsync(pl->tolp, s.h_tolp.data(), batch * sizeof(double), cudaMemcpyHostToDevice, pl->stream));
+    CK(cudaMemcpyAsync(pl->thrp, s.h_thrp.data(), batch * sizeof(double), cudaMemcpyHostToDevice, pl->stream));
+    CK(cudaMemcpyAsync(pl->thrm, s.h_thrm.data(), batch * sizeof(double), cudaMemcpyHostToDevice, pl->stream));
+    CK(cudaMemcpyAsync(pl->energy, s.h_en.data(), batch * sizeof(double), cudaMemcpyHostToDevice, pl->stream));
     return PM_OK;
+}
+
+constexpr int kPsumBlocks = 32;
+
+int enqueue_escale(pm_plan* pl) {
+    auto& s = pl->s;
+    const long long n = (long long)pl->N;
+    const long long chunk = (n + kPsumBlocks - 1) / kPsumBlocks;
+    const int npg = s.prm.p_per_mask ? s.batch : 1;
+    const dim3 grid(kPsumBlocks, npg);
+    if (pl->prec == PM_SINGLE)
+        psum_partial_kernel<float><<<grid, 256, 0, pl->stream>>>((const float*)s.p, n, chunk, s.p_stride,
+                                                                  pl->psum, kPsumBlocks);
+    else
+        psum_partial_kernel<double><<<grid, 256, 0, pl->stream>>>((const double*)s.p, n, chunk, s.p_stride,
+                                                                   pl->psum, kPsumBlocks);
+    escale_kernel<<<(s.batch + 127) / 128, 128, 0, pl->stream>>>(pl->psum, kPsumBlocks, s.prm.p_per_mask,
+                                                                  pl->energy, pl->escale, s.batch);
+    CK(cudaGetLastError());
+    pl->launches += 2;
+    return PM_OK;
+}
+
+bool persistent(const pm_plan* pl) {
+    static const bool off = getenv("PM_NO_PERSISTENT") != nullptr;
+    return pl->solve_grid > 0 && !off;
 }
 
 int enqueue_begin(pm_plan* pl) {
     auto& s = pl->s;
     CK(cudaMemsetAsync(pl->st, 0, s.batch * sizeof(MaskState), pl->stream));
     CK(cudaMemsetAsync(pl->hist, 0, (size_t)s.batch * pl->hist_cap * 4 * sizeof(double), pl->stream));
+    CKR(enqueue_escale(pl));
+    if (persistent(pl)) return solve_launch(pl, 1, 1, 1, 0);
     CKR(col(pl, s.batch, s.prm.init_complex ? 1 : 0, 0));   // u0 column half
     CKR(row(pl, s.batch, 0, 0));                            // u0 row half, w0 = RowFFT(u0)
     CKR(col(pl, s.batch, 2, 0));                            // z1 = ColIFFT replace F u0
@@ -517,6 +697,12 @@ int enqueue_begin(pm_plan* pl) {
 
 int enqueue_steps(pm_plan* pl, int n) {
     auto& s = pl->s;
+    if (persistent(pl)) {
+        const int first = s.it + 1, last = std::min(s.it + n, s.prm.max_iters);
+        if (last < first) return PM_OK;
+        s.it = last;
+        return solve_launch(pl, 0, first, last + 1, 0);
+    }
     for (int i = 0; i < n && s.it < s.prm.max_iters; ++i) {
         s.it += 1;
         CKR(row(pl, s.batch, 1, s.it));        // u_it, w_it
@@ -525,7 +711,10 @@ int enqueue_steps(pm_plan* pl, int n) {
     return PM_OK;
 }
 
-int enqueue_finish(pm_plan* pl) { return row(pl, pl->s.batch, 2, pl->s.it); }
+int enqueue_finish(pm_plan* pl) {
+    if (persistent(pl)) return solve_launch(pl, 0, 1, 1, 1);
+    return final_pair(pl, pl->s.batch);
+}
 
 std::string graph_key(const pm_plan* pl) {
     const auto& s = pl->s;
@@ -541,6 +730,14 @@ std::string graph_key(const pm_plan* pl) {
 int enqueue_full_solve(pm_plan* pl) {
     static const bool no_graph = getenv("PM_NO_GRAPH") != nullptr;
     auto& s = pl->s;
+    if (persistent(pl)) {
+        // one cooperative launch: initial iterate, all iterations, final pair
+        CK(cudaMemsetAsync(pl->st, 0, s.batch * sizeof(MaskState), pl->stream));
+        CK(cudaMemsetAsync(pl->hist, 0, (size_t)s.batch * pl->hist_cap * 4 * sizeof(double), pl->stream));
+        CKR(enqueue_escale(pl));
+        s.it = s.prm.max_iters;
+        return solve_launch(pl, 1, 1, s.prm.max_iters + 1, 1);
+    }
     if (no_graph) {
         CKR(enqueue_begin(pl));
         CKR(enqueue_steps(pl, s.prm.max_iters));
@@ -571,7 +768,7 @@ int enqueue_full_solve(pm_plan* pl) {
     }
     s.it = s.prm.max_iters;
     CK(cudaGraphLaunch(it->second, pl->stream));
-    pl->launches += 2LL * s.prm.max_iters + 4;
+    pl->launches += 2LL * s.prm.max_iters + 6;
     return PM_OK;
 }
 
@@ -674,32 +871,38 @@ int pm_plan_create(int device, int n_x, int n_y, int precision, int max_batch, p
     // twiddle tables
     for (int axis = 0; axis < 2; ++axis) {
         const int lg = axis == 0 ? lgx : lgy;
-        const KernelSet& k = kset(precision, lg);
-        void** dst = axis == 0 ? &pl->tw_row : &pl->tw_col;
-        const size_t nbytes = std::max(1, k.TW) * pl->csz;
-        cudaError_t e2 = cudaMalloc(dst, nbytes);
-        if (e2 != cudaSuccess) return fail(cuda_err(e2, "cudaMalloc(twiddles)"));
-        if (k.TW > 0) {
-            if (precision == PM_SINGLE) {
-                auto t = make_twiddles<float2>(lg, k.lgR);
-                if ((int)t.size() != k.TW) return fail(set_err(PM_ERR_CUDA, "twiddle table size mismatch"));
-                e2 = cudaMemcpy(*dst, t.data(), nbytes, cudaMemcpyHostToDevice);
-            } else {
-                auto t = make_twiddles<double2>(lg, k.lgR);
-                if ((int)t.size() != k.TW) return fail(set_err(PM_ERR_CUDA, "twiddle table size mismatch"));
-                e2 = cudaMemcpy(*dst, t.data(), nbytes, cudaMemcpyHostToDevice);
-            }
-            if (e2 != cudaSuccess) return fail(cuda_err(e2, "cudaMemcpy(twiddles)"));
-        }
+        const AxisShape& k = axis == 0 ? kset(precision, lg).row : kset(precision, lg).col;
+        int r2 = axis == 0 ? upload_twiddles(precision, lg, k.lgR, k.TW, &pl->tw_row, &pl->tw_row_i)
+                           : upload_twiddles(precision, lg, k.lgR, k.TW, &pl->tw_col, &pl->tw_col_i);
+        if (r2 != PM_OK) return fail(r2);
     }
     {
         const KernelSet& kr = kset(precision, lgx);
         const KernelSet& kc = kset(precision, lgy);
         cudaError_t e3 = allow_smem(kr.row_iter, pl->rc.smem);
         if (e3 == cudaSuccess) e3 = allow_smem(kr.row_fft, pl->rc.smem);
+        if (e3 == cudaSuccess) e3 = allow_smem(kr.row_final, pl->rc.smem);
         if (e3 == cudaSuccess) e3 = allow_smem(kc.col_iter, pl->cc.smem);
         if (e3 == cudaSuccess) e3 = allow_smem(kc.col_fft, pl->cc.smem);
         if (e3 != cudaSuccess) return fail(cuda_err(e3, "cudaFuncSetAttribute"));
+    }
+    {
+        // persistent cooperative solve kernel (square grids, n >= 128)
+        const KernelSet& ks = kset(precision, lgx);
+        int coop = 0, nsm = 0, per_sm = 0;
+        cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
+        if (n_x == n_y && ks.solve && coop) {
+            cudaError_t e4 = allow_smem(ks.solve, ks.solve_smem);
+            if (e4 == cudaSuccess)
+                e4 = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ks.solve, ks.solve_threads,
+                                                                   ks.solve_smem);
+            if (e4 == cudaSuccess && per_sm > 0) pl->solve_grid = per_sm * nsm;
+            cudaGetLastError();
+        }
+        if (cudaMalloc((void**)&pl->bar, sizeof(GridBar)) != cudaSuccess ||
+            cudaMemset(pl->bar, 0, sizeof(GridBar)) != cudaSuccess)
+            return fail(cuda_err(cudaGetLastError(), "cudaMalloc(barrier)"));
     }
     int r = ensure_capacity(pl, std::max(1, max_batch), 1);
     if (r != PM_OK) return fail(r);
@@ -713,9 +916,13 @@ int pm_plan_destroy(pm_plan* pl) {
     if (pl->stream) cudaStreamSynchronize(pl->stream);
     drop_graphs(pl);
     free_buffers(pl);
+    if (pl->tw_row_i && pl->tw_row_i != pl->tw_row) cudaFree(pl->tw_row_i);
+    if (pl->tw_col_i && pl->tw_col_i != pl->tw_col) cudaFree(pl->tw_col_i);
     if (pl->tw_row) cudaFree(pl->tw_row);
     if (pl->tw_col) cudaFree(pl->tw_col);
     if (pl->red) cudaFree(pl->red);
+    if (pl->bar) cudaFree(pl->bar);
+    if (pl->stamps) cudaFree(pl->stamps);
     if (pl->ev0) cudaEventDestroy(pl->ev0);
     if (pl->ev1) cudaEventDestroy(pl->ev1);
     if (pl->own_stream && pl->stream) cudaStreamDestroy(pl->stream);
@@ -1189,6 +1396,23 @@ int pm_time_sweep(pm_plan* pl, int which, int batch, int reps, float* avg_ms) {
     float ms = 0;
     CK(cudaEventElapsedTime(&ms, pl->ev0, pl->ev1));
     *avg_ms = ms / reps;
+    return PM_OK;
+}
+
+int pm_debug_phase_stamps(pm_plan* pl, int enable, unsigned long long* out, int n) {
+    CKR(check_plan(pl));
+    if (enable) {
+        const size_t n_st = (size_t)std::max(pl->solve_grid, 1) * kStampsPerCta;
+        if (!pl->stamps) CK(cudaMalloc((void**)&pl->stamps, n_st * sizeof(unsigned long long)));
+        CK(cudaMemset(pl->stamps, 0, n_st * sizeof(unsigned long long)));
+        return PM_OK;
+    }
+    if (out && pl->stamps) {
+        CK(cudaStreamSynchronize(pl->stream));
+        const size_t n_st = (size_t)std::max(pl->solve_grid, 1) * kStampsPerCta;
+        CK(cudaMemcpy(out, pl->stamps, std::min<size_t>(n, n_st) * sizeof(unsigned long long),
+                      cudaMemcpyDeviceToHost));
+    }
     return PM_OK;
 }
 

@@ -6,29 +6,47 @@
 
 #if PM_F64
 #define PM_T double
-#define PM_LGR 4
 #define PM_TAG f64
+#ifndef PM_LGR_ROW
+#define PM_LGR_ROW 4
+#endif
+#ifndef PM_LGR_COL
+#define PM_LGR_COL 3
+#endif
 #else
 #define PM_T float
-#define PM_LGR 5
 #define PM_TAG f32
+#ifndef PM_LGR_ROW
+#define PM_LGR_ROW 4
+#endif
+#ifndef PM_LGR_COL
+#define PM_LGR_COL 4
+#endif
 #endif
 #define PM_CAT3_(a, b, c) a##b##_##c
 #define PM_CAT3(a, b, c) PM_CAT3_(a, b, c)
 
 namespace pm {
 KernelSet PM_CAT3(make_set_, PM_TAG, PM_LG)() {
-    using F = FftShape<PM_LG, PM_LGR>;
+    using FR = FftShape<PM_LG, PM_LGR_ROW>;
+    using FC = FftShape<PM_LG, PM_LGR_COL>;
     KernelSet s;
-    s.row_iter = (const void*)&row_iter_kernel<PM_T, PM_LG, PM_LGR>;
-    s.col_iter = (const void*)&col_iter_kernel<PM_T, PM_LG, PM_LGR>;
-    s.row_fft = (const void*)&row_fft_kernel<PM_T, PM_LG, PM_LGR>;
-    s.col_fft = (const void*)&col_fft_kernel<PM_T, PM_LG, PM_LGR>;
-    s.lgR = F::lgR;
-    s.TG = F::TG;
-    s.NP = F::NP;
-    s.SM = F::SM;
-    s.TW = F::TW;
+    s.row_iter = (const void*)&row_iter_kernel<PM_T, PM_LG, PM_LGR_ROW>;
+    s.row_final = (const void*)&row_final_kernel<PM_T, PM_LG, PM_LGR_ROW>;
+    s.row_fft = (const void*)&row_fft_kernel<PM_T, PM_LG, PM_LGR_ROW>;
+    s.col_iter = (const void*)&col_iter_kernel<PM_T, PM_LG, PM_LGR_COL>;
+    s.col_fft = (const void*)&col_fft_kernel<PM_T, PM_LG, PM_LGR_COL>;
+    s.solve = nullptr;
+    s.solve_smem = 0;
+    s.solve_threads = 0;
+    // persistent kernel: square grids n >= 128 whose transforms fit one CTA
+    if constexpr (PM_LG >= 7 && FR::TG <= kSolveThreads && FC::TG <= kSolveThreads) {
+        s.solve = (const void*)&solve_kernel<PM_T, PM_LG, PM_LGR_ROW, PM_LGR_COL>;
+        s.solve_smem = solve_smem_bytes<PM_T, PM_LG, PM_LGR_ROW, PM_LGR_COL>();
+        s.solve_threads = kSolveThreads;
+    }
+    s.row = AxisShape{FR::lgR, FR::TG, FR::NP, FR::SM, FR::TW};
+    s.col = AxisShape{FC::lgR, FC::TG, FC::NP, FC::SM, FC::TW};
     return s;
 }
 }  // namespace pm

@@ -7,38 +7,48 @@
 //   column sweep  (col_iter_kernel):  w -> column FFT -> [metrics of u] ->
 //                 replace modulus with m -> column IFFT -> z
 //   row sweep     (row_iter_kernel):  z -> row IFFT -> P_S with p ->
-//                 row FFT -> w   (or, on the last iterate: v*, u*, mask)
+//                 row FFT -> w
 //
 // Between sweeps the field is held "row-transformed" (w = RowFFT(u)), so the
 // column sweep completes F(u) and the row sweep completes F^-1(v^). Each
 // sweep reads and writes the field once and reads one real grid: 40 B/pixel
-// per iteration in fp32, 80 B in fp64.
+// per iteration in fp32, 80 B in fp64. The best-approximation
+// pair and the mask come from row_final_kernel after the last column sweep.
 //
 // Convergence metrics (gap, err_lit, err_dark; src/metrics.py:67-112) are
 // reduced on the device with a fixed-order tree (per-CTA partials + the last
 // CTA of each mask combining them in index order), so they are bitwise
 // reproducible run to run and independent of batch size. The last CTA of a
-// column sweep also takes the stop decision (max_iters, early stop, host
-// abort, non-finite), so a whole solve runs without host round trips.
+// column sweep also takes the stop decision (max_iters, early stop,
+// non-finite), so a whole solve runs without host round trips; sweeps after
+// the decision exit at their first instruction.
 #pragma once
 #include "pm_fft.cuh"
 
 namespace pm {
 
 constexpr double kTwoPi = 6.283185307179586;   // float64(2*np.pi)
-constexpr int kColPad = 2;                      // extra elements per column buffer (bank spread)
+
+// Elements between the exchange buffers of the C columns of a CTA: the
+// padded transform plus 128/(E*C) so the C columns of a warp's phase land in
+// distinct banks (scripts/bank_sim.py checks every configuration).
+template <typename T, int SM>
+__host__ __device__ __forceinline__ int col_stride(int C) {
+    const int pad = 128 / (int)(sizeof(cx<T>) * C);
+    return SM + (pad > 0 ? pad : 1);
+}
 
 struct MaskState {
-    int stop;        // the current iterate is the last one: next row sweep finalises
-    int done;        // final pair written; all later launches exit immediately
+    int stop;        // the current iterate is the last one: sweeps exit, final runs
+    int done;        // nothing more to do (diverged): every launch exits
     int iters_run;   // SolveResult.iters_run
     int diverged;    // iteration whose iterate went non-finite (0 = never)
     int aborted;     // host requested stop (should_abort)
     int have_prev;   // early stop: a previous gap exists
+    int bad;         // row sweep saw a non-finite value (iteration index)
     int n_records;
-    int pad_;
     double prev_gap;
-    double energy;   // sum |u|^2 of the latest SLM-plane iterate (fp64)
+    double pad_;
 };
 
 struct SolveCtl {
@@ -53,17 +63,27 @@ struct RowArgs {
     cx<T>* field;
     const T* p;
     long long p_stride;       // elements between masks' p (0: shared)
-    const cx<T>* tw;
+    const twe<T>* twf;        // forward twiddles
+    const twe<T>* twi;        // inverse twiddles (fp64: same as twf)
     int nx, ny;
-    T scale;                  // 1/sqrt(nx)
-    const double* tol_p;      // [batch]
-    int mode;                 // 0: no projection (initial iterate), 1: iterate, 2: final
+    T scale;                  // S = 1/sqrt(nx*ny)
+    const double* thr_p;      // [batch] zero-branch threshold on v' = v/S (fp32: on |v'|^2, fp64: on |v'|)
+    int mode;                 // 0: no projection (initial iterate), 1: iterate
     int it;                   // index of the iterate this sweep produces
     MaskState* st;
-    double* part;             // [batch][nblk][2]
-    unsigned* ctr;            // [batch]
-    int nblk;
-    cx<T>* v_star;            // final outputs, nullable
+};
+
+template <typename T>
+struct FinalArgs {
+    const cx<T>* field;
+    const T* p;
+    long long p_stride;
+    const twe<T>* twi;
+    int nx, ny;
+    T scale;
+    const double* tol_p;      // [batch] reference zero_tol (compared to |u|)
+    MaskState* st;
+    cx<T>* v_star;            // outputs, nullable
     cx<T>* u_star;
     double* phases;
     uint8_t* levels;
@@ -74,11 +94,12 @@ struct ColArgs {
     cx<T>* field;
     const T* m;
     long long m_stride;
-    const cx<T>* tw;
+    const twe<T>* twf;
+    const twe<T>* twi;
     int nx, ny;
-    T scale;                  // 1/sqrt(ny)
-    const double* tol_m;      // [batch]
-    const double* energy_target;  // [batch] sum m^2 (fp64)
+    T scale;                  // S = 1/sqrt(nx*ny)
+    const double* thr_m;      // [batch] zero-branch threshold (as thr_p)
+    const double* escale;     // [batch] sum m^2 / sum |u|^2 (reconstructed-intensity scale)
     int mode;                 // 0: init from real m, 1: init from complex field, 2: iterate
     int u_iter;               // metrics of iterate u_{u_iter} (0 = none)
     SolveCtl ctl;
@@ -90,8 +111,19 @@ struct ColArgs {
     int nblk;
 };
 
-__device__ __forceinline__ bool finite2(float2 a) { return isfinite(a.x) && isfinite(a.y); }
-__device__ __forceinline__ bool finite2(double2 a) { return isfinite(a.x) && isfinite(a.y); }
+// Fixed-order warp sum that tolerates partial warps (CTAs of < 32 threads):
+// lanes outside the CTA contribute nothing. Lane 0 holds the result.
+__device__ __forceinline__ double warp_sum(double x) {
+    const unsigned mask = __activemask();
+    const int lane = threadIdx.x & 31;
+    const int nl = min(32, (int)blockDim.x - (int)(threadIdx.x & ~31u));
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+        const double y = __shfl_xor_sync(mask, x, o);
+        if ((lane ^ o) < nl) x += y;
+    }
+    return x;
+}
 
 // Fixed-order block reduction of NV fp64 accumulators into this CTA's
 // partial slot, then a ticket; returns true in the last CTA of the mask,
@@ -105,9 +137,7 @@ __device__ __forceinline__ bool reduce_ticket(double (&acc)[NV], double* part, u
     const int nw = (blockDim.x + 31) >> 5;
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
-        double x = acc[v];
-#pragma unroll
-        for (int o = 16; o >= 1; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        const double x = warp_sum(acc[v]);
         if (lane == 0) wsum[warp][v] = x;
     }
     __syncthreads();
@@ -126,12 +156,12 @@ __device__ __forceinline__ bool reduce_ticket(double (&acc)[NV], double* part, u
     if (!s_last) return false;
     __threadfence();
     if (warp == 0) {
+        const int stride = min(32, (int)blockDim.x);
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
             double x = 0.0;
-            for (int i = lane; i < nblk; i += 32) x += __ldcg(&part[i * NV + v]);
-#pragma unroll
-            for (int o = 16; o >= 1; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+            for (int i = lane; i < nblk; i += stride) x += __ldcg(&part[i * NV + v]);
+            x = warp_sum(x);
             if (lane == 0) tot[v] = x;
         }
     }
@@ -155,97 +185,261 @@ __device__ __forceinline__ uint8_t level_of(double th) {
     return (uint8_t)l;
 }
 
-// ----------------------------------------------------------------- row sweep
+// Groups of <= 32 threads live inside one warp and synchronise with a warp
+// barrier; larger groups use the CTA barrier.
+template <int TG> struct GroupSync { using type = SyncBlock; };
+template <> struct GroupSync<1> { using type = SyncWarp; };
+template <> struct GroupSync<2> { using type = SyncWarp; };
+template <> struct GroupSync<4> { using type = SyncWarp; };
+template <> struct GroupSync<8> { using type = SyncWarp; };
+template <> struct GroupSync<16> { using type = SyncWarp; };
+template <> struct GroupSync<32> { using type = SyncWarp; };
+
+// The synchroniser of row group g: a warp barrier for TG <= 32, else named
+// barrier 1+g over the group's TG threads.
+template <int TG>
+__device__ __forceinline__ auto group_sync(int g) {
+    if constexpr (TG <= 32) return SyncWarp{};
+    else return SyncNamed{1 + g, TG};
+}
+
+template <typename C> __device__ __forceinline__ auto norm_sq(C u) { return u.x * u.x + u.y * u.y; }
+
+// Per-mask decision after the metrics of iterate u_i are reduced: record,
+// early stop, divergence, max_iters (src/solver.py:173-199). Runs in one
+// thread; `tot` = {gap^2, err_lit, err_dark}.
+__device__ __forceinline__ void decide(MaskState* st, double* hist_row, const SolveCtl& ctl, int i, bool rec,
+                                       const double (&tot)[3]) {
+    const double g = sqrt(tot[0]);
+    int stop = 0;
+    if (!isfinite(tot[0]) || st->bad) {
+        st->diverged = st->bad ? st->bad : i;
+        st->done = 1;
+        stop = 1;
+    }
+    if (rec) {
+        hist_row[0] = g; hist_row[1] = tot[1]; hist_row[2] = tot[2]; hist_row[3] = 1.0;
+        st->n_records += 1;
+    }
+    if (ctl.early_tol >= 0.0) {
+        if (st->have_prev && g > 0.0 && fabs(g - st->prev_gap) <= ctl.early_tol * g) stop = 1;
+        st->prev_gap = g;
+        st->have_prev = 1;
+    }
+    if (i >= ctl.max_iters) stop = 1;
+    if (stop) {
+        st->stop = 1;
+        st->iters_run = i;
+    }
+}
+
+// Cross-CTA field loads bypass L1 (the field is rewritten between phases).
+template <typename C> __device__ __forceinline__ C ld_field(const C* p) { return __ldcg(p); }
+
+// ------------------------------------------------------------------ tasks
+// Scaling convention: the field holds UNNORMALISED half transforms between
+// phases (w' = RowFFT(u), z' = ColIFFT(v^)); the unitary factor
+// S = 1/sqrt(n_x n_y) is applied once per iteration, where the column phase
+// forms u^ = F(u) = S * ColFFT(w'). The row projection works on
+// v' = RowIFFT(z') = v / S, with its zero-branch threshold pre-scaled on the
+// host (exact for power-of-two grids, where S is a power of two), because
+// P_S(v) = P_S(v / S).
+
+// A row task: the TG threads of group g transform one row. `act` == false
+// runs the same instruction stream on zeros without touching memory, so
+// group barriers stay aligned when a CTA has fewer rows than groups.
+template <typename T, int LG_L, int LG_R, class Sync>
+__device__ __forceinline__ void row_task(const RowArgs<T>& a, int b, int row, int j, cx<T>* sm, bool act,
+                                         Sync sync) {
+    using F = FftShape<LG_L, LG_R>;
+    const size_t N = (size_t)a.nx * a.ny;
+    cx<T>* f = a.field + b * N + (size_t)row * a.nx + j;
+    const T* p = a.p + b * a.p_stride + (size_t)row * a.nx + j;
+    cx<T> v[F::R];
+#pragma unroll
+    for (int k = 0; k < F::R; ++k) v[k] = act ? ld_field(f + F::TG * k) : mk<T>(T(0), T(0));
+    fft1d<T, LG_L, LG_R, +1>(v, sm, a.twi, j, sync);                 // v' = RowIFFT(z')
+    if (a.mode == 1) {
+        // u = P_S v = P_S v' (src/projections.py:69-74), threshold pre-scaled
+        const T thr = T(a.thr_p[b]);
+        T chk = T(0);
+#pragma unroll
+        for (int k = 0; k < F::R; ++k) {
+            T s2;
+            v[k] = replace_mod(v[k], act ? p[F::TG * k] : T(0), thr, s2);
+            chk += s2;                              // non-finite detector (reference Field checks)
+        }
+        if (act && !isfinite(chk)) atomicMax(&a.st[b].bad, a.it);
+    } else {
+#pragma unroll
+        for (int k = 0; k < F::R; ++k) v[k] = cscale(v[k], a.scale);  // u0 = S * v'
+    }
+    fft1d<T, LG_L, LG_R, -1>(v, sm, a.twf, j, sync);                 // w' = RowFFT(u)
+    if (act) {
+#pragma unroll
+        for (int k = 0; k < F::R; ++k) f[F::TG * k] = v[k];
+    }
+}
+
+// Best-approximation pair for one row: v* = P_M u_K = S * RowIFFT(z'),
+// u* = P_S v*, mask = phases_of(u*, zero_tol_p)
+// (src/solver.py:201-206, src/grid.py:168-176).
+template <typename T, int LG_L, int LG_R, class Sync>
+__device__ __forceinline__ void final_task(const FinalArgs<T>& a, int b, int row, int j, cx<T>* sm, bool act,
+                                           Sync sync) {
+    using F = FftShape<LG_L, LG_R>;
+    const size_t N = (size_t)a.nx * a.ny;
+    const size_t o = b * N + (size_t)row * a.nx + j;
+    const T* p = a.p + b * a.p_stride + (size_t)row * a.nx + j;
+    cx<T> v[F::R];
+#pragma unroll
+    for (int k = 0; k < F::R; ++k) v[k] = act ? ld_field(a.field + o + F::TG * k) : mk<T>(T(0), T(0));
+    fft1d<T, LG_L, LG_R, +1>(v, sm, a.twi, j, sync);
+    if (!act) return;
+    const T tol = T(a.tol_p[b]);
+#pragma unroll
+    for (int k = 0; k < F::R; ++k) {
+        const size_t x = o + F::TG * k;
+        const cx<T> vs = cscale(v[k], a.scale);
+        if (a.v_star) a.v_star[x] = vs;
+        const cx<T> us = replace_mod_exact<T>(vs, p[F::TG * k], tol);
+        if (a.u_star) a.u_star[x] = us;
+        if (a.phases || a.levels) {
+            double th = phase_of((double)us.x, (double)us.y);
+            const T mag = sqrt(us.x * us.x + us.y * us.y);
+            if (tol > T(0) && mag < tol) th = 0.0;
+            if (a.phases) a.phases[x] = th;
+            if (a.levels) a.levels[x] = level_of(th);
+        }
+    }
+}
+
+// A column task: C interleaved transforms (thread c + C*j) over columns
+// col0..col0+C-1 of mask b. NX > 0 fixes n_x at compile time (square
+// persistent path) so every column access is base + immediate offset.
+template <typename T, int LG_L, int LG_R, int NX>
+__device__ __forceinline__ void col_task(const ColArgs<T>& a, int b, int col0, int C, cx<T>* smbase, bool act,
+                                         double (&acc)[3]) {
+    using F = FftShape<LG_L, LG_R>;
+    const int c = threadIdx.x % C, j = threadIdx.x / C;
+    const size_t nx = NX > 0 ? (size_t)NX : (size_t)a.nx;
+    const size_t N = nx * a.ny;
+    const size_t rs = nx * F::TG;                    // stride between a thread's elements
+    cx<T>* sm = smbase + c * col_stride<T, F::SM>(C);
+    cx<T>* f = a.field + b * N + (size_t)j * nx + col0 + c;
+    const T* m = a.m + b * a.m_stride + (size_t)j * nx + col0 + c;
+    acc[0] = acc[1] = acc[2] = 0.0;
+
+    cx<T> v[F::R];
+    if (a.mode == 0) {
+#pragma unroll
+        for (int k = 0; k < F::R; ++k) v[k] = mk<T>(act ? m[k * rs] : T(0), T(0));
+    } else {
+#pragma unroll
+        for (int k = 0; k < F::R; ++k) v[k] = act ? ld_field(f + k * rs) : mk<T>(T(0), T(0));
+    }
+    if (a.mode < 2) {
+        // initial iterate u0 = F^-1(m e^{i0}): unnormalised column half
+        // (src/solver.py:93-108); the row phase applies S
+        fft1d<T, LG_L, LG_R, +1>(v, sm, a.twi, j, SyncBlock{});
+        if (act) {
+#pragma unroll
+            for (int k = 0; k < F::R; ++k) f[k * rs] = v[k];
+        }
+        return;
+    }
+    fft1d<T, LG_L, LG_R, -1>(v, sm, a.twf, j, SyncBlock{});
+#pragma unroll
+    for (int k = 0; k < F::R; ++k) v[k] = cscale(v[k], a.scale);     // u^ = F(u) = S * ColFFT(w')
+
+    const bool metr = a.u_iter >= 1;
+    const bool rec = metr && ((a.u_iter - 1) % a.ctl.record_every == 0);
+    const T thr = T(a.thr_m[b]);
+    T mm[F::R];
+#pragma unroll
+    for (int k = 0; k < F::R; ++k) mm[k] = act ? m[k * rs] : T(0);
+    if (rec && act) {
+        // reconstructed intensity and physical error (src/metrics.py:74-112);
+        // the energy scale is sum m^2 / sum |u|^2 (Parseval: sum |F u|^2 = sum |u|^2)
+        const double sc = a.escale[b];
+#pragma unroll
+        for (int k = 0; k < F::R; ++k) {
+            const double inten = (double)norm_sq(v[k]) * sc;
+            const double m2 = (double)mm[k] * (double)mm[k];
+            if (m2 > 0.0) {
+                const double dev = fabs(m2 - inten);
+                if (dev > a.ctl.t_lit * m2 && dev / m2 > a.ctl.t_lit)
+                    acc[1] += a.ctl.t_dark * dev / (a.ctl.t_lit * m2) - a.ctl.t_dark;
+            } else if (inten > a.ctl.t_dark) {
+                acc[2] += inten - a.ctl.t_dark;
+            }
+        }
+    }
+    T g2 = T(0);
+#pragma unroll
+    for (int k = 0; k < F::R; ++k) {
+        const cx<T> vh = replace_mod(v[k], mm[k], thr);     // v^ = replace_m(u^)
+        // G(u) = ||P_S u - P_M u|| = ||u^ - v^||  (Parseval; u is on S)
+        g2 += norm_sq(csub(v[k], vh));
+        v[k] = vh;
+    }
+    acc[0] = act ? (double)g2 : 0.0;
+    fft1d<T, LG_L, LG_R, +1>(v, sm, a.twi, j, SyncBlock{});         // z' = ColIFFT(v^)
+    if (act) {
+#pragma unroll
+        for (int k = 0; k < F::R; ++k) f[k * rs] = v[k];
+    }
+}
+
+// Fixed-order CTA sum of NV accumulators; thread 0 gets the totals.
+template <int NV>
+__device__ __forceinline__ void block_reduce(double (&acc)[NV], double (&tot)[NV]) {
+    __shared__ double wsum[32][NV];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+        const double x = warp_sum(acc[v]);
+        if (lane == 0) wsum[warp][v] = x;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+            double s = 0.0;
+            for (int w = 0; w < nw; ++w) s += wsum[w][v];
+            tot[v] = s;
+        }
+    }
+    __syncthreads();
+}
+
+// ------------------------------------------------------------ sweep kernels
+// One launch per sweep (general path: any power-of-two n_x x n_y).
 template <typename T, int LG_L, int LG_R>
 __global__ void __launch_bounds__(256) row_iter_kernel(RowArgs<T> a) {
     using F = FftShape<LG_L, LG_R>;
     extern __shared__ __align__(16) unsigned char smraw[];
     const int b = blockIdx.y;
-    MaskState* st = a.st + b;
-    if (st->done) return;
-    const bool fin = a.mode == 2 || st->stop;
+    if (a.st[b].stop | a.st[b].done) return;
     const int G = blockDim.x / F::TG;
     const int g = threadIdx.x / F::TG, j = threadIdx.x % F::TG;
-    const int row = blockIdx.x * G + g;
-    const size_t N = (size_t)a.nx * a.ny;
-    cx<T>* sm = reinterpret_cast<cx<T>*>(smraw) + g * F::SM;
-    cx<T>* f = a.field + b * N + (size_t)row * a.nx;
-    const T* p = a.p + b * a.p_stride + (size_t)row * a.nx;
-
-    cx<T> v[F::R];
-#pragma unroll
-    for (int k = 0; k < F::R; ++k) v[k] = f[j + F::TG * k];
-
-    double acc[2] = {0.0, 0.0};   // energy sum |u|^2, non-finite count
-    if constexpr (F::TG <= 32) {
-        fft1d<T, LG_L, LG_R, +1>(v, sm, a.tw, j, SyncWarp{});
-    } else {
-        fft1d<T, LG_L, LG_R, +1>(v, sm, a.tw, j, SyncBlock{});
-    }
-    const T tol = T(a.tol_p[b]);
-#pragma unroll
-    for (int k = 0; k < F::R; ++k) { v[k].x *= a.scale; v[k].y *= a.scale; }
-
-    if (fin) {
-        // Best-approximation pair: v* = P_M u_K (this row's IFFT), u* = P_S v*,
-        // mask = phases_of(u*, tol_p)  (src/solver.py:201-206).
-        const size_t o = b * N + (size_t)row * a.nx;
-#pragma unroll
-        for (int k = 0; k < F::R; ++k) {
-            const int x = j + F::TG * k;
-            const cx<T> vs = v[k];
-            if (!finite2(vs)) acc[1] += 1.0;
-            if (a.v_star) a.v_star[o + x] = vs;
-            const cx<T> us = replace_mod(vs, p[x], tol);
-            if (a.u_star) a.u_star[o + x] = us;
-            double th = phase_of((double)us.x, (double)us.y);
-            const T mag = sqrt(us.x * us.x + us.y * us.y);
-            if (tol > T(0) && mag < tol) th = 0.0;
-            if (a.phases) a.phases[o + x] = th;
-            if (a.levels) a.levels[o + x] = level_of(th);
-        }
-    } else {
-        if (a.mode == 1) {
-#pragma unroll
-            for (int k = 0; k < F::R; ++k) {
-                if (!finite2(v[k])) acc[1] += 1.0;
-                v[k] = replace_mod(v[k], p[j + F::TG * k], tol);
-                acc[0] += (double)v[k].x * (double)v[k].x + (double)v[k].y * (double)v[k].y;
-            }
-        }
-        if constexpr (F::TG <= 32) {
-            fft1d<T, LG_L, LG_R, -1>(v, sm, a.tw, j, SyncWarp{});
-        } else {
-            fft1d<T, LG_L, LG_R, -1>(v, sm, a.tw, j, SyncBlock{});
-        }
-#pragma unroll
-        for (int k = 0; k < F::R; ++k) {
-            v[k].x *= a.scale; v[k].y *= a.scale;
-            f[j + F::TG * k] = v[k];
-        }
-        if (a.mode == 0) return;   // initial iterate: nothing to reduce
-    }
-
-    double tot[2];
-    if (reduce_ticket<2>(acc, a.part + (size_t)b * a.nblk * 2, a.ctr + b, a.nblk, blockIdx.x, tot)) {
-        if (threadIdx.x == 0) {
-            if (fin) {
-                if (tot[1] != 0.0 && st->diverged == 0) st->diverged = st->iters_run > 0 ? st->iters_run : 1;
-                st->done = 1;
-            } else {
-                st->energy = tot[0];
-                if (tot[1] != 0.0 || !isfinite(tot[0])) {
-                    st->diverged = a.it;
-                    st->iters_run = a.it;
-                    st->stop = 1;
-                    st->done = 1;
-                }
-            }
-        }
-    }
+    row_task<T, LG_L, LG_R>(a, b, blockIdx.x * G + g, j, reinterpret_cast<cx<T>*>(smraw) + g * F::SM, true,
+                            group_sync<F::TG>(g));
 }
 
-// -------------------------------------------------------------- column sweep
+template <typename T, int LG_L, int LG_R>
+__global__ void __launch_bounds__(256) row_final_kernel(FinalArgs<T> a) {
+    using F = FftShape<LG_L, LG_R>;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    const int b = blockIdx.y;
+    if (a.st[b].done) return;
+    const int G = blockDim.x / F::TG;
+    const int g = threadIdx.x / F::TG, j = threadIdx.x % F::TG;
+    final_task<T, LG_L, LG_R>(a, b, blockIdx.x * G + g, j, reinterpret_cast<cx<T>*>(smraw) + g * F::SM, true,
+                              group_sync<F::TG>(g));
+}
+
 // Largest CTA a column kernel is launched with (see col_config in pm_capi.cu):
 // 256 threads while a transform needs <= 64 threads, else 512.
 template <int LG_L, int LG_R>
@@ -257,152 +451,278 @@ __global__ void __launch_bounds__(col_max_threads<LG_L, LG_R>()) col_iter_kernel
     extern __shared__ __align__(16) unsigned char smraw[];
     const int b = blockIdx.y;
     MaskState* st = a.st + b;
-    if (st->done) return;
+    if (st->stop | st->done) return;
     const int C = blockDim.x / F::TG;
-    const int c = threadIdx.x % C, j = threadIdx.x / C;
-    const int col = blockIdx.x * C + c;
-    const size_t N = (size_t)a.nx * a.ny;
-    const size_t nx = a.nx;
-    cx<T>* sm = reinterpret_cast<cx<T>*>(smraw) + c * (F::SM + kColPad);
-    cx<T>* f = a.field + b * N + col;
-    const T* m = a.m + b * a.m_stride + col;
-
-    cx<T> v[F::R];
-    if (a.mode == 0) {
-#pragma unroll
-        for (int k = 0; k < F::R; ++k) v[k] = mk<T>(m[(j + F::TG * k) * nx], T(0));
-    } else {
-#pragma unroll
-        for (int k = 0; k < F::R; ++k) v[k] = f[(j + F::TG * k) * nx];
-    }
-    if (a.mode < 2) {
-        // initial iterate u0 = F^-1(m e^{i0}), column half (src/solver.py:93-108)
-        fft1d<T, LG_L, LG_R, +1>(v, sm, a.tw, j, SyncBlock{});
-#pragma unroll
-        for (int k = 0; k < F::R; ++k) {
-            v[k].x *= a.scale; v[k].y *= a.scale;
-            f[(j + F::TG * k) * nx] = v[k];
-        }
-        return;
-    }
-    fft1d<T, LG_L, LG_R, -1>(v, sm, a.tw, j, SyncBlock{});
-
-    const bool metr = a.u_iter >= 1;
-    const bool rec = metr && ((a.u_iter - 1) % a.ctl.record_every == 0);
-    const T tol = T(a.tol_m[b]);
-    const double s = rec ? a.energy_target[b] / st->energy : 0.0;
-    double acc[3] = {0.0, 0.0, 0.0};   // gap^2, err_lit, err_dark
-#pragma unroll
-    for (int k = 0; k < F::R; ++k) {
-        const T mm = m[(j + F::TG * k) * nx];
-        cx<T> u = v[k];
-        u.x *= a.scale; u.y *= a.scale;                    // u^ = F(u)
-        const cx<T> vh = replace_mod(u, mm, tol);          // v^ = replace_m(u^)
-        if (metr) {
-            // G(u) = ||P_S u - P_M u|| = ||u^ - v^|| (Parseval; u is on S)
-            const double dx = (double)(u.x - vh.x), dy = (double)(u.y - vh.y);
-            acc[0] += dx * dx + dy * dy;
-            if (rec) {
-                // reconstructed intensity and physical error (src/metrics.py:74-112)
-                const double inten = ((double)u.x * (double)u.x + (double)u.y * (double)u.y) * s;
-                const double m2 = (double)mm * (double)mm;
-                if (m2 > 0.0) {
-                    const double dev = fabs(m2 - inten);
-                    if (dev / m2 > a.ctl.t_lit)
-                        acc[1] += a.ctl.t_dark * dev / (a.ctl.t_lit * m2) - a.ctl.t_dark;
-                } else if (inten > a.ctl.t_dark) {
-                    acc[2] += inten - a.ctl.t_dark;
-                }
-            }
-        }
-        v[k] = vh;
-    }
-    fft1d<T, LG_L, LG_R, +1>(v, sm, a.tw, j, SyncBlock{});
-#pragma unroll
-    for (int k = 0; k < F::R; ++k) {
-        v[k].x *= a.scale; v[k].y *= a.scale;
-        f[(j + F::TG * k) * nx] = v[k];
-    }
-    if (!metr) return;
-
+    double acc[3];
+    col_task<T, LG_L, LG_R, 0>(a, b, blockIdx.x * C, C, reinterpret_cast<cx<T>*>(smraw), true, acc);
+    if (a.mode < 2 || a.u_iter < 1) return;
     double tot[3];
     if (reduce_ticket<3>(acc, a.part + (size_t)b * a.nblk * 3, a.ctr + b, a.nblk, blockIdx.x, tot)) {
         if (threadIdx.x == 0) {
-            // record / early-stop / abort logic of src/solver.py:173-199 for u_i
             const int i = a.u_iter;
-            const double g = sqrt(tot[0]);
-            double* h = a.hist + ((size_t)b * a.hist_stride + (i - 1)) * 4;
-            int stop = 0;
-            if (!isfinite(tot[0])) {
-                st->diverged = i;
-                stop = 1;
+            decide(st, a.hist + ((size_t)b * a.hist_stride + (i - 1)) * 4, a.ctl, i,
+                   (i - 1) % a.ctl.record_every == 0, tot);
+        }
+    }
+}
+
+// -------------------------------------------------------- persistent solve
+// The whole solve in one cooperative launch: one CTA per SM, phases
+// separated by a grid barrier instead of kernel boundaries (a kernel
+// boundary costs several microseconds on B200, a barrier about one).
+struct GridBar {
+    unsigned count;   // arrivals, monotonic within a launch (zeroed before it)
+    unsigned gen;     // released epoch
+};
+
+__device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Grid barrier: every CTA releases one arrival (no returned atomic), CTA 0
+// alone polls the arrival count and publishes the epoch, the others poll the
+// epoch word. `epoch` counts this launch's barriers (identical in all CTAs).
+__device__ __forceinline__ void grid_sync(GridBar* bar, unsigned& epoch) {
+    __syncthreads();
+    ++epoch;
+    if (threadIdx.x == 0) {
+        red_release_add(&bar->count, 1u);
+        if (blockIdx.x == 0) {
+            const unsigned target = epoch * gridDim.x;
+            while (ld_acquire(&bar->count) < target) {
             }
-            if (rec) {
-                h[0] = g; h[1] = tot[1]; h[2] = tot[2]; h[3] = 1.0;
-                st->n_records += 1;
-            }
-            if (a.ctl.early_tol >= 0.0) {
-                if (st->have_prev && g > 0.0 && fabs(g - st->prev_gap) <= a.ctl.early_tol * g) stop = 1;
-                st->prev_gap = g;
-                st->have_prev = 1;
-            }
-            if (i >= a.ctl.max_iters) stop = 1;
-            if (stop) {
-                st->stop = 1;
-                st->iters_run = i;
-                if (st->diverged) st->done = 1;
+            st_release(&bar->gen, epoch);
+        } else {
+            while (ld_acquire(&bar->gen) < epoch) __nanosleep(16);
+        }
+    }
+    __syncthreads();
+}
+
+template <typename T>
+struct SolveArgs {
+    RowArgs<T> row;
+    ColArgs<T> col;
+    FinalArgs<T> fin;
+    GridBar* bar;
+    int batch;
+    int it_begin, it_end;      // iterations it_begin..it_end-1 (row it, col it)
+    int do_init;               // run the initial-iterate phases first
+    int do_final;              // finish with the best-approximation pair
+    int init_mode;             // column init from real m (0) or complex field (1)
+    unsigned long long* stamps; // optional: globaltimer at every phase boundary (CTA 0)
+};
+
+// stamps[cta * kStampsPerCta + i] = %globaltimer at the i-th stamp point.
+constexpr int kStampsPerCta = 256;
+__device__ __forceinline__ void stamp(unsigned long long* s, int& i) {
+    if (s && threadIdx.x == 0 && i < kStampsPerCta) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        s[blockIdx.x * kStampsPerCta + i] = t;
+    }
+    ++i;
+}
+
+__device__ __forceinline__ bool mask_live(const MaskState* st) {
+    return !(__ldcg(&st->stop) | __ldcg(&st->done));
+}
+
+template <typename T, int LG, int LGR_R, int LGR_C>
+__device__ __forceinline__ void row_phase(const RowArgs<T>& a, int batch, cx<T>* smem) {
+    using F = FftShape<LG, LGR_R>;
+    const int G = blockDim.x / F::TG;
+    const int g = threadIdx.x / F::TG, j = threadIdx.x % F::TG;
+    const int total = batch << LG;
+    for (int base = blockIdx.x * G; base < total; base += gridDim.x * G) {
+        const int r = base + g;
+        const int b = r >> LG;
+        const bool act = r < total && mask_live(a.st + (r < total ? b : 0));
+        row_task<T, LG, LGR_R>(a, r < total ? b : 0, r & ((1 << LG) - 1), j, smem + g * F::SM, act,
+                               group_sync<F::TG>(g));
+    }
+}
+
+template <typename T, int LG, int LGR_R, int LGR_C>
+__device__ __forceinline__ void final_phase(const FinalArgs<T>& a, int batch, cx<T>* smem) {
+    using F = FftShape<LG, LGR_R>;
+    const int G = blockDim.x / F::TG;
+    const int g = threadIdx.x / F::TG, j = threadIdx.x % F::TG;
+    const int total = batch << LG;
+    for (int base = blockIdx.x * G; base < total; base += gridDim.x * G) {
+        const int r = base + g;
+        const int b = r < total ? (r >> LG) : 0;
+        const bool act = r < total && !__ldcg(&a.st[b].done);
+        final_task<T, LG, LGR_R>(a, b, r & ((1 << LG) - 1), j, smem + g * F::SM, act, group_sync<F::TG>(g));
+    }
+}
+
+// Column phase; with metrics, task t of mask b leaves its block sum in
+// part[b][t] so the per-mask total is combined in task order (independent of
+// which CTA ran which task, hence of batch size and grid size).
+template <typename T, int LG, int LGR_R, int LGR_C>
+__device__ __forceinline__ void col_phase(const ColArgs<T>& a, int batch, cx<T>* smem) {
+    using F = FftShape<LG, LGR_C>;
+    const int C = blockDim.x / F::TG;
+    const int tpm = (1 << LG) / C;          // tasks per mask
+    const int total = batch * tpm;
+    const bool metr = a.mode == 2 && a.u_iter >= 1;
+    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        const int b = t / tpm, tt = t - b * tpm;
+        const bool act = mask_live(a.st + b);
+        double acc[3];
+        col_task<T, LG, LGR_C, (1 << LG)>(a, b, tt * C, C, smem, act, acc);
+        if (metr && act) {
+            double tot[3];
+            block_reduce<3>(acc, tot);
+            if (threadIdx.x == 0) {
+                double* q = a.part + ((size_t)b * tpm + tt) * 3;
+                q[0] = tot[0]; q[1] = tot[1]; q[2] = tot[2];
             }
         }
     }
+}
+
+// Per-mask reduction of the column phase's task partials and the stop
+// decision, by CTA (b mod grid).
+template <typename T, int LG, int LGR_C>
+__device__ __forceinline__ void decide_phase(const ColArgs<T>& a, int batch) {
+    using F = FftShape<LG, LGR_C>;
+    const int C = blockDim.x / F::TG;
+    const int tpm = (1 << LG) / C;
+    const int lane = threadIdx.x & 31;
+    if (threadIdx.x >= 32) return;
+    for (int b = blockIdx.x; b < batch; b += gridDim.x) {
+        MaskState* st = a.st + b;
+        if (!mask_live(st)) continue;
+        double tot[3];
+#pragma unroll
+        for (int v = 0; v < 3; ++v) {
+            double x = 0.0;
+            for (int i = lane; i < tpm; i += 32) x += __ldcg(&a.part[((size_t)b * tpm + i) * 3 + v]);
+#pragma unroll
+            for (int o = 16; o >= 1; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+            tot[v] = x;
+        }
+        if (lane == 0) {
+            const int i = a.u_iter;
+            decide(st, a.hist + ((size_t)b * a.hist_stride + (i - 1)) * 4, a.ctl, i,
+                   (i - 1) % a.ctl.record_every == 0, tot);
+        }
+    }
+}
+
+#ifndef PM_SOLVE_NT
+#define PM_SOLVE_NT 512
+#endif
+constexpr int kSolveThreads = PM_SOLVE_NT;
+
+// Dynamic shared memory of solve_kernel: the larger of the row phase
+// (512/TG_row transforms) and the column phase (512/TG_col interleaved).
+template <typename T, int LG, int LGR_R, int LGR_C>
+__host__ __device__ constexpr int solve_smem_bytes() {
+    using FR = FftShape<LG, LGR_R>;
+    using FC = FftShape<LG, LGR_C>;
+    constexpr int rows = (kSolveThreads / FR::TG > 0 ? kSolveThreads / FR::TG : 1) * FR::SM;
+    constexpr int C = kSolveThreads / FC::TG > 0 ? kSolveThreads / FC::TG : 1;
+    constexpr int pad = 128 / (int)(sizeof(cx<T>) * C) > 0 ? 128 / (int)(sizeof(cx<T>) * C) : 1;
+    constexpr int cols = FC::SM ? C * (FC::SM + pad) : 0;
+    return (int)sizeof(cx<T>) * (rows > cols ? rows : cols);
+}
+
+template <typename T, int LG, int LGR_R, int LGR_C>
+__global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(SolveArgs<T> a) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    cx<T>* smem = reinterpret_cast<cx<T>*>(smraw);
+    const int B = a.batch;
+    int si = 0;
+    unsigned epoch = 0;
+    stamp(a.stamps, si);
+    if (a.do_init) {
+        ColArgs<T> c = a.col;
+        c.mode = a.init_mode;
+        c.u_iter = 0;
+        col_phase<T, LG, LGR_R, LGR_C>(c, B, smem);       // u0 column half
+        grid_sync(a.bar, epoch);
+        RowArgs<T> r = a.row;
+        r.mode = 0;
+        row_phase<T, LG, LGR_R, LGR_C>(r, B, smem);       // u0 row half, w0
+        grid_sync(a.bar, epoch);
+        c.mode = 2;
+        col_phase<T, LG, LGR_R, LGR_C>(c, B, smem);       // z1
+        grid_sync(a.bar, epoch);
+    }
+    const bool early = a.col.ctl.early_tol >= 0.0;
+    for (int it = a.it_begin; it < a.it_end; ++it) {
+        RowArgs<T> r = a.row;
+        r.mode = 1;
+        r.it = it;
+        row_phase<T, LG, LGR_R, LGR_C>(r, B, smem);       // u_it, w_it
+        stamp(a.stamps, si);
+        grid_sync(a.bar, epoch);
+        stamp(a.stamps, si);
+        ColArgs<T> c = a.col;
+        c.mode = 2;
+        c.u_iter = it;
+        col_phase<T, LG, LGR_R, LGR_C>(c, B, smem);       // metrics of u_it, z_{it+1}
+        stamp(a.stamps, si);
+        grid_sync(a.bar, epoch);
+        stamp(a.stamps, si);
+        decide_phase<T, LG, LGR_C>(c, B);
+        if (early) grid_sync(a.bar, epoch);                      // stop flags must be seen by every CTA
+    }
+    if (a.do_final) final_phase<T, LG, LGR_R, LGR_C>(a.fin, B, smem);
+    stamp(a.stamps, si);
 }
 
 // ------------------------------------------------ standalone transform sweeps
 // FftProvider.forward / inverse (src/transform.py:47-55): one axis per launch.
+// `tw` is the table for `dir` (fp32) or the forward table (fp64).
 template <typename T, int LG_L, int LG_R>
-__global__ void __launch_bounds__(256) row_fft_kernel(const cx<T>* in, cx<T>* out, const cx<T>* tw,
+__global__ void __launch_bounds__(256) row_fft_kernel(const cx<T>* in, cx<T>* out, const twe<T>* tw,
                                                       int nx, int ny, T scale, int dir) {
     using F = FftShape<LG_L, LG_R>;
+    using Sync = typename GroupSync<F::TG>::type;
     extern __shared__ __align__(16) unsigned char smraw[];
     const int G = blockDim.x / F::TG;
     const int g = threadIdx.x / F::TG, j = threadIdx.x % F::TG;
-    const size_t o = (size_t)blockIdx.y * nx * ny + (size_t)(blockIdx.x * G + g) * nx;
+    const size_t o = (size_t)blockIdx.y * nx * ny + (size_t)(blockIdx.x * G + g) * nx + j;
     cx<T>* sm = reinterpret_cast<cx<T>*>(smraw) + g * F::SM;
     cx<T> v[F::R];
 #pragma unroll
-    for (int k = 0; k < F::R; ++k) v[k] = in[o + j + F::TG * k];
-    if constexpr (F::TG <= 32) {
-        if (dir < 0) fft1d<T, LG_L, LG_R, -1>(v, sm, tw, j, SyncWarp{});
-        else fft1d<T, LG_L, LG_R, +1>(v, sm, tw, j, SyncWarp{});
-    } else {
-        if (dir < 0) fft1d<T, LG_L, LG_R, -1>(v, sm, tw, j, SyncBlock{});
-        else fft1d<T, LG_L, LG_R, +1>(v, sm, tw, j, SyncBlock{});
-    }
+    for (int k = 0; k < F::R; ++k) v[k] = in[o + F::TG * k];
+    if (dir < 0) fft1d<T, LG_L, LG_R, -1>(v, sm, tw, j, Sync{});
+    else fft1d<T, LG_L, LG_R, +1>(v, sm, tw, j, Sync{});
 #pragma unroll
-    for (int k = 0; k < F::R; ++k) {
-        v[k].x *= scale; v[k].y *= scale;
-        out[o + j + F::TG * k] = v[k];
-    }
+    for (int k = 0; k < F::R; ++k) out[o + F::TG * k] = cscale(v[k], scale);
 }
 
 template <typename T, int LG_L, int LG_R>
-__global__ void __launch_bounds__(col_max_threads<LG_L, LG_R>()) col_fft_kernel(const cx<T>* in, cx<T>* out, const cx<T>* tw,
-                                                       int nx, int ny, T scale, int dir) {
+__global__ void __launch_bounds__(col_max_threads<LG_L, LG_R>()) col_fft_kernel(const cx<T>* in, cx<T>* out,
+                                                                              const twe<T>* tw, int nx, int ny,
+                                                                              T scale, int dir) {
     using F = FftShape<LG_L, LG_R>;
     extern __shared__ __align__(16) unsigned char smraw[];
     const int C = blockDim.x / F::TG;
     const int c = threadIdx.x % C, j = threadIdx.x / C;
-    const size_t o = (size_t)blockIdx.y * nx * ny + (size_t)(blockIdx.x * C + c);
-    cx<T>* sm = reinterpret_cast<cx<T>*>(smraw) + c * (F::SM + kColPad);
+    const size_t o = (size_t)blockIdx.y * nx * ny + (size_t)j * nx + (size_t)(blockIdx.x * C + c);
+    const size_t rs = (size_t)nx * F::TG;
+    cx<T>* sm = reinterpret_cast<cx<T>*>(smraw) + c * col_stride<T, F::SM>(C);
     cx<T> v[F::R];
 #pragma unroll
-    for (int k = 0; k < F::R; ++k) v[k] = in[o + (size_t)(j + F::TG * k) * nx];
+    for (int k = 0; k < F::R; ++k) v[k] = in[o + k * rs];
     if (dir < 0) fft1d<T, LG_L, LG_R, -1>(v, sm, tw, j, SyncBlock{});
     else fft1d<T, LG_L, LG_R, +1>(v, sm, tw, j, SyncBlock{});
 #pragma unroll
-    for (int k = 0; k < F::R; ++k) {
-        v[k].x *= scale; v[k].y *= scale;
-        out[o + (size_t)(j + F::TG * k) * nx] = v[k];
-    }
+    for (int k = 0; k < F::R; ++k) out[o + k * rs] = cscale(v[k], scale);
 }
 
 }  // namespace pm

@@ -4,11 +4,7 @@
 
 namespace pm {
 
-struct KernelSet {
-    const void* row_iter;   // row_iter_kernel<T, lg, lgR>
-    const void* col_iter;   // col_iter_kernel<T, lg, lgR>
-    const void* row_fft;    // row_fft_kernel<T, lg, lgR>
-    const void* col_fft;    // col_fft_kernel<T, lg, lgR>
+struct AxisShape {
     int lgR;                // log2 points per thread
     int TG;                 // threads per transform
     int NP;                 // Stockham passes
@@ -16,7 +12,22 @@ struct KernelSet {
     int TW;                 // twiddle-table entries
 };
 
+// Row kernels (contiguous axis, length n_x) and column kernels (strided
+// axis, length n_y) may use different points-per-thread.
+struct KernelSet {
+    const void* row_iter;   // row_iter_kernel<T, lg, lgR_row>
+    const void* row_final;  // row_final_kernel<T, lg, lgR_row>
+    const void* row_fft;    // row_fft_kernel<T, lg, lgR_row>
+    const void* col_iter;   // col_iter_kernel<T, lg, lgR_col>
+    const void* col_fft;    // col_fft_kernel<T, lg, lgR_col>
+    const void* solve;      // solve_kernel<T, lg, lgR_row, lgR_col> (square grids, lg >= 7) or null
+    int solve_smem;         // its dynamic shared memory (bytes)
+    int solve_threads;      // its CTA size
+    AxisShape row, col;
+};
+
 constexpr int kMaxLg = 12;  // n_x, n_y up to 4096
+
 
 const KernelSet& kernels_f32(int lg);
 const KernelSet& kernels_f64(int lg);
