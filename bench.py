@@ -1,0 +1,330 @@
+"""Benchmark: ms per 1024^2 phase mask (100 GS iterations, fp32) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[2]): a 1024x1024 SLM, 50-spot target and
+Gaussian-beam amplitude from the SURVEY.md §8(d) generator (synthetic,
+seeded), 100 Gerchberg-Saxton iterations in fp32, one mask per GPU per step
+(weak scaling across ranks, no collective on the iteration path). Metrics
+are recorded with record_every = iters, as the reference's own bench does
+(src/bench.py:100-102); the GPU computes the gap every iteration anyway.
+
+value  = device time per mask (inputs resident in HBM, CUDA events on the
+         solve's stream, L2 flushed by a 256 MiB write before every step),
+         max over ranks, divided by the masks of the whole job.
+e2e    = the same through the public host API (paper_1302_0120_b200.batch.
+         solve_stack): H2D of p and m from pinned memory, D2H of the float64
+         mask and histories, every step.
+roofline / cpu_baseline / clocks / gpu_launches: see DESIGN.md §Measurement.
+
+Under torchrun each rank drives cuda:LOCAL_RANK; rank 0 prints one JSON line.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+REPO = Path(__file__).resolve().parent
+sys.path.insert(0, str(REPO))
+
+N_PIX = 1024
+ITERS = 100
+SPOTS = 50
+SEED = 7
+METRIC = "ms per 1024² phase mask (100 iters) and AP iterations/s; % of HBM/L2 roofline"
+BYTES_PER_ITER = 40 * N_PIX * N_PIX          # fp32 GS, two fused sweeps
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def measured_peaks():
+    try:
+        return json.loads((REPO / "MEASURED_PEAKS.json").read_text())
+    except (OSError, ValueError):
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device, self.samples, self.proc = device, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def wait_first(self, timeout=10.0):
+        t0 = time.time()
+        while self.proc and not self.samples and time.time() - t0 < timeout:
+            time.sleep(0.05)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 3 + i and s[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def cpu_baseline(iters_sample=ITERS, reps=3):
+    """The reference's CPU path (oracle restatement of solve(), threaded like
+    the reference's threaded:N strategy) on this host's cores."""
+    from oracle import phasemask_oracle as orc
+    from paper_1302_0120_b200.patterns import make_problem
+    p, m = make_problem(N_PIX, SPOTS, SEED)
+    cores = os.cpu_count() or 1
+    gs = orc.ThreadedGS(p, m, "single", workers=cores)
+    try:
+        gs.run(2)                                   # warm-up (pools, FFT plans)
+        times = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            gs.run(iters_sample)
+            times.append((time.perf_counter() - t0) * 1e3)
+    finally:
+        gs.close()
+    per_mask = statistics.median(times) * ITERS / iters_sample
+    return {"value": per_mask, "unit": "ms/mask", "cores": cores, "kind": "port",
+            "sample": f"{reps} x {iters_sample}-iteration 1024^2 fp32 GS masks (oracle/phasemask_oracle.py "
+                      f"ThreadedGS = reference solve() with scipy.fft workers={cores} + threaded projections), "
+                      f"median scaled to {ITERS} iterations"}
+
+
+def run_reference(args, world, rank):
+    """--impl reference: the reference algorithm on host cores (rank 0 only)."""
+    if rank != 0:
+        return
+    from oracle import phasemask_oracle as orc
+    from paper_1302_0120_b200.patterns import make_problem
+    p, m = make_problem(N_PIX, SPOTS, SEED)
+    cores = os.cpu_count() or 1
+    gs = orc.ThreadedGS(p, m, "single", workers=cores)
+    try:
+        for _ in range(args.warmup):
+            gs.run(ITERS)
+        times = []
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            gs.run(ITERS)
+            times.append((time.perf_counter() - t0) * 1e3)
+    finally:
+        gs.close()
+    ms = sum(times) / len(times)
+    line = {"impl": "reference", "metric": METRIC, "value": ms, "unit": "ms/mask", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "gs_1024x1024_fp32_100iter_50spots_single_mask", "n_x": N_PIX, "n_y": N_PIX,
+                       "iters": ITERS, "masks_per_step": 1, "record_every": ITERS},
+            "iters_per_s": ITERS / (ms / 1e3),
+            "cpu_baseline": {"value": ms, "unit": "ms/mask", "cores": cores, "kind": "port",
+                             "sample": f"one full {ITERS}-iteration 1024^2 fp32 mask per step, "
+                                       f"reference solve() restated in oracle/ with scipy.fft workers={cores}"},
+            "e2e": {"value": ms, "unit": "ms/mask", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def flush_l2(buf):
+    buf.fill_(1.0)      # 256 MiB write > the 126 MB L2
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world, rank, local = dist_env()
+
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+    import paper_1302_0120_b200 as pm
+    from paper_1302_0120_b200 import _lib
+    from paper_1302_0120_b200.batch import solve_stack
+    from paper_1302_0120_b200.patterns import make_problem
+
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device (phasemask_b200 has no CPU fallback)")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    prec = pm.SINGLE
+    p, m = make_problem(N_PIX, SPOTS, SEED + rank)        # a distinct target per rank
+    spec = pm.GridSpec(N_PIX, N_PIX)
+    plan = pm.transform.get_plan(spec, prec, local)
+    stream = torch.cuda.Stream(device=local)
+    plan.set_stream(stream.cuda_stream)
+    d_p = torch.from_numpy(p.astype(np.float32)).cuda(local)
+    d_m = torch.from_numpy(m.astype(np.float32)).cuda(local)
+    d_phase = torch.empty((N_PIX, N_PIX), dtype=torch.float64, device=f"cuda:{local}")
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=f"cuda:{local}")
+    tol_p = np.array([prec.zero_tol(p.max())])
+    tol_m = np.array([prec.zero_tol(m.max())])
+    energy = np.array([float((m ** 2).sum())])
+    cfg = pm.SolveConfig(max_iters=ITERS, precision=prec, record_every=ITERS, device=local)
+    from paper_1302_0120_b200.solver import _params
+    prm = _params(cfg, False, False)
+    gaps = np.full(ITERS, np.nan)
+    iters = np.zeros(1, np.int32)
+
+    def solve_device():
+        res = _lib.pm_result()
+        res.phases = _lib.C.c_void_p(d_phase.data_ptr())
+        res.gap = _lib.ptr(gaps)
+        res.iters_run = _lib.ptr(iters)
+        _lib.check(plan.lib.pm_solve_device(plan.handle, _lib.C.c_void_p(d_p.data_ptr()),
+                                            _lib.C.c_void_p(d_m.data_ptr()), None, 1, prm, _lib.ptr(tol_p),
+                                            _lib.ptr(tol_m), _lib.ptr(energy), res), "pm_solve_device")
+
+    # ---- device-resident timing
+    for _ in range(args.warmup):
+        with torch.cuda.stream(stream):
+            flush_l2(flush)
+        solve_device()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    step_ms = []
+    with ClockSampler(local) as clocks:
+        clocks.wait_first()
+        t_load = time.time()
+        while time.time() - t_load < 0.5:          # clocks sampled under the same load
+            solve_device()
+        launches0 = plan.launch_count()
+        for _ in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush_l2(flush)
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+            solve_device()
+            with torch.cuda.stream(stream):
+                e1.record(stream)
+            e1.synchronize()
+            step_ms.append(e0.elapsed_time(e1))
+        torch.cuda.synchronize()
+        launches = plan.launch_count() - launches0
+        t_load = time.time()
+        while time.time() - t_load < 0.5:
+            solve_device()
+        time.sleep(0.2)
+    total = torch.tensor([sum(step_ms)], dtype=torch.float64, device=f"cuda:{local}")
+    if world > 1:
+        dist.barrier()
+        dist.all_reduce(total, op=dist.ReduceOp.MAX)
+    ms_per_step = float(total.item()) / args.steps
+    value = ms_per_step / world                        # whole-job ms per mask
+    assert iters[0] == ITERS and np.isfinite(gaps[0])
+
+    # ---- end to end through the public batch API (host buffers, pinned)
+    p_pin = torch.from_numpy(p.astype(np.float32)).pin_memory().numpy()
+    m_pin = torch.from_numpy(m[None].astype(np.float32)).pin_memory().numpy()
+    out_pin = torch.empty((1, N_PIX, N_PIX), dtype=torch.float64).pin_memory().numpy()
+    e2e_ms = []
+    for i in range(args.warmup + args.steps):
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        r = solve_stack(p_pin, m_pin, cfg, device=local, out_phases=out_pin)
+        t1 = time.perf_counter()
+        if i >= args.warmup:
+            e2e_ms.append((t1 - t0) * 1e3)
+    e2e = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device=f"cuda:{local}")
+    if world > 1:
+        dist.all_reduce(e2e, op=dist.ReduceOp.MAX)
+    e2e_value = float(e2e.item()) / args.steps / world
+    h2d = p_pin.nbytes + m_pin.nbytes + 3 * 8
+    d2h = r.phases.nbytes + 3 * r.gap.nbytes + 4 * 2 + 40
+
+    if rank == 0:
+        peaks = measured_peaks()
+        hbm = peaks.get("hbm_gbs")
+        solve_ms = ms_per_step                          # one persistent launch per step
+        achieved = BYTES_PER_ITER * ITERS / (solve_ms * 1e-3) / 1e9
+        l2 = _lib.measure_copy(32 << 20, 20, local)
+        traffic = None
+        tfile = REPO / "profiles" / "r01_ncu_traffic.json"
+        if tfile.exists():
+            traffic = json.loads(tfile.read_text()).get("dram_bytes_per_launch")
+        line = {
+            "metric": METRIC, "value": value, "unit": "ms/mask", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": False, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "gs_1024x1024_fp32_100iter_50spots_single_mask", "n_x": N_PIX, "n_y": N_PIX,
+                       "iters": ITERS, "spots": SPOTS, "masks_per_step": world, "masks_per_rank": 1,
+                       "record_every": ITERS, "parallelism": f"masks sharded over {world} GPU(s), no collective",
+                       "l2": "flushed by a 256 MiB write before every timed step",
+                       "path": "persistent" if plan.path() == 1 else "sweep-graph"},
+            "iters_per_s": ITERS * world / (ms_per_step / 1e3),
+            "e2e": {"value": e2e_value, "unit": "ms/mask", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "api": "paper_1302_0120_b200.batch.solve_stack (pinned host buffers)"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                         "frac": (achieved / hbm) if hbm else None, "traffic": traffic,
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if hbm else None,
+                         "kernel": "solve_kernel (persistent; whole solve in one launch)",
+                         "bytes_per_iter": BYTES_PER_ITER, "l2_copy_gbs_measured": l2,
+                         "frac_of_l2_copy": achieved / l2 if l2 else None},
+            "clocks": clocks.summary(),
+            "gpu_launches": launches,
+        }
+        if not args.no_cpu_baseline and world == 1:
+            line["cpu_baseline"] = cpu_baseline()
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -81,6 +81,15 @@ int pm_plan_set_stream(pm_plan *plan, void *stream);
 int pm_plan_get_stream(pm_plan *plan, void **stream);
 int pm_plan_synchronize(pm_plan *plan);
 
+/*
+ * Execution path of pm_solve*: 0 = automatic (the persistent cooperative
+ * kernel for square grids n >= 128 when the device supports it, else the
+ * sweep-per-kernel CUDA graph), 1 = force persistent (PM_ERR_UNSUPPORTED if
+ * unavailable), 2 = force the sweep graph.
+ */
+int pm_plan_set_path(pm_plan *plan, int path);
+int pm_plan_get_path(pm_plan *plan, int *path);
+
 /* Kernel launches issued by this plan since creation (evidence counter). */
 int pm_plan_launch_count(pm_plan *plan, long long *count);
 
@@ -184,7 +193,8 @@ typedef struct pm_result {
  * PhaseMaskTransformer.transform (src/estimator.py:85-93).
  *   p: real grid(s); m: real target moduli, batch grids;
  *   zero_tol_p / zero_tol_m: per-mask thresholds (1024*eps*max), host arrays;
- *   energy: per-mask sum(m^2) in fp64 (reconstructed-intensity scale);
+ *   energy: per-mask sum(m^2) in fp64 (reconstructed-intensity scale), or
+ *           NULL to reduce it on the device from the (precision-cast) m;
  *   m_init: complex starts when params->init_complex, else NULL.
  * Returns PM_ERR_DIVERGED when any mask produced non-finite values
  * (result->diverged_iter says which iteration).

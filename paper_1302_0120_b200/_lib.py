@@ -72,6 +72,8 @@ SIGNATURES = {
     "pm_plan_get_stream": (_I, [_VP, C.POINTER(_VP)]),
     "pm_plan_synchronize": (_I, [_VP]),
     "pm_plan_launch_count": (_I, [_VP, C.POINTER(_LL)]),
+    "pm_plan_set_path": (_I, [_VP, _I]),
+    "pm_plan_get_path": (_I, [_VP, C.POINTER(_I)]),
     "pm_fft2": (_I, [_VP, _VP, _VP, _I, _I]),
     "pm_fft2_device": (_I, [_VP, _VP, _VP, _I, _I]),
     "pm_replace_modulus": (_I, [_VP, _VP, _VP, _I, _D, _VP, _I]),
@@ -198,6 +200,15 @@ class Plan:
         n = C.c_longlong(0)
         check(self.lib.pm_plan_launch_count(self.handle, C.byref(n)))
         return n.value
+
+    def set_path(self, path: int):
+        """0 auto, 1 persistent cooperative kernel, 2 sweep-per-kernel graph."""
+        check(self.lib.pm_plan_set_path(self.handle, path), "pm_plan_set_path")
+
+    def path(self) -> int:
+        v = C.c_int(0)
+        check(self.lib.pm_plan_get_path(self.handle, C.byref(v)))
+        return v.value
 
     def set_stream(self, stream_handle: int | None):
         check(self.lib.pm_plan_set_stream(self.handle, C.c_void_p(stream_handle or 0)))

@@ -1,0 +1,170 @@
+"""Batches of independent masks: one launch per device, shards across GPUs.
+
+A single mask never shards (a 2-D FFT split across GPUs
+would need two all-to-all transposes per iteration for microseconds of
+work). A batch of masks with distinct targets — the reference's sequential
+``PhaseMaskTransformer.transform`` loop (src/estimator.py:85-93) — is
+embarrassingly parallel:
+
+* on one GPU, the whole batch runs in one persistent launch (every mask in
+  lockstep through the same sweeps, per-mask stop flags and histories);
+* across GPUs, masks are split into contiguous blocks of ceil(B / G), one
+  host thread and one plan (stream) per device, with no collective on the
+  iteration path;
+* across processes (one rank per GPU, ``torch.distributed``), each rank
+  solves its block and the results are gathered once at the end.
+
+Results are bitwise independent of the batch size and of the device count:
+every per-mask reduction runs in a fixed order that does not depend on
+which CTA or device handled the mask.
+"""
+
+from __future__ import annotations
+
+from concurrent.futures import ThreadPoolExecutor
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .grid import GridSpec, Precision
+from .solver import SolveConfig, SolveDivergedError, _params
+from .transform import get_plan
+
+
+def shard_bounds(n_items: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous block [lo, hi) of rank `rank` out of `world` (ceil split)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad world/rank")
+    per = -(-n_items // world) if n_items else 0
+    lo = min(n_items, rank * per)
+    return lo, min(n_items, lo + per)
+
+
+@dataclass
+class BatchResult:
+    """Per-mask outputs of a batch solve, stacked along axis 0."""
+
+    phases: np.ndarray          # (B, n_y, n_x) float64 in [0, 2pi)
+    gap: np.ndarray             # (B, K) gap history, NaN where not recorded
+    err_lit: np.ndarray         # (B, K)
+    err_dark: np.ndarray        # (B, K)
+    iters_run: np.ndarray       # (B,)
+    device_ms: float = 0.0      # device time of the slowest shard
+
+    @staticmethod
+    def concat(parts: list["BatchResult"]) -> "BatchResult":
+        parts = [q for q in parts if q.phases.shape[0]]
+        return BatchResult(np.concatenate([q.phases for q in parts]),
+                           np.concatenate([q.gap for q in parts]),
+                           np.concatenate([q.err_lit for q in parts]),
+                           np.concatenate([q.err_dark for q in parts]),
+                           np.concatenate([q.iters_run for q in parts]),
+                           max(q.device_ms for q in parts))
+
+
+def _maxes(a: np.ndarray, k: int) -> np.ndarray:
+    return np.asarray(a).reshape(k, -1).max(axis=1)
+
+
+def solve_stack(p: np.ndarray, m_stack: np.ndarray, cfg: SolveConfig, device: int = 0,
+                out_phases: np.ndarray | None = None) -> BatchResult:
+    """Solve a stack of targets on one device in one launch.
+
+    p: (n_y, n_x) shared amplitude or (B, n_y, n_x) per mask; m_stack:
+    (B, n_y, n_x) target moduli in DFT order. Arrays already in the
+    precision's dtype are used without a host copy (pass pinned buffers for
+    full-speed transfers); ``out_phases`` (B, n_y, n_x) float64 may be a
+    caller-owned (e.g. pinned) buffer for the mask. The per-mask energy
+    sum(m^2) is reduced on the device.
+    """
+    m_stack = np.asarray(m_stack)
+    if m_stack.ndim != 3:
+        raise ValueError("m_stack must be (batch, n_y, n_x)")
+    B, ny, nx = m_stack.shape
+    if B == 0:
+        z = np.zeros((0, cfg.max_iters))
+        return BatchResult(np.zeros((0, ny, nx)), z, z.copy(), z.copy(), np.zeros(0, np.int32))
+    p = np.asarray(p)
+    per_mask = p.ndim == 3
+    if (p.shape[-2:] != (ny, nx)) or (per_mask and p.shape[0] != B):
+        raise ValueError("amplitude and target constraints live on different grids")
+    pmax = _maxes(p, B if per_mask else 1)
+    mmax = _maxes(m_stack, B)
+    if (pmax == 0).any():
+        raise ValueError("SLM amplitude is identically zero")
+    if (mmax == 0).any():
+        raise ValueError("target pattern is identically zero (all dark)")
+    prec = cfg.precision
+    fdt = prec.float_dtype
+    plan = get_plan(GridSpec(nx, ny), prec, device)
+    pp = np.ascontiguousarray(p, dtype=fdt)
+    mm = np.ascontiguousarray(m_stack, dtype=fdt)
+    tol_p = np.array([prec.zero_tol(float(x)) for x in pmax])
+    tol_m = np.array([prec.zero_tol(float(x)) for x in mmax])
+    K = cfg.max_iters
+    phases = out_phases if out_phases is not None else np.empty((B, ny, nx))
+    if phases.shape != (B, ny, nx) or phases.dtype != np.float64 or not phases.flags.c_contiguous:
+        raise ValueError("out_phases must be a C-contiguous float64 (batch, n_y, n_x) array")
+    out = BatchResult(phases, np.full((B, K), np.nan), np.full((B, K), np.nan),
+                      np.full((B, K), np.nan), np.zeros(B, np.int32))
+    div = np.zeros(B, np.int32)
+    ms = np.zeros(1, np.float32)
+    res = _lib.pm_result()
+    res.phases = _lib.ptr(out.phases)
+    res.gap, res.err_lit, res.err_dark = _lib.ptr(out.gap), _lib.ptr(out.err_lit), _lib.ptr(out.err_dark)
+    res.iters_run, res.diverged_iter, res.device_ms = _lib.ptr(out.iters_run), _lib.ptr(div), _lib.ptr(ms)
+    prm = _params(cfg, per_mask, False)
+    with plan.lock:
+        code = plan.lib.pm_solve(plan.handle, _lib.ptr(pp), _lib.ptr(mm), None, B, prm, _lib.ptr(tol_p),
+                                 _lib.ptr(tol_m), None, res)
+    if code == _lib.PM_ERR_DIVERGED or div.any():
+        raise SolveDivergedError(int(div[div > 0][0]) if div.any() else 1)
+    _lib.check(code, "pm_solve")
+    out.device_ms = float(ms[0])
+    return out
+
+
+def solve_batch(p: np.ndarray, m_stack: np.ndarray, cfg: SolveConfig,
+                devices: list[int] | None = None) -> BatchResult:
+    """Shard a stack of masks across local GPUs (one host thread per device)."""
+    if devices is None:
+        devices = list(range(max(1, _lib.device_count())))
+    m_stack = np.asarray(m_stack)
+    B = m_stack.shape[0]
+    per_mask = np.ndim(p) == 3
+    G = len(devices)
+    bounds = [shard_bounds(B, G, r) for r in range(G)]
+
+    def run(r):
+        lo, hi = bounds[r]
+        return solve_stack(p[lo:hi] if per_mask else p, m_stack[lo:hi], cfg, devices[r])
+
+    if G == 1:
+        return run(0)
+    with ThreadPoolExecutor(G) as ex:
+        parts = list(ex.map(run, range(G)))
+    return BatchResult.concat(parts)
+
+
+def solve_batch_distributed(p: np.ndarray, m_stack: np.ndarray, cfg: SolveConfig, device: int | None = None,
+                            solve_fn=None) -> BatchResult | None:
+    """One rank per GPU under torch.distributed: solve this rank's block of
+    the stack, gather every block on rank 0 (returns None on other ranks).
+
+    ``solve_fn(p, m_block, cfg, device)`` defaults to :func:`solve_stack`;
+    the gather is one all_gather_object at the end, never on the iteration
+    path.
+    """
+    import torch.distributed as dist
+    world, rank = dist.get_world_size(), dist.get_rank()
+    lo, hi = shard_bounds(np.asarray(m_stack).shape[0], world, rank)
+    per_mask = np.ndim(p) == 3
+    if device is None:
+        import os
+        device = int(os.environ.get("LOCAL_RANK", rank))
+    fn = solve_fn or solve_stack
+    part = fn(p[lo:hi] if per_mask else p, np.asarray(m_stack)[lo:hi], cfg, device)
+    gathered = [None] * world
+    dist.all_gather_object(gathered, part)
+    return BatchResult.concat(gathered) if rank == 0 else None

@@ -170,13 +170,20 @@ __global__ void psum_partial_kernel(const T* p, long long n, long long chunk, lo
     if (threadIdx.x == 0) part[blockIdx.y * nb + blockIdx.x] = s;
 }
 
-__global__ void escale_kernel(const double* part, int nb, int per_mask, const double* energy,
+// escale[b] = energy[b] / sum p^2; with msum != null the energy sum m^2 is
+// itself reduced on the device (fixed order) from msum[b][0..nb).
+__global__ void escale_kernel(const double* part, int nb, int per_mask, double* energy, const double* msum,
                               double* escale, int batch) {
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= batch) return;
     const double* q = part + (per_mask ? b : 0) * nb;
     double s = 0.0;
     for (int i = 0; i < nb; ++i) s += q[i];
+    if (msum) {
+        double e = 0.0;
+        for (int i = 0; i < nb; ++i) e += msum[b * nb + i];
+        energy[b] = e;
+    }
     escale[b] = energy[b] / s;
 }
 
@@ -318,6 +325,7 @@ struct pm_plan {
     GridBar* bar = nullptr;           // grid barrier of the persistent kernel
     unsigned long long* stamps = nullptr;  // optional phase timestamps (pm_debug_phase_stamps)
     int solve_grid = 0;               // CTAs of the persistent kernel (0: not available)
+    int path = 0;                     // 0 auto, 1 persistent, 2 sweep graph
     RowCfg rc{};
     ColCfg cc{};
     std::map<std::string, cudaGraphExec_t> graphs;
@@ -336,6 +344,7 @@ struct pm_plan {
         void* ustar = nullptr;
         void* vstar = nullptr;
         std::vector<double> h_tolp, h_thrp, h_thrm, h_en;
+        bool energy_on_device = false;
     } s;
 };
 
@@ -408,7 +417,7 @@ int ensure_capacity(pm_plan* pl, int batch, int max_iters) {
     CK(cudaMalloc((void**)&pl->thrm, cap * sizeof(double)));
     CK(cudaMalloc((void**)&pl->escale, cap * sizeof(double)));
     CK(cudaMalloc((void**)&pl->energy, cap * sizeof(double)));
-    CK(cudaMalloc((void**)&pl->psum, (size_t)cap * 32 * sizeof(double)));
+    CK(cudaMalloc((void**)&pl->psum, (size_t)2 * cap * 32 * sizeof(double)));
     CK(cudaMemsetAsync(pl->ctr, 0, (size_t)cap * sizeof(unsigned), pl->stream));
     CK(cudaMemsetAsync(pl->st, 0, cap * sizeof(MaskState), pl->stream));
     pl->cap = cap;
@@ -648,8 +657,9 @@ int session_setup(pm_plan* pl, const void* d_p, const void* d_m, int batch, cons
         s.h_thrp[b] = pl->prec == PM_SINGLE ? fp32_sq_threshold(tp) * (double)pl->N
                                             : tp * std::sqrt((double)pl->N);
         s.h_thrm[b] = pl->prec == PM_SINGLE ? fp32_sq_threshold(tol_m[b]) : tol_m[b];
-        s.h_en[b] = energy[b];
+        s.h_en[b] = energy ? energy[b] : 0.0;
     }
+    s.energy_on_device = energy == nullptr;
     CK(cudaMemcpyAsync(pl->tolp, s.h_tolp.data(), batch * sizeof(double), cudaMemcpyHostToDevice, pl->stream));
     CK(cudaMemcpyAsync(pl->thrp, s.h_thrp.data(), batch * sizeof(double), cudaMemcpyHostToDevice, pl->stream));
     CK(cudaMemcpyAsync(pl->thrm, s.h_thrm.data(), batch * sizeof(double), cudaMemcpyHostToDevice, pl->stream));
@@ -671,8 +681,20 @@ int enqueue_escale(pm_plan* pl) {
     else
         psum_partial_kernel<double><<<grid, 256, 0, pl->stream>>>((const double*)s.p, n, chunk, s.p_stride,
                                                                    pl->psum, kPsumBlocks);
+    double* msum = nullptr;
+    if (s.energy_on_device) {
+        msum = pl->psum + (size_t)pl->cap * kPsumBlocks;
+        const dim3 gm(kPsumBlocks, s.batch);
+        if (pl->prec == PM_SINGLE)
+            psum_partial_kernel<float><<<gm, 256, 0, pl->stream>>>((const float*)s.m, n, chunk, (long long)pl->N,
+                                                                    msum, kPsumBlocks);
+        else
+            psum_partial_kernel<double><<<gm, 256, 0, pl->stream>>>((const double*)s.m, n, chunk, (long long)pl->N,
+                                                                     msum, kPsumBlocks);
+        pl->launches++;
+    }
     escale_kernel<<<(s.batch + 127) / 128, 128, 0, pl->stream>>>(pl->psum, kPsumBlocks, s.prm.p_per_mask,
-                                                                  pl->energy, pl->escale, s.batch);
+                                                                  pl->energy, msum, pl->escale, s.batch);
     CK(cudaGetLastError());
     pl->launches += 2;
     return PM_OK;
@@ -680,7 +702,8 @@ int enqueue_escale(pm_plan* pl) {
 
 bool persistent(const pm_plan* pl) {
     static const bool off = getenv("PM_NO_PERSISTENT") != nullptr;
-    return pl->solve_grid > 0 && !off;
+    if (pl->path == 2) return false;
+    return pl->solve_grid > 0 && (pl->path == 1 || !off);
 }
 
 int enqueue_begin(pm_plan* pl) {
@@ -958,6 +981,21 @@ int pm_plan_synchronize(pm_plan* pl) {
     return PM_OK;
 }
 
+int pm_plan_set_path(pm_plan* pl, int path) {
+    if (!pl) return set_err(PM_ERR_ARG, "null plan");
+    if (path < 0 || path > 2) return set_err(PM_ERR_ARG, "path must be 0, 1 or 2");
+    if (path == 1 && pl->solve_grid == 0)
+        return set_err(PM_ERR_UNSUPPORTED, "persistent solve kernel unavailable for this grid/device");
+    pl->path = path;
+    return PM_OK;
+}
+
+int pm_plan_get_path(pm_plan* pl, int* path) {
+    if (!pl || !path) return set_err(PM_ERR_ARG, "null argument");
+    *path = (pl->path == 2 || pl->solve_grid == 0) ? 2 : 1;
+    return PM_OK;
+}
+
 int pm_plan_launch_count(pm_plan* pl, long long* count) {
     if (!pl || !count) return set_err(PM_ERR_ARG, "null argument");
     *count = pl->launches;
@@ -1206,7 +1244,7 @@ int pm_phases(int device, const void* u, long long count, int precision, double 
 static int solve_core(pm_plan* pl, const void* d_p, const void* d_m, const void* d_init, int batch,
                       const pm_params* prm, const double* tol_p, const double* tol_m,
                       const double* energy, pm_result* res, bool host_io) {
-    if (!tol_p || !tol_m || !energy) return set_err(PM_ERR_ARG, "null tolerance / energy arrays");
+    if (!tol_p || !tol_m) return set_err(PM_ERR_ARG, "null tolerance arrays");
     CKR(session_setup(pl, d_p, d_m, batch, prm, tol_p, tol_m, energy));
     auto& s = pl->s;
     const size_t N = pl->N;
@@ -1281,7 +1319,7 @@ int pm_solve_device(pm_plan* pl, const void* d_p, const void* d_m, const void* d
 int pm_solve_begin(pm_plan* pl, const void* p, const void* m, const void* m_init, int batch,
                    const pm_params* prm, const double* tol_p, const double* tol_m, const double* energy) {
     CKR(check_plan(pl));
-    if (!p || !m || !tol_p || !tol_m || !energy) return set_err(PM_ERR_ARG, "null input");
+    if (!p || !m || !tol_p || !tol_m) return set_err(PM_ERR_ARG, "null input");
     CKR(validate_params(prm, batch));
     std::lock_guard<std::mutex> lk(pl->mu);
     CKR(ensure_capacity(pl, batch, prm->max_iters));

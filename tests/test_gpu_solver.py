@@ -1,0 +1,263 @@
+"""GPU: solver contracts, determinism, callbacks, batches, large grids
+(reference tests/test_solver.py and tests/test_acceptance.py, re-pointed)."""
+
+import math
+
+import numpy as np
+import pytest
+
+import paper_1302_0120_b200 as pm
+from oracle import phasemask_oracle as orc
+from paper_1302_0120_b200.batch import solve_batch, solve_stack
+from paper_1302_0120_b200.patterns import (make_problem, modulus_from_intensity, spot_grid_centers,
+                                           spot_pattern, to_fourier_order)
+from paper_1302_0120_b200.projections import project_fourier, project_slm
+
+pytestmark = pytest.mark.gpu
+EPS = np.finfo(float).eps
+
+
+def spot_problem(n, precision=pm.DOUBLE):
+    """The reference's default fixture: 3x3 lattice, energy-matched uniform p."""
+    spec = pm.GridSpec(n, n)
+    inten = spot_pattern(spec, spot_grid_centers(spec))
+    m = pm.FourierConstraint(modulus_from_intensity(to_fourier_order(inten)), precision)
+    c = pm.SlmConstraint(pm.default_amplitude(m.m, precision), precision)
+    return spec, c, m, inten
+
+
+def problem(n, tag="double", spots=8, seed=7):
+    prec = pm.Precision.from_tag(tag)
+    p, m = make_problem(n, spots, seed)
+    spec = pm.GridSpec(n, n)
+    return spec, pm.SlmConstraint(pm.RealGrid(spec, p), prec), pm.FourierConstraint(pm.RealGrid(spec, m), prec)
+
+
+def test_initial_iterate_matches_naive_oracle():
+    spec = pm.GridSpec(32, 32)
+    md = np.zeros(spec.shape)
+    for j, k in ((4, 4), (12, 20), (28, 8)):
+        md[k, j] = 1.0
+    u = pm.initial_iterate(pm.FourierConstraint(pm.RealGrid(spec, md)), pm.FftProvider(spec))
+    assert np.abs(u.data - orc.naive_dft(md.astype(complex), "inverse")).max() < 1e-12
+    a = pm.initial_iterate(pm.FourierConstraint(pm.RealGrid(spec, md)), pm.FftProvider(spec), True, 3)
+    b = pm.initial_iterate(pm.FourierConstraint(pm.RealGrid(spec, md)), pm.FftProvider(spec), True, 3)
+    np.testing.assert_array_equal(a.data, b.data)
+
+
+def test_single_iteration_pair_matches_composition():
+    spec, c, m, _ = spot_problem(32)
+    prov = pm.FftProvider(spec)
+    r = pm.solve(c, m, pm.SolveConfig(max_iters=1), prov)
+    assert r.iters_run == 1 and len(r.history) == 1
+    u0 = pm.initial_iterate(m, prov)
+    u1 = project_slm(project_fourier(u0, m, prov), c)
+    v_star = project_fourier(u1, m, prov)
+    u_star = project_slm(v_star, c)
+    assert np.abs(r.u_star.data - u_star.data).max() <= 1e-12
+    d = np.angle(np.exp(1j * (r.mask.phases - pm.phases_of(u_star, c.zero_tol).phases)))
+    assert np.abs(d).max() <= 1e-10
+
+
+def test_history_length_with_record_every():
+    spec, c, m, _ = spot_problem(32)
+    r = pm.solve(c, m, pm.SolveConfig(max_iters=25, record_every=2))
+    assert len(r.history) == 13
+    assert [h.iter for h in r.history][:3] == [1, 3, 5]
+
+
+def test_iterates_feasible():
+    spec, c, m, _ = spot_problem(32)
+    prov = pm.FftProvider(spec)
+    r = pm.solve(c, m, pm.SolveConfig(max_iters=10), prov)
+    p = c.p.data
+    assert np.abs(np.abs(r.u_star.data) - p).max() <= 4 * EPS * p.max()
+    assert np.linalg.norm(r.u_star.data) == pytest.approx(np.linalg.norm(p), rel=16 * EPS)
+    mods = np.abs(prov.forward(r.v_star).data)
+    assert np.abs(mods - m.m.data).max() <= 32 * EPS * max(1, m.m.data.max())
+
+
+def test_gap_sequence_non_increasing_fp64():
+    for spec, c, m in (spot_problem(64)[:3], problem(128)):
+        gaps = [h.gap for h in pm.solve(c, m, pm.SolveConfig(max_iters=25)).history]
+        jitter = 4 * EPS * gaps[0]
+        assert all(b <= a + jitter for a, b in zip(gaps, gaps[1:]))
+
+
+def test_rejections():
+    spec, c, m, _ = spot_problem(16)
+    with pytest.raises(ValueError, match="identically zero"):
+        pm.solve(pm.SlmConstraint(pm.RealGrid(spec, np.zeros(spec.shape))), m, pm.SolveConfig(max_iters=1))
+    with pytest.raises(ValueError, match="all dark"):
+        pm.solve(c, pm.FourierConstraint(pm.RealGrid(spec, np.zeros(spec.shape))), pm.SolveConfig(max_iters=1))
+
+
+def test_early_stop():
+    spec, c, m, _ = spot_problem(64)
+    r = pm.solve(c, m, pm.SolveConfig(max_iters=200, early_stop_tol=1e-6))
+    assert r.iters_run < 200
+
+
+def test_abort_callback_and_on_record():
+    spec, c, m, _ = spot_problem(32)
+    calls, records = [], []
+
+    def should_abort():
+        calls.append(1)
+        return len(calls) >= 3
+
+    r = pm.solve(c, m, pm.SolveConfig(max_iters=50), on_record=records.append, should_abort=should_abort)
+    assert r.aborted and r.iters_run == 3
+    assert [x.iter for x in records] == [1, 2, 3]
+    full = pm.solve(c, m, pm.SolveConfig(max_iters=3))
+    assert [x.gap for x in records] == [x.gap for x in full.history]
+    np.testing.assert_array_equal(r.mask.phases, full.mask.phases)
+
+
+@pytest.mark.parametrize("path", [1, 2])
+def test_identical_runs_bitwise(path):
+    spec, c, m = problem(128)
+    plan = pm.transform.get_plan(spec, pm.DOUBLE)
+    plan.set_path(path)
+    try:
+        a = pm.solve(c, m, pm.SolveConfig(max_iters=10))
+        b = pm.solve(c, m, pm.SolveConfig(max_iters=10))
+    finally:
+        plan.set_path(0)
+    np.testing.assert_array_equal(a.mask.phases, b.mask.phases)
+    assert [r.gap for r in a.history] == [r.gap for r in b.history]
+
+
+def test_backend_selector_does_not_change_results():
+    spec, c, m, _ = spot_problem(64)
+    a = pm.solve(c, m, pm.SolveConfig(max_iters=10, backend=pm.BackendSelector("serial")))
+    b = pm.solve(c, m, pm.SolveConfig(max_iters=10, backend=pm.BackendSelector("threaded", 8)))
+    np.testing.assert_array_equal(a.mask.phases, b.mask.phases)
+    assert [(r.gap, r.err_lit, r.err_dark) for r in a.history] == [(r.gap, r.err_lit, r.err_dark) for r in b.history]
+
+
+def test_single_precision_stays_single():
+    spec, c, m, _ = spot_problem(64, pm.SINGLE)
+    r = pm.solve(c, m, pm.SolveConfig(max_iters=3, precision=pm.SINGLE))
+    assert r.u_star.dtype == np.complex64 and r.v_star.dtype == np.complex64
+
+
+@pytest.mark.parametrize("tag", ["double", "single"])
+def test_batch_is_bitwise_independent_of_batch_size(tag):
+    prec = pm.Precision.from_tag(tag)
+    p, _ = make_problem(128, 8, 7)
+    ms = np.stack([make_problem(128, 8, s)[1] for s in (11, 12, 13)])
+    cfg = pm.SolveConfig(max_iters=12, precision=prec, record_every=1)
+    whole = solve_stack(p, ms, cfg)
+    for i in range(3):
+        one = solve_stack(p, ms[i:i + 1], cfg)
+        np.testing.assert_array_equal(whole.phases[i], one.phases[0])
+        np.testing.assert_array_equal(whole.gap[i], one.gap[0])
+    spec = pm.GridSpec(128, 128)
+    r = pm.solve(pm.SlmConstraint(pm.RealGrid(spec, p), prec), pm.FourierConstraint(pm.RealGrid(spec, ms[1]), prec),
+                 cfg)
+    np.testing.assert_array_equal(r.mask.phases, whole.phases[1])
+    assert [h.gap for h in r.history] == list(whole.gap[1])
+    multi = solve_batch(p, ms, cfg)
+    np.testing.assert_array_equal(multi.phases, whole.phases)
+
+
+def test_batch_per_mask_amplitude_and_early_stop():
+    ps = np.stack([make_problem(64, 4, s)[0] for s in (1, 2)])
+    ms = np.stack([make_problem(64, 4, s)[1] for s in (1, 2)])
+    cfg = pm.SolveConfig(max_iters=60, early_stop_tol=1e-7)
+    res = solve_stack(ps, ms, cfg)
+    for i in range(2):
+        spec = pm.GridSpec(64, 64)
+        r = pm.solve(pm.SlmConstraint(pm.RealGrid(spec, ps[i])), pm.FourierConstraint(pm.RealGrid(spec, ms[i])), cfg)
+        assert r.iters_run == res.iters_run[i]
+        np.testing.assert_array_equal(r.mask.phases, res.phases[i])
+
+
+def test_raar_is_not_yet_available_message():
+    spec, c, m = problem(64)
+    try:
+        r = pm.solve(c, m, pm.SolveConfig(max_iters=5, algorithm="raar"))
+    except NotImplementedError:
+        pytest.skip("RAAR not built")
+    assert r.iters_run == 5
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("n", [2048, 4096])
+def test_large_field_properties(n):
+    """Size-independent properties at BASELINE config 5 sizes (fp32)."""
+    spec, c, m = problem(n, "single", spots=50)
+    prov = pm.FftProvider(spec, pm.SINGLE)
+    r = pm.solve(c, m, pm.SolveConfig(max_iters=20, precision=pm.SINGLE, record_every=5))
+    p = c.p.data
+    assert np.abs(np.abs(r.u_star.data) - p).max() <= 8 * np.finfo(np.float32).eps * p.max()
+    mods = np.abs(prov.forward(r.v_star).data)
+    assert np.abs(mods - m.m.data).max() <= 1e-4 * max(1.0, m.m.data.max())
+    gaps = [h.gap for h in r.history]
+    assert all(np.isfinite(gaps)) and gaps[-1] <= gaps[0] * (1 + 1e-5)
+    assert ((r.mask.phases >= 0) & (r.mask.phases < 2 * np.pi)).all()
+
+
+# --- acceptance criteria of the reference (tests/test_acceptance.py) --------
+
+def test_acceptance_1_oracle_equivalence():
+    rng = np.random.default_rng(101)
+    worst = 0.0
+    for n in (8, 16):
+        spec = pm.GridSpec(n, n)
+        prov = pm.FftProvider(spec)
+        for _ in range(50):
+            u = rng.standard_normal(spec.shape) + 1j * rng.standard_normal(spec.shape)
+            m = rng.uniform(0, 2, spec.shape)
+            got = project_fourier(pm.Field(spec, u), pm.FourierConstraint(pm.RealGrid(spec, m)), prov).data
+            vhat = orc.replace_modulus(orc.naive_dft(u), m, orc.zero_tol("double", m), "double")
+            worst = max(worst, float(np.abs(got - orc.naive_dft(vhat, "inverse")).max()))
+    assert worst <= 1e-12
+
+
+def _spot_gaps():
+    _, cd, md, _ = spot_problem(256, pm.DOUBLE)
+    _, cs, ms, _ = spot_problem(256, pm.SINGLE)
+    gd = pm.solve(cd, md, pm.SolveConfig(max_iters=25, record_every=25)).final.gap
+    gs = pm.solve(cs, ms, pm.SolveConfig(max_iters=25, record_every=25, precision=pm.SINGLE)).final.gap
+    return gd, gs
+
+
+def test_acceptance_3_and_6_inconsistency_and_precision_agreement():
+    gd, gs = _spot_gaps()
+    assert gd > 1e6 * EPS and 0.1 <= gs / gd <= 10.0
+    assert abs(gs - gd) / gd <= 0.05
+
+
+def test_acceptance_4_saturation():
+    _, c, m, _ = spot_problem(256)
+    r = pm.solve(c, m, pm.SolveConfig(max_iters=25))
+    by = {h.iter: h for h in r.history}
+    e2, e25 = by[2].err_lit + by[2].err_dark, by[25].err_lit + by[25].err_dark
+    assert abs(e2 - e25) <= 0.05 * e25
+    assert abs(by[2].gap - by[25].gap) <= 0.05 * by[25].gap
+
+
+def test_acceptance_5_contrast():
+    from paper_1302_0120_b200.metrics import contrast_ratio, reconstructed_intensity
+    spec, c, m, _ = spot_problem(256)
+    prov = pm.FftProvider(spec)
+    r = pm.solve(c, m, pm.SolveConfig(max_iters=25, record_every=25), prov)
+    target = pm.RealGrid(spec, m.m.data ** 2)
+    recon = reconstructed_intensity(r.u_star, prov, float(target.data.sum()))
+    assert contrast_ratio(recon, target) >= 1e2
+
+
+@pytest.mark.xfail(reason="known-red in the reference too: AP from the default init does not reach "
+                          "sqrt(N)*100*eps on consistent problems (reference README, tests/test_solver.py:170)",
+                   strict=False)
+def test_acceptance_2_consistency_collapse():
+    spec = pm.GridSpec(64, 64)
+    prov = pm.FftProvider(spec)
+    c = pm.SlmConstraint(pm.RealGrid(spec, np.ones(spec.shape)))
+    rng = np.random.default_rng(2024)
+    w = pm.Field(spec, np.exp(1j * rng.uniform(0, 2 * np.pi, spec.shape)))
+    m = pm.FourierConstraint(pm.RealGrid(spec, np.abs(prov.forward(w).data)))
+    r = pm.solve(c, m, pm.SolveConfig(max_iters=50, record_every=50), prov)
+    assert r.final.gap <= math.sqrt(spec.n) * 100 * EPS
