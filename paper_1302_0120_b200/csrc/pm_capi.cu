@@ -308,9 +308,14 @@ struct pm_plan {
     uint8_t* levels = nullptr;        // cap * N
     void* ustar = nullptr;            // cap * N complex
     void* vstar = nullptr;
+    void* field2 = nullptr;           // RAAR: cap * N complex, second field buffer (w')
+    void* xbuf = nullptr;             // RAAR: cap * N complex, the iterate x
+    double* rpart = nullptr;          // RAAR: cap * ny * wpr * 2 row partials
+    double* thrx = nullptr;           // RAAR: cap P_S thresholds on true-scale values
+    int raar_cap = 0;
     MaskState* st = nullptr;          // cap
     double* hist = nullptr;           // cap * hist_cap * 4
-    double* part = nullptr;           // partial sums (row + col), cap * nblk * 3 each
+    double* part = nullptr;           // column partial sums, 2 (parity) * cap * nb * 3
     unsigned* ctr = nullptr;          // 2 * cap counters
     double* tolp = nullptr;           // cap: reference zero_tol of p
     double* thrp = nullptr;           // cap: decision thresholds (fp32: on |u|^2)
@@ -343,7 +348,7 @@ struct pm_plan {
         void* levels = nullptr;
         void* ustar = nullptr;
         void* vstar = nullptr;
-        std::vector<double> h_tolp, h_thrp, h_thrm, h_en;
+        std::vector<double> h_tolp, h_thrp, h_thrm, h_en, h_thrx;
         bool energy_on_device = false;
     } s;
 };
@@ -380,6 +385,12 @@ void free_buffers(pm_plan* pl) {
                     pl->thrm, pl->escale, pl->energy, pl->psum};
     for (void* b : bufs)
         if (b) cudaFree(b);
+    void* rbufs[] = {pl->field2, pl->xbuf, pl->rpart, pl->thrx};
+    for (void* b : rbufs)
+        if (b) cudaFree(b);
+    pl->field2 = pl->xbuf = nullptr;
+    pl->rpart = pl->thrx = nullptr;
+    pl->raar_cap = 0;
     pl->field = pl->tmp = pl->pbuf = pl->mbuf = pl->ustar = pl->vstar = nullptr;
     pl->phases = nullptr;
     pl->levels = nullptr;
@@ -410,7 +421,7 @@ int ensure_capacity(pm_plan* pl, int batch, int max_iters) {
     CK(cudaMalloc(&pl->mbuf, cap * N * pl->rsz));
     CK(cudaMalloc((void**)&pl->st, cap * sizeof(MaskState)));
     CK(cudaMalloc((void**)&pl->hist, (size_t)cap * hcap * 4 * sizeof(double)));
-    CK(cudaMalloc((void**)&pl->part, (size_t)cap * nb * 3 * sizeof(double)));
+    CK(cudaMalloc((void**)&pl->part, (size_t)2 * cap * nb * 3 * sizeof(double)));
     CK(cudaMalloc((void**)&pl->ctr, (size_t)cap * sizeof(unsigned)));
     CK(cudaMalloc((void**)&pl->tolp, cap * sizeof(double)));
     CK(cudaMalloc((void**)&pl->thrp, cap * sizeof(double)));
@@ -422,6 +433,36 @@ int ensure_capacity(pm_plan* pl, int batch, int max_iters) {
     CK(cudaMemsetAsync(pl->st, 0, cap * sizeof(MaskState), pl->stream));
     pl->cap = cap;
     pl->hist_cap = hcap;
+    return PM_OK;
+}
+
+// Partial slots per row of the row sweep (one per warp of a row group).
+int row_wpr(const pm_plan* pl) { return std::max(1, kset(pl->prec, pl->lgx).row.TG / 32); }
+
+// Elements of one parity half of `part`.
+size_t part_half(const pm_plan* pl) { return (size_t)pl->cap * std::max(pl->cc.nblk, pl->nx) * 3; }
+
+// Column tasks per mask of the persistent kernel.
+int solve_tpm(const pm_plan* pl) {
+    const KernelSet& k = kset(pl->prec, pl->lgy);
+    const int C = std::max(1, k.solve_threads / std::max(1, k.col.TG));
+    return std::max(1, pl->nx / C);
+}
+
+// RAAR buffers (allocated on first use, sized to the batch capacity).
+int ensure_raar(pm_plan* pl) {
+    if (pl->raar_cap >= pl->cap) return PM_OK;
+    for (void* b : {pl->field2, pl->xbuf, (void*)pl->rpart, (void*)pl->thrx})
+        if (b) cudaFree(b);
+    pl->field2 = pl->xbuf = nullptr;
+    pl->rpart = pl->thrx = nullptr;
+    pl->raar_cap = 0;
+    const size_t n = (size_t)pl->cap * pl->N;
+    CK(cudaMalloc(&pl->field2, n * pl->csz));
+    CK(cudaMalloc(&pl->xbuf, n * pl->csz));
+    CK(cudaMalloc((void**)&pl->rpart, (size_t)pl->cap * pl->ny * row_wpr(pl) * 2 * sizeof(double)));
+    CK(cudaMalloc((void**)&pl->thrx, (size_t)pl->cap * sizeof(double)));
+    pl->raar_cap = pl->cap;
     return PM_OK;
 }
 
@@ -437,8 +478,11 @@ int ensure_outputs(pm_plan* pl, bool phases, bool levels, bool ustar, bool vstar
 // --------------------------------------------------------------- launches
 template <typename T>
 RowArgs<T> row_args(pm_plan* pl, int mode, int it) {
+    const pm_params& prm = pl->s.prm;
+    const bool raar = prm.algorithm == PM_ALGO_RAAR;
     RowArgs<T> a;
     a.field = (cx<T>*)pl->field;
+    a.out = raar ? (cx<T>*)pl->field2 : a.field;
     a.p = (const T*)pl->s.p;
     a.p_stride = pl->s.p_stride;
     a.twf = (const twe<T>*)pl->tw_row;
@@ -450,6 +494,24 @@ RowArgs<T> row_args(pm_plan* pl, int mode, int it) {
     a.mode = mode;
     a.it = it;
     a.st = pl->st;
+    a.x = raar ? (cx<T>*)pl->xbuf : nullptr;
+    a.beta = (T)prm.beta;
+    a.c1 = (T)(1.0 - 2.0 * prm.beta);
+    a.thr_x = pl->thrx;
+    a.rpart = pl->rpart;
+    a.wpr = row_wpr(pl);
+    a.ctl.max_iters = prm.max_iters;
+    a.ctl.record_every = prm.record_every;
+    a.ctl.early_tol = prm.early_stop_tol;
+    a.ctl.t_lit = prm.t_lit;
+    a.ctl.t_dark = prm.t_dark;
+    a.hist = pl->hist;
+    a.hist_stride = pl->hist_cap;
+    a.cpart = pl->part;
+    a.cpart_alt = (long long)part_half(pl);
+    a.tpm = solve_tpm(pl);
+    a.ctr = pl->ctr;
+    a.nblk = pl->rc.nblk;
     return a;
 }
 
@@ -469,14 +531,32 @@ FinalArgs<T> final_args(pm_plan* pl) {
     a.u_star = (cx<T>*)pl->s.ustar;
     a.phases = (double*)pl->s.phases;
     a.levels = (uint8_t*)pl->s.levels;
+    const pm_params& prm = pl->s.prm;
+    const bool raar = prm.algorithm == PM_ALGO_RAAR;
+    a.x = raar ? (const cx<T>*)pl->xbuf : nullptr;
+    a.thr_x = pl->thrx;
+    a.rpart = pl->rpart;
+    a.wpr = row_wpr(pl);
+    a.ctl.max_iters = prm.max_iters;
+    a.ctl.record_every = prm.record_every;
+    a.ctl.early_tol = prm.early_stop_tol;
+    a.ctl.t_lit = prm.t_lit;
+    a.ctl.t_dark = prm.t_dark;
     return a;
 }
 
 template <typename T>
 ColArgs<T> col_args(pm_plan* pl, int mode, int u_iter) {
     const pm_params& prm = pl->s.prm;
+    const bool raar = prm.algorithm == PM_ALGO_RAAR;
     ColArgs<T> a;
     a.field = (cx<T>*)pl->field;
+    a.in = raar ? (const cx<T>*)pl->field2 : a.field;
+    a.raar = raar ? 1 : 0;
+    a.xpart = pl->rpart;
+    a.xparts = pl->ny * row_wpr(pl);
+    a.energy = pl->energy;
+    a.part_alt = (long long)part_half(pl);
     a.m = (const T*)pl->s.m;
     a.m_stride = (long long)pl->N;
     a.twf = (const twe<T>*)pl->tw_col;
@@ -515,7 +595,11 @@ int launch_row(pm_plan* pl, int batch, int mode, int it) {
 template <typename T>
 int launch_final(pm_plan* pl, int batch) {
     FinalArgs<T> a = final_args<T>(pl);
-    void* args[] = {&a};
+    double* hist = pl->hist;
+    int hs = pl->hist_cap;
+    unsigned* ctr = pl->ctr;
+    int nblk = pl->rc.nblk;
+    void* args[] = {&a, &hist, &hs, &ctr, &nblk};
     CK(cudaLaunchKernel(kset(pl->prec, pl->lgx).row_final, dim3(pl->rc.nblk, batch), dim3(pl->rc.threads),
                         args, pl->rc.smem, pl->stream));
     pl->launches++;
@@ -535,7 +619,7 @@ int launch_col(pm_plan* pl, int batch, int mode, int u_iter) {
 // One cooperative launch of the persistent solve kernel: optional initial
 // iterate, iterations [it_begin, it_end), optional final pair.
 template <typename T>
-int launch_solve(pm_plan* pl, int do_init, int it_begin, int it_end, int do_final) {
+int launch_solve(pm_plan* pl, int do_init, int it_begin, int it_end, int do_final, int do_probe) {
     const KernelSet& k = kset(pl->prec, pl->lgx);
     SolveArgs<T> a;
     a.row = row_args<T>(pl, 1, 0);
@@ -548,6 +632,7 @@ int launch_solve(pm_plan* pl, int do_init, int it_begin, int it_end, int do_fina
     a.do_init = do_init;
     a.do_final = do_final;
     a.init_mode = pl->s.prm.init_complex ? 1 : 0;
+    a.do_probe = do_probe;
     a.stamps = pl->stamps;
     void* args[] = {&a};
     cudaLaunchConfig_t cfg = {};
@@ -561,14 +646,14 @@ int launch_solve(pm_plan* pl, int do_init, int it_begin, int it_end, int do_fina
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     CK(cudaMemsetAsync(pl->bar, 0, sizeof(GridBar), pl->stream));
-    CK(cudaLaunchKernelExC(&cfg, k.solve, args));
+    CK(cudaLaunchKernelExC(&cfg, pl->s.prm.algorithm == PM_ALGO_RAAR ? k.solve_raar : k.solve, args));
     pl->launches++;
     return PM_OK;
 }
 
-int solve_launch(pm_plan* pl, int do_init, int it_begin, int it_end, int do_final) {
-    return pl->prec == PM_SINGLE ? launch_solve<float>(pl, do_init, it_begin, it_end, do_final)
-                                 : launch_solve<double>(pl, do_init, it_begin, it_end, do_final);
+int solve_launch(pm_plan* pl, int do_init, int it_begin, int it_end, int do_final, int do_probe = 0) {
+    return pl->prec == PM_SINGLE ? launch_solve<float>(pl, do_init, it_begin, it_end, do_final, do_probe)
+                                 : launch_solve<double>(pl, do_init, it_begin, it_end, do_final, do_probe);
 }
 
 int row(pm_plan* pl, int batch, int mode, int it) {
@@ -626,8 +711,10 @@ int validate_params(const pm_params* prm, int batch) {
     if (batch < 1) return set_err(PM_ERR_ARG, "batch must be >= 1");
     if (prm->max_iters < 1) return set_err(PM_ERR_ARG, "max_iters must be >= 1");
     if (prm->record_every < 1) return set_err(PM_ERR_ARG, "record_every must be >= 1");
-    if (prm->algorithm != PM_ALGO_GS)
-        return set_err(PM_ERR_UNSUPPORTED, "only the GS algorithm is available in this build");
+    if (prm->algorithm != PM_ALGO_GS && prm->algorithm != PM_ALGO_RAAR)
+        return set_err(PM_ERR_ARG, "algorithm must be 0 (GS) or 1 (RAAR)");
+    if (prm->algorithm == PM_ALGO_RAAR && !std::isfinite(prm->beta))
+        return set_err(PM_ERR_ARG, "RAAR beta must be finite");
     return PM_OK;
 }
 
@@ -636,6 +723,7 @@ int session_setup(pm_plan* pl, const void* d_p, const void* d_m, int batch, cons
                   const double* tol_p, const double* tol_m, const double* energy) {
     CKR(validate_params(prm, batch));
     CKR(ensure_capacity(pl, batch, prm->max_iters));
+    if (prm->algorithm == PM_ALGO_RAAR) CKR(ensure_raar(pl));
     auto& s = pl->s;
     s = pm_plan::Session();
     s.active = true;
@@ -650,6 +738,7 @@ int session_setup(pm_plan* pl, const void* d_p, const void* d_m, int batch, cons
     s.h_thrp.resize(batch);
     s.h_thrm.resize(batch);
     s.h_en.resize(batch);
+    s.h_thrx.resize(batch);
     for (int b = 0; b < batch; ++b) {
         const double tp = tol_p[prm->p_per_mask ? b : 0];
         s.h_tolp[b] = tp;
@@ -658,12 +747,15 @@ int session_setup(pm_plan* pl, const void* d_p, const void* d_m, int batch, cons
                                             : tp * std::sqrt((double)pl->N);
         s.h_thrm[b] = pl->prec == PM_SINGLE ? fp32_sq_threshold(tol_m[b]) : tol_m[b];
         s.h_en[b] = energy ? energy[b] : 0.0;
+        s.h_thrx[b] = pl->prec == PM_SINGLE ? fp32_sq_threshold(tp) : tp;   // RAAR P_S on true scale
     }
     s.energy_on_device = energy == nullptr;
     CK(cudaMemcpyAsync(pl->tolp, s.h_tolp.data(), batch * sizeof(double), cudaMemcpyHostToDevice, pl->stream));
     CK(cudaMemcpyAsync(pl->thrp, s.h_thrp.data(), batch * sizeof(double), cudaMemcpyHostToDevice, pl->stream));
     CK(cudaMemcpyAsync(pl->thrm, s.h_thrm.data(), batch * sizeof(double), cudaMemcpyHostToDevice, pl->stream));
     CK(cudaMemcpyAsync(pl->energy, s.h_en.data(), batch * sizeof(double), cudaMemcpyHostToDevice, pl->stream));
+    if (pl->thrx)
+        CK(cudaMemcpyAsync(pl->thrx, s.h_thrx.data(), batch * sizeof(double), cudaMemcpyHostToDevice, pl->stream));
     return PM_OK;
 }
 
@@ -713,24 +805,31 @@ int enqueue_begin(pm_plan* pl) {
     CKR(enqueue_escale(pl));
     if (persistent(pl)) return solve_launch(pl, 1, 1, 1, 0);
     CKR(col(pl, s.batch, s.prm.init_complex ? 1 : 0, 0));   // u0 column half
-    CKR(row(pl, s.batch, 0, 0));                            // u0 row half, w0 = RowFFT(u0)
+    CKR(row(pl, s.batch, kRowInit, 0));                     // u0 row half, w0 = RowFFT(u0)
     CKR(col(pl, s.batch, 2, 0));                            // z1 = ColIFFT replace F u0
     return PM_OK;
 }
 
-int enqueue_steps(pm_plan* pl, int n) {
+// Iterations s.it+1 .. s.it+n. With `probe` (the stepping API), a RAAR solve
+// also measures and decides the last iterate now instead of in the next
+// sweep, so its record is readable when the call returns.
+int enqueue_steps(pm_plan* pl, int n, bool probe = false) {
     auto& s = pl->s;
+    const bool raar = s.prm.algorithm == PM_ALGO_RAAR;
     if (persistent(pl)) {
         const int first = s.it + 1, last = std::min(s.it + n, s.prm.max_iters);
         if (last < first) return PM_OK;
         s.it = last;
-        return solve_launch(pl, 0, first, last + 1, 0);
+        return solve_launch(pl, 0, first, last + 1, 0, probe && raar);
     }
+    bool any = false;
     for (int i = 0; i < n && s.it < s.prm.max_iters; ++i) {
         s.it += 1;
-        CKR(row(pl, s.batch, 1, s.it));        // u_it, w_it
+        any = true;
+        CKR(row(pl, s.batch, raar ? kRowRaar : kRowGS, s.it));   // u_it (x_it), w_it
         CKR(col(pl, s.batch, 2, s.it));        // metrics of u_it, stop decision, z_{it+1}
     }
+    if (any && probe && raar) CKR(row(pl, s.batch, kRowProbe, s.it + 1));   // gap + decision of x_it
     return PM_OK;
 }
 
@@ -742,10 +841,10 @@ int enqueue_finish(pm_plan* pl) {
 std::string graph_key(const pm_plan* pl) {
     const auto& s = pl->s;
     char buf[512];
-    snprintf(buf, sizeof buf, "%d|%d|%d|%d|%a|%a|%a|%d|%d|%p|%p|%lld|%p|%p|%p|%p", s.batch,
+    snprintf(buf, sizeof buf, "%d|%d|%d|%d|%a|%a|%a|%d|%d|%a|%p|%p|%lld|%p|%p|%p|%p", s.batch,
              s.prm.max_iters, s.prm.record_every, s.prm.init_complex, s.prm.early_stop_tol,
-             s.prm.t_lit, s.prm.t_dark, s.prm.p_per_mask, s.prm.algorithm, s.p, s.m, s.p_stride,
-             s.phases, s.levels, s.ustar, s.vstar);
+             s.prm.t_lit, s.prm.t_dark, s.prm.p_per_mask, s.prm.algorithm, s.prm.beta, s.p, s.m,
+             s.p_stride, s.phases, s.levels, s.ustar, s.vstar);
     return buf;
 }
 
@@ -916,10 +1015,17 @@ int pm_plan_create(int device, int n_x, int n_y, int precision, int max_batch, p
         cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
         if (n_x == n_y && ks.solve && coop) {
+            // one grid size for both algorithms' kernels: the smaller occupancy
+            int per_sm_raar = 0;
             cudaError_t e4 = allow_smem(ks.solve, ks.solve_smem);
+            if (e4 == cudaSuccess) e4 = allow_smem(ks.solve_raar, ks.solve_smem);
             if (e4 == cudaSuccess)
                 e4 = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ks.solve, ks.solve_threads,
                                                                    ks.solve_smem);
+            if (e4 == cudaSuccess)
+                e4 = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_raar, ks.solve_raar,
+                                                                   ks.solve_threads, ks.solve_smem);
+            per_sm = std::min(per_sm, per_sm_raar);
             if (e4 == cudaSuccess && per_sm > 0) pl->solve_grid = per_sm * nsm;
             cudaGetLastError();
         }
@@ -1342,7 +1448,7 @@ int pm_solve_step(pm_plan* pl, int n_iters, int* all_stopped) {
     CKR(check_plan(pl));
     std::lock_guard<std::mutex> lk(pl->mu);
     if (!pl->s.active) return set_err(PM_ERR_ARG, "no solve in progress (call pm_solve_begin)");
-    CKR(enqueue_steps(pl, n_iters));
+    CKR(enqueue_steps(pl, n_iters, true));
     std::vector<MaskState> st(pl->s.batch);
     CK(cudaMemcpyAsync(st.data(), pl->st, st.size() * sizeof(MaskState), cudaMemcpyDeviceToHost, pl->stream));
     CK(cudaStreamSynchronize(pl->stream));
@@ -1420,11 +1526,12 @@ int pm_time_sweep(pm_plan* pl, int which, int batch, int reps, float* avg_ms) {
     pm_params saved = s.prm;
     s.prm.max_iters = big;
     s.prm.record_every = 1;
+    s.prm.algorithm = PM_ALGO_GS;
     s.prm.early_stop_tol = -1.0;
     int r = PM_OK;
     for (int i = 0; i <= reps && r == PM_OK; ++i) {
         if (i == 1) CK(cudaEventRecord(pl->ev0, pl->stream));
-        r = which == 0 ? row(pl, batch, 1, 1) : col(pl, batch, 2, 1);
+        r = which == 0 ? row(pl, batch, kRowGS, 1) : col(pl, batch, 2, 1);
     }
     s.prm = saved;
     s.batch = saved_batch;

@@ -37,11 +37,13 @@ KernelSet PM_CAT3(make_set_, PM_TAG, PM_LG)() {
     s.col_iter = (const void*)&col_iter_kernel<PM_T, PM_LG, PM_LGR_COL>;
     s.col_fft = (const void*)&col_fft_kernel<PM_T, PM_LG, PM_LGR_COL>;
     s.solve = nullptr;
+    s.solve_raar = nullptr;
     s.solve_smem = 0;
     s.solve_threads = 0;
     // persistent kernel: square grids n >= 128 whose transforms fit one CTA
     if constexpr (PM_LG >= 7 && FR::TG <= kSolveThreads && FC::TG <= kSolveThreads) {
-        s.solve = (const void*)&solve_kernel<PM_T, PM_LG, PM_LGR_ROW, PM_LGR_COL>;
+        s.solve = (const void*)&solve_kernel<PM_T, PM_LG, PM_LGR_ROW, PM_LGR_COL, 0>;
+        s.solve_raar = (const void*)&solve_kernel<PM_T, PM_LG, PM_LGR_ROW, PM_LGR_COL, 1>;
         s.solve_smem = solve_smem_bytes<PM_T, PM_LG, PM_LGR_ROW, PM_LGR_COL>();
         s.solve_threads = kSolveThreads;
     }

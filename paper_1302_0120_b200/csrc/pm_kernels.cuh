@@ -48,7 +48,9 @@ struct MaskState {
     int bad;         // row sweep saw a non-finite value (iteration index)
     int n_records;
     double prev_gap;
-    double pad_;
+    int decided;     // last iteration whose record / stop decision is taken
+    int pad_;
+    double pend_lit, pend_dark;   // RAAR, sweep path: physical error of the last column sweep's iterate
 };
 
 struct SolveCtl {
@@ -58,9 +60,24 @@ struct SolveCtl {
     double t_lit, t_dark;
 };
 
+// Iterate i needs its gap: recorded, or early stopping is on (src/solver.py:173-174).
+__host__ __device__ __forceinline__ bool gap_needed(const SolveCtl& c, int i) {
+    return (i - 1) % c.record_every == 0 || c.early_tol >= 0.0;
+}
+__host__ __device__ __forceinline__ bool recorded(const SolveCtl& c, int i) { return (i - 1) % c.record_every == 0; }
+
+// Row-sweep modes.
+enum RowMode : int {
+    kRowInit = 0,    // initial iterate: no projection (src/solver.py:93-108)
+    kRowGS = 1,      // GS iterate: u = P_S v
+    kRowRaar = 2,    // RAAR iterate: x+ = b x + b P_S(2v - x) + (1 - 2b) v, gap of x
+    kRowProbe = 3,   // RAAR: only the gap of the current x (no writes)
+};
+
 template <typename T>
 struct RowArgs {
-    cx<T>* field;
+    cx<T>* field;             // source z' (and destination of w' for GS)
+    cx<T>* out;               // destination of w' (GS: == field; RAAR: the second field buffer)
     const T* p;
     long long p_stride;       // elements between masks' p (0: shared)
     const twe<T>* twf;        // forward twiddles
@@ -68,9 +85,23 @@ struct RowArgs {
     int nx, ny;
     T scale;                  // S = 1/sqrt(nx*ny)
     const double* thr_p;      // [batch] zero-branch threshold on v' = v/S (fp32: on |v'|^2, fp64: on |v'|)
-    int mode;                 // 0: no projection (initial iterate), 1: iterate
+    int mode;                 // RowMode
     int it;                   // index of the iterate this sweep produces
     MaskState* st;
+    // RAAR; unused by GS
+    cx<T>* x;                 // [batch][N] iterate x (SLM plane, true scale)
+    T beta, c1;               // beta and 1 - 2 beta, rounded to T as numpy does (NEP 50)
+    const double* thr_x;      // [batch] P_S threshold on true-scale values (fp32: on |.|^2)
+    double* rpart;            // [batch][ny * wpr][2]: gap^2 of x_{it-1}, |x_it|^2, per row warp
+    int wpr;                  // partial slots per row: max(1, TG / 32)
+    SolveCtl ctl;
+    double* hist;
+    int hist_stride;
+    const double* cpart;      // persistent path: lit/dark partials of the column sweeps
+    long long cpart_alt;      // offset of the odd-iteration buffer in cpart
+    int tpm;                  // column tasks per mask (persistent path)
+    unsigned* ctr;
+    int nblk;                 // row CTAs per mask (sweep path ticket)
 };
 
 template <typename T>
@@ -87,11 +118,23 @@ struct FinalArgs {
     cx<T>* u_star;
     double* phases;
     uint8_t* levels;
+    // RAAR: gap of the last iterate x_K = ||P_S x_K - v*|| (null x for GS)
+    const cx<T>* x;
+    const double* thr_x;
+    double* rpart;
+    int wpr;
+    SolveCtl ctl;
 };
 
 template <typename T>
 struct ColArgs {
-    cx<T>* field;
+    cx<T>* field;             // destination z' (and source for GS / init)
+    const cx<T>* in;          // source w' of an iterate sweep (GS: == field)
+    int raar;                 // RAAR: energy scale from the row partials, lit/dark kept for the row decision
+    const double* xpart;      // RAAR: row partials ([batch][ny * wpr][2], component 1 = |x|^2)
+    int xparts;               // ny * wpr
+    const double* energy;     // [batch] sum m^2
+    long long part_alt;       // persistent RAAR: offset of the odd-iteration partial buffer
     const T* m;
     long long m_stride;
     const twe<T>* twf;
@@ -111,12 +154,15 @@ struct ColArgs {
     int nblk;
 };
 
+// Lanes 0..nl-1 (every lane of this warp present in the CTA).
+__device__ __forceinline__ unsigned lane_mask(int nl) { return nl >= 32 ? 0xffffffffu : (1u << nl) - 1u; }
+
 // Fixed-order warp sum that tolerates partial warps (CTAs of < 32 threads):
 // lanes outside the CTA contribute nothing. Lane 0 holds the result.
 __device__ __forceinline__ double warp_sum(double x) {
-    const unsigned mask = __activemask();
     const int lane = threadIdx.x & 31;
     const int nl = min(32, (int)blockDim.x - (int)(threadIdx.x & ~31u));
+    const unsigned mask = lane_mask(nl);
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) {
         const double y = __shfl_xor_sync(mask, x, o);
@@ -227,10 +273,76 @@ __device__ __forceinline__ void decide(MaskState* st, double* hist_row, const So
         st->have_prev = 1;
     }
     if (i >= ctl.max_iters) stop = 1;
+    st->decided = i;
     if (stop) {
         st->stop = 1;
         st->iters_run = i;
     }
+}
+
+// Fixed-order sum of n values p[0], p[s], p[2s], ... by one warp (the lanes
+// present when the CTA is smaller than a warp): lane l takes l, l+nl, ...,
+// then a xor tree. Lane 0 holds the total.
+__device__ __forceinline__ double warp_sum_strided(const double* p, int n, int s) {
+    const int lane = threadIdx.x & 31;
+    const int nl = min(32, (int)blockDim.x - (int)(threadIdx.x & ~31u));
+    double x = 0.0;
+    for (int i = lane; i < n; i += nl) x += __ldcg(p + (size_t)i * s);
+    return warp_sum(x);
+}
+
+// RAAR decision for iterate i of mask b, by one full warp (SURVEY.md §8 a15:
+// the reference's record / early-stop logic applied to the RAAR iterate).
+// gap^2 comes from the row partials; lit/dark from `lit_dark` (host of the
+// persistent path: column-task partials [tpm][3]; sweep path: MaskState).
+__device__ __forceinline__ void decide_raar_warp(MaskState* st, double* hist, int hist_stride, const SolveCtl& ctl,
+                                                 int b, int i, const double* gparts, int ngp,
+                                                 const double* cparts, int ncp) {
+    if (i < 1 || __ldcg(&st->decided) >= i || __ldcg(&st->done)) return;
+    const bool rec = recorded(ctl, i);
+    double tot[3] = {0.0, 0.0, 0.0};
+    if (gap_needed(ctl, i)) tot[0] = warp_sum_strided(gparts, ngp, 2);
+    if (rec) {
+        if (cparts) {
+            tot[1] = warp_sum_strided(cparts + 1, ncp, 3);
+            tot[2] = warp_sum_strided(cparts + 2, ncp, 3);
+        } else {
+            tot[1] = __ldcg(&st->pend_lit);
+            tot[2] = __ldcg(&st->pend_dark);
+        }
+    }
+    if ((threadIdx.x & 31) == 0) decide(st, hist + ((size_t)b * hist_stride + (i - 1)) * 4, ctl, i, rec, tot);
+}
+
+// Group-wide sums of two per-thread values over the TG threads of a row
+// group (xor tree inside each warp); lane 0 of every warp of the group
+// stores its warp's sums into dst[w][0..1]. Called by all threads.
+template <int TG>
+__device__ __forceinline__ void row_partials(double g2, double e2, double* dst, int j, bool store) {
+    constexpr int W = TG < 32 ? TG : 32;
+    const unsigned mask = lane_mask(min(32, (int)blockDim.x - (int)(threadIdx.x & ~31u)));
+#pragma unroll
+    for (int o = W / 2; o >= 1; o >>= 1) {
+        g2 += __shfl_xor_sync(mask, g2, o);
+        e2 += __shfl_xor_sync(mask, e2, o);
+    }
+    if (store && (j & 31) == 0) {
+        dst[(j >> 5) * 2 + 0] = g2;
+        dst[(j >> 5) * 2 + 1] = e2;
+    }
+}
+
+// Round-to-nearest complex helpers with no FMA contraction, for the RAAR
+// combine, which must follow numpy's operation order.
+__device__ __forceinline__ float2 cmul_rn(float2 a, float s) { return mul2(a, make_float2(s, s)); }
+__device__ __forceinline__ double2 cmul_rn(double2 a, double s) { return make_double2(__dmul_rn(a.x, s), __dmul_rn(a.y, s)); }
+__device__ __forceinline__ float2 cadd_rn(float2 a, float2 b) { return add2(a, b); }
+__device__ __forceinline__ double2 cadd_rn(double2 a, double2 b) { return make_double2(__dadd_rn(a.x, b.x), __dadd_rn(a.y, b.y)); }
+__device__ __forceinline__ float2 csub_rn(float2 a, float2 b) { return sub2(a, b); }
+__device__ __forceinline__ double2 csub_rn(double2 a, double2 b) { return make_double2(__dsub_rn(a.x, b.x), __dsub_rn(a.y, b.y)); }
+
+template <typename C> __device__ __forceinline__ double norm_sq_d(C u) {
+    return (double)u.x * (double)u.x + (double)u.y * (double)u.y;
 }
 
 // Cross-CTA field loads bypass L1 (the field is rewritten between phases).
@@ -248,7 +360,10 @@ template <typename C> __device__ __forceinline__ C ld_field(const C* p) { return
 // A row task: the TG threads of group g transform one row. `act` == false
 // runs the same instruction stream on zeros without touching memory, so
 // group barriers stay aligned when a CTA has fewer rows than groups.
-template <typename T, int LG_L, int LG_R, class Sync>
+// ALG selects the code compiled in: 0 GS modes only, 1 RAAR modes only,
+// -1 both (the persistent kernel instantiates one algorithm at a time so the
+// other's registers do not count against it).
+template <typename T, int LG_L, int LG_R, class Sync, int ALG = -1>
 __device__ __forceinline__ void row_task(const RowArgs<T>& a, int b, int row, int j, cx<T>* sm, bool act,
                                          Sync sync) {
     using F = FftShape<LG_L, LG_R>;
@@ -259,7 +374,7 @@ __device__ __forceinline__ void row_task(const RowArgs<T>& a, int b, int row, in
 #pragma unroll
     for (int k = 0; k < F::R; ++k) v[k] = act ? ld_field(f + F::TG * k) : mk<T>(T(0), T(0));
     fft1d<T, LG_L, LG_R, +1>(v, sm, a.twi, j, sync);                 // v' = RowIFFT(z')
-    if (a.mode == 1) {
+    if (ALG != 1 && a.mode == kRowGS) {
         // u = P_S v = P_S v' (src/projections.py:69-74), threshold pre-scaled
         const T thr = T(a.thr_p[b]);
         T chk = T(0);
@@ -270,14 +385,46 @@ __device__ __forceinline__ void row_task(const RowArgs<T>& a, int b, int row, in
             chk += s2;                              // non-finite detector (reference Field checks)
         }
         if (act && !isfinite(chk)) atomicMax(&a.st[b].bad, a.it);
-    } else {
+    } else if (a.mode == kRowInit) {
+        cx<T>* xp = (ALG != 0 && a.x) ? a.x + b * N + (size_t)row * a.nx + j : nullptr;
 #pragma unroll
-        for (int k = 0; k < F::R; ++k) v[k] = cscale(v[k], a.scale);  // u0 = S * v'
+        for (int k = 0; k < F::R; ++k) {
+            v[k] = cscale(v[k], a.scale);                             // u0 = S * v'
+            if (xp && act) xp[F::TG * k] = v[k];                      // RAAR: x_0 = u0
+        }
+    } else if (ALG != 0) {
+        // RAAR, v = P_M x_{it-1} = S * v':
+        //   gap of x_{it-1} = ||P_S x_{it-1} - v|| (src/metrics.py:67-71), when needed;
+        //   x_it = beta x + beta P_S(2v - x) + (1 - 2 beta) v, numpy's operation order.
+        const int gi = a.it - 1;
+        const bool gneed = act && gi >= 1 && gap_needed(a.ctl, gi) && __ldcg(&a.st[b].decided) < gi;
+        const bool upd = a.mode == kRowRaar;
+        const T thr = T(a.thr_x[b]);
+        cx<T>* xp = a.x + b * N + (size_t)row * a.nx + j;
+        double g2 = 0.0, e2 = 0.0;
+#pragma unroll
+        for (int k = 0; k < F::R; ++k) {
+            const cx<T> vv = cscale(v[k], a.scale);
+            const cx<T> xo = act ? ld_field(xp + F::TG * k) : mk<T>(T(0), T(0));
+            const T pk = act ? p[F::TG * k] : T(0);
+            if (gneed) g2 += norm_sq_d(csub_rn(replace_mod(xo, pk, thr), vv));
+            if (upd) {
+                const cx<T> py = replace_mod(csub_rn(cscale(vv, T(2)), xo), pk, thr);
+                const cx<T> xn = cadd_rn(cadd_rn(cmul_rn(xo, a.beta), cmul_rn(py, a.beta)), cmul_rn(vv, a.c1));
+                if (act) xp[F::TG * k] = xn;
+                e2 += norm_sq_d(xn);
+                v[k] = xn;
+            }
+        }
+        if (upd && act && !isfinite(e2)) atomicMax(&a.st[b].bad, a.it);
+        row_partials<F::TG>(g2, e2, a.rpart + ((size_t)b * a.ny + row) * a.wpr * 2, j, act);
+        if (!upd) return;
     }
     fft1d<T, LG_L, LG_R, -1>(v, sm, a.twf, j, sync);                 // w' = RowFFT(u)
     if (act) {
+        cx<T>* o = a.out + (f - a.field);
 #pragma unroll
-        for (int k = 0; k < F::R; ++k) f[F::TG * k] = v[k];
+        for (int k = 0; k < F::R; ++k) o[F::TG * k] = v[k];
     }
 }
 
@@ -295,6 +442,20 @@ __device__ __forceinline__ void final_task(const FinalArgs<T>& a, int b, int row
 #pragma unroll
     for (int k = 0; k < F::R; ++k) v[k] = act ? ld_field(a.field + o + F::TG * k) : mk<T>(T(0), T(0));
     fft1d<T, LG_L, LG_R, +1>(v, sm, a.twi, j, sync);
+    if (a.x) {
+        // RAAR: gap of the last iterate, ||P_S x_K - P_M x_K|| with P_M x_K = v*
+        const int i = a.ctl.max_iters;
+        const bool gneed = act && !__ldcg(&a.st[b].stop) && gap_needed(a.ctl, i) && __ldcg(&a.st[b].decided) < i;
+        double g2 = 0.0;
+        if (gneed) {
+            const T thr = T(a.thr_x[b]);
+#pragma unroll
+            for (int k = 0; k < F::R; ++k)
+                g2 += norm_sq_d(csub_rn(replace_mod(ld_field(a.x + o + F::TG * k), p[F::TG * k], thr),
+                                        cscale(v[k], a.scale)));
+        }
+        row_partials<F::TG>(g2, 0.0, a.rpart + ((size_t)b * a.ny + row) * a.wpr * 2, j, gneed);
+    }
     if (!act) return;
     const T tol = T(a.tol_p[b]);
 #pragma unroll
@@ -335,8 +496,9 @@ __device__ __forceinline__ void col_task(const ColArgs<T>& a, int b, int col0, i
 #pragma unroll
         for (int k = 0; k < F::R; ++k) v[k] = mk<T>(act ? m[k * rs] : T(0), T(0));
     } else {
+        const cx<T>* src = (a.mode == 2 ? a.in : a.field) + (f - a.field);
 #pragma unroll
-        for (int k = 0; k < F::R; ++k) v[k] = act ? ld_field(f + k * rs) : mk<T>(T(0), T(0));
+        for (int k = 0; k < F::R; ++k) v[k] = act ? ld_field(src + k * rs) : mk<T>(T(0), T(0));
     }
     if (a.mode < 2) {
         // initial iterate u0 = F^-1(m e^{i0}): unnormalised column half
@@ -360,8 +522,22 @@ __device__ __forceinline__ void col_task(const ColArgs<T>& a, int b, int col0, i
     for (int k = 0; k < F::R; ++k) mm[k] = act ? m[k * rs] : T(0);
     if (rec && act) {
         // reconstructed intensity and physical error (src/metrics.py:74-112);
-        // the energy scale is sum m^2 / sum |u|^2 (Parseval: sum |F u|^2 = sum |u|^2)
-        const double sc = a.escale[b];
+        // the energy scale is sum m^2 / sum |u|^2 (Parseval: sum |F u|^2 = sum |u|^2).
+        // GS: u is on S, so sum |u|^2 = sum p^2 (precomputed). RAAR: sum |x|^2
+        // from the row sweep's partials, in a fixed order.
+        double sc;
+        if (a.raar) {
+            __shared__ double s_sc;
+            if (threadIdx.x < 32) {
+                const double e = warp_sum_strided(a.xpart + (size_t)b * a.xparts * 2 + 1, a.xparts, 2);
+                if (threadIdx.x == 0) s_sc = a.energy[b] / e;
+            }
+            __syncthreads();
+            sc = s_sc;
+            __syncthreads();
+        } else {
+            sc = a.escale[b];
+        }
 #pragma unroll
         for (int k = 0; k < F::R; ++k) {
             const double inten = (double)norm_sq(v[k]) * sc;
@@ -416,28 +592,59 @@ __device__ __forceinline__ void block_reduce(double (&acc)[NV], double (&tot)[NV
 
 // ------------------------------------------------------------ sweep kernels
 // One launch per sweep (general path: any power-of-two n_x x n_y).
+// Arrival ticket over the nblk CTAs of one mask: true in the last CTA to
+// arrive (after a fence, so every other CTA's global writes are visible),
+// which also re-arms the counter.
+__device__ __forceinline__ bool cta_ticket(unsigned* ctr, int nblk) {
+    __shared__ int s_last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned t = atomicAdd(ctr, 1u);
+        s_last = (t == (unsigned)(nblk - 1));
+        if (s_last) *ctr = 0u;
+    }
+    __syncthreads();
+    if (s_last) __threadfence();
+    return s_last;
+}
+
 template <typename T, int LG_L, int LG_R>
 __global__ void __launch_bounds__(256) row_iter_kernel(RowArgs<T> a) {
     using F = FftShape<LG_L, LG_R>;
     extern __shared__ __align__(16) unsigned char smraw[];
     const int b = blockIdx.y;
-    if (a.st[b].stop | a.st[b].done) return;
+    MaskState* st = a.st + b;
+    if (st->stop | st->done) return;
+    // RAAR: this sweep measures the gap of x_{it-1}; the last CTA decides it
+    const int gi = a.it - 1;
+    const bool dec = a.mode >= kRowRaar && gi >= 1 && st->decided < gi;
     const int G = blockDim.x / F::TG;
     const int g = threadIdx.x / F::TG, j = threadIdx.x % F::TG;
     row_task<T, LG_L, LG_R>(a, b, blockIdx.x * G + g, j, reinterpret_cast<cx<T>*>(smraw) + g * F::SM, true,
                             group_sync<F::TG>(g));
+    if (dec && cta_ticket(a.ctr + b, a.nblk) && threadIdx.x < 32)
+        decide_raar_warp(st, a.hist, a.hist_stride, a.ctl, b, gi, a.rpart + (size_t)b * a.ny * a.wpr * 2,
+                         a.ny * a.wpr, nullptr, 0);
 }
 
 template <typename T, int LG_L, int LG_R>
-__global__ void __launch_bounds__(256) row_final_kernel(FinalArgs<T> a) {
+__global__ void __launch_bounds__(256) row_final_kernel(FinalArgs<T> a, double* hist, int hist_stride,
+                                                        unsigned* ctr, int nblk) {
     using F = FftShape<LG_L, LG_R>;
     extern __shared__ __align__(16) unsigned char smraw[];
     const int b = blockIdx.y;
-    if (a.st[b].done) return;
+    MaskState* st = a.st + b;
+    if (st->done) return;
+    const int K = a.ctl.max_iters;
+    const bool dec = a.x && !st->stop && st->decided < K;
     const int G = blockDim.x / F::TG;
     const int g = threadIdx.x / F::TG, j = threadIdx.x % F::TG;
     final_task<T, LG_L, LG_R>(a, b, blockIdx.x * G + g, j, reinterpret_cast<cx<T>*>(smraw) + g * F::SM, true,
                               group_sync<F::TG>(g));
+    if (dec && cta_ticket(ctr + b, nblk) && threadIdx.x < 32)
+        decide_raar_warp(st, hist, hist_stride, a.ctl, b, K, a.rpart + (size_t)b * a.ny * a.wpr * 2,
+                         a.ny * a.wpr, nullptr, 0);
 }
 
 // Largest CTA a column kernel is launched with (see col_config in pm_capi.cu):
@@ -457,6 +664,16 @@ __global__ void __launch_bounds__(col_max_threads<LG_L, LG_R>()) col_iter_kernel
     col_task<T, LG_L, LG_R, 0>(a, b, blockIdx.x * C, C, reinterpret_cast<cx<T>*>(smraw), true, acc);
     if (a.mode < 2 || a.u_iter < 1) return;
     double tot[3];
+    if (a.raar) {
+        // lit/dark of x_{u_iter}, kept for the decision the next row sweep takes
+        if (recorded(a.ctl, a.u_iter) &&
+            reduce_ticket<3>(acc, a.part + (size_t)b * a.nblk * 3, a.ctr + b, a.nblk, blockIdx.x, tot) &&
+            threadIdx.x == 0) {
+            st->pend_lit = tot[1];
+            st->pend_dark = tot[2];
+        }
+        return;
+    }
     if (reduce_ticket<3>(acc, a.part + (size_t)b * a.nblk * 3, a.ctr + b, a.nblk, blockIdx.x, tot)) {
         if (threadIdx.x == 0) {
             const int i = a.u_iter;
@@ -518,6 +735,7 @@ struct SolveArgs {
     int do_init;               // run the initial-iterate phases first
     int do_final;              // finish with the best-approximation pair
     int init_mode;             // column init from real m (0) or complex field (1)
+    int do_probe;              // RAAR: end with the gap / decision of the last iterate
     unsigned long long* stamps; // optional: globaltimer at every phase boundary (CTA 0)
 };
 
@@ -536,7 +754,7 @@ __device__ __forceinline__ bool mask_live(const MaskState* st) {
     return !(__ldcg(&st->stop) | __ldcg(&st->done));
 }
 
-template <typename T, int LG, int LGR_R, int LGR_C>
+template <typename T, int LG, int LGR_R, int LGR_C, int ALG>
 __device__ __forceinline__ void row_phase(const RowArgs<T>& a, int batch, cx<T>* smem) {
     using F = FftShape<LG, LGR_R>;
     const int G = blockDim.x / F::TG;
@@ -546,8 +764,8 @@ __device__ __forceinline__ void row_phase(const RowArgs<T>& a, int batch, cx<T>*
         const int r = base + g;
         const int b = r >> LG;
         const bool act = r < total && mask_live(a.st + (r < total ? b : 0));
-        row_task<T, LG, LGR_R>(a, r < total ? b : 0, r & ((1 << LG) - 1), j, smem + g * F::SM, act,
-                               group_sync<F::TG>(g));
+        row_task<T, LG, LGR_R, decltype(group_sync<F::TG>(g)), ALG>(a, r < total ? b : 0, r & ((1 << LG) - 1), j,
+                                                                   smem + g * F::SM, act, group_sync<F::TG>(g));
     }
 }
 
@@ -574,7 +792,11 @@ __device__ __forceinline__ void col_phase(const ColArgs<T>& a, int batch, cx<T>*
     const int C = blockDim.x / F::TG;
     const int tpm = (1 << LG) / C;          // tasks per mask
     const int total = batch * tpm;
-    const bool metr = a.mode == 2 && a.u_iter >= 1;
+    // RAAR keeps only lit/dark (the gap comes from the row sweep), in a
+    // parity-selected buffer: the decision on x_{it-1} reads it while this
+    // phase of iteration it may already run
+    const bool metr = a.mode == 2 && a.u_iter >= 1 && (!a.raar || recorded(a.ctl, a.u_iter));
+    double* const part = a.part + ((a.raar && (a.u_iter & 1)) ? a.part_alt : 0);
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
         const int b = t / tpm, tt = t - b * tpm;
         const bool act = mask_live(a.st + b);
@@ -584,7 +806,7 @@ __device__ __forceinline__ void col_phase(const ColArgs<T>& a, int batch, cx<T>*
             double tot[3];
             block_reduce<3>(acc, tot);
             if (threadIdx.x == 0) {
-                double* q = a.part + ((size_t)b * tpm + tt) * 3;
+                double* q = part + ((size_t)b * tpm + tt) * 3;
                 q[0] = tot[0]; q[1] = tot[1]; q[2] = tot[2];
             }
         }
@@ -620,6 +842,19 @@ __device__ __forceinline__ void decide_phase(const ColArgs<T>& a, int batch) {
     }
 }
 
+// RAAR decision on iterate i of every live mask, by CTA (b mod grid): gap
+// from the row partials, lit/dark from the column partials of iteration i.
+template <typename T>
+__device__ __forceinline__ void decide_phase_raar(const RowArgs<T>& r, int batch, int i) {
+    if (threadIdx.x >= 32 || i < 1) return;
+    for (int b = blockIdx.x; b < batch; b += gridDim.x) {
+        MaskState* st = r.st + b;
+        if (!mask_live(st)) continue;
+        decide_raar_warp(st, r.hist, r.hist_stride, r.ctl, b, i, r.rpart + (size_t)b * r.ny * r.wpr * 2,
+                         r.ny * r.wpr, r.cpart + ((i & 1) ? r.cpart_alt : 0) + (size_t)b * r.tpm * 3, r.tpm);
+    }
+}
+
 #ifndef PM_SOLVE_NT
 #define PM_SOLVE_NT 512
 #endif
@@ -638,7 +873,7 @@ __host__ __device__ constexpr int solve_smem_bytes() {
     return (int)sizeof(cx<T>) * (rows > cols ? rows : cols);
 }
 
-template <typename T, int LG, int LGR_R, int LGR_C>
+template <typename T, int LG, int LGR_R, int LGR_C, int ALG>
 __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(SolveArgs<T> a) {
     extern __shared__ __align__(16) unsigned char smraw[];
     cx<T>* smem = reinterpret_cast<cx<T>*>(smraw);
@@ -653,19 +888,50 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(SolveArgs<T> a)
         col_phase<T, LG, LGR_R, LGR_C>(c, B, smem);       // u0 column half
         grid_sync(a.bar, epoch);
         RowArgs<T> r = a.row;
-        r.mode = 0;
-        row_phase<T, LG, LGR_R, LGR_C>(r, B, smem);       // u0 row half, w0
+        r.mode = kRowInit;
+        row_phase<T, LG, LGR_R, LGR_C, ALG>(r, B, smem);       // u0 row half, w0 (RAAR: and x_0)
         grid_sync(a.bar, epoch);
         c.mode = 2;
         col_phase<T, LG, LGR_R, LGR_C>(c, B, smem);       // z1
         grid_sync(a.bar, epoch);
     }
     const bool early = a.col.ctl.early_tol >= 0.0;
+    if constexpr (ALG == 1) {
+        // RAAR: the decision on x_{it-1} follows the row phase that measures its gap
+        for (int it = a.it_begin; it < a.it_end; ++it) {
+            RowArgs<T> r = a.row;
+            r.mode = kRowRaar;
+            r.it = it;
+            row_phase<T, LG, LGR_R, LGR_C, ALG>(r, B, smem);   // gap of x_{it-1}, x_it, w_it
+            grid_sync(a.bar, epoch);
+            decide_phase_raar<T>(r, B, it - 1);
+            if (early) grid_sync(a.bar, epoch);
+            ColArgs<T> c = a.col;
+            c.mode = 2;
+            c.u_iter = it;
+            col_phase<T, LG, LGR_R, LGR_C>(c, B, smem);   // lit/dark of x_it, z_{it+1}
+            grid_sync(a.bar, epoch);
+        }
+        if (a.do_probe) {
+            RowArgs<T> r = a.row;
+            r.mode = kRowProbe;
+            r.it = a.it_end;
+            row_phase<T, LG, LGR_R, LGR_C, ALG>(r, B, smem);   // gap of x_{it_end-1}
+            grid_sync(a.bar, epoch);
+            decide_phase_raar<T>(r, B, a.it_end - 1);
+            grid_sync(a.bar, epoch);
+        }
+        if (a.do_final) {
+            final_phase<T, LG, LGR_R, LGR_C>(a.fin, B, smem);   // pair, mask, gap of x_K
+            grid_sync(a.bar, epoch);
+            decide_phase_raar<T>(a.row, B, a.fin.ctl.max_iters);
+        }
+    } else {
     for (int it = a.it_begin; it < a.it_end; ++it) {
         RowArgs<T> r = a.row;
-        r.mode = 1;
+        r.mode = kRowGS;
         r.it = it;
-        row_phase<T, LG, LGR_R, LGR_C>(r, B, smem);       // u_it, w_it
+        row_phase<T, LG, LGR_R, LGR_C, ALG>(r, B, smem);       // u_it, w_it
         stamp(a.stamps, si);
         grid_sync(a.bar, epoch);
         stamp(a.stamps, si);
@@ -680,6 +946,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(SolveArgs<T> a)
         if (early) grid_sync(a.bar, epoch);                      // stop flags must be seen by every CTA
     }
     if (a.do_final) final_phase<T, LG, LGR_R, LGR_C>(a.fin, B, smem);
+    }
     stamp(a.stamps, si);
 }
 

@@ -20,7 +20,8 @@ struct KernelSet {
     const void* row_fft;    // row_fft_kernel<T, lg, lgR_row>
     const void* col_iter;   // col_iter_kernel<T, lg, lgR_col>
     const void* col_fft;    // col_fft_kernel<T, lg, lgR_col>
-    const void* solve;      // solve_kernel<T, lg, lgR_row, lgR_col> (square grids, lg >= 7) or null
+    const void* solve;      // solve_kernel<T, lg, lgR_row, lgR_col, GS> (square grids, lg >= 7) or null
+    const void* solve_raar; // the same for RAAR
     int solve_smem;         // its dynamic shared memory (bytes)
     int solve_threads;      // its CTA size
     AxisShape row, col;

@@ -92,7 +92,12 @@ def random_spot_centers(spec: GridSpec, n_spots: int, seed: int,
         draw = lambda: rng.integers(lo_x, hi_x, 2)  # noqa: E731  (square: one call, as §8d)
     else:
         draw = lambda: (rng.integers(lo_x, hi_x), rng.integers(lo_y, hi_y))  # noqa: E731
+    tries = 0
     while len(chosen) < n_spots:
+        tries += 1
+        if tries > 200 * n_spots + 10000:
+            raise ValueError(f"cannot place {n_spots} spots {math.sqrt(min_sep2):g} px apart "
+                             f"on a {spec.n_x}x{spec.n_y} grid")
         j, k = draw()
         j, k = int(j), int(k)
         if all((j - a) ** 2 + (k - b) ** 2 >= min_sep2 for a, b in chosen):

@@ -19,9 +19,9 @@ for n, tag in [cases[i] for i in sel]:
     plan = pm.transform.get_plan(spec, prec)
     plan.lib.pm_debug_phase_stamps(plan.handle, 1, None, 0)
     r = pm.solve(c, mm, cfg)
-    st = np.zeros(148 * SPC, dtype=np.uint64)
+    st = np.zeros(1184 * SPC, dtype=np.uint64)
     plan.lib.pm_debug_phase_stamps(plan.handle, 0, st.ctypes.data_as(_lib.C.c_void_p), st.size)
-    S = st.reshape(148, SPC).astype(np.int64)
+    S = st.reshape(1184, SPC).astype(np.int64)
     ncta = int((S[:, 0] > 0).sum())
     S = S[:ncta]
     t0 = S[:, 0].min()

@@ -8,7 +8,7 @@ from paper_1302_0120_b200.patterns import make_problem
 
 def run(n, tag, K=100, batch=1):
     prec = pm.Precision.from_tag(tag)
-    p, m = make_problem(n, 50, 7)
+    p, m = make_problem(n, 50 if n >= 128 else 4, 7)
     plan = pm.transform.get_plan(pm.GridSpec(n, n), prec)
     fdt = prec.float_dtype
     P = np.ascontiguousarray(p, fdt); M = np.ascontiguousarray(np.broadcast_to(m, (batch,) + m.shape), fdt)

@@ -174,15 +174,6 @@ def test_batch_per_mask_amplitude_and_early_stop():
         np.testing.assert_array_equal(r.mask.phases, res.phases[i])
 
 
-def test_raar_is_not_yet_available_message():
-    spec, c, m = problem(64)
-    try:
-        r = pm.solve(c, m, pm.SolveConfig(max_iters=5, algorithm="raar"))
-    except NotImplementedError:
-        pytest.skip("RAAR not built")
-    assert r.iters_run == 5
-
-
 @pytest.mark.slow
 @pytest.mark.parametrize("n", [2048, 4096])
 def test_large_field_properties(n):
