@@ -41,28 +41,39 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found: the CUDA toolkit is required to build phasemask_b200")
 
 
-# log2 points per thread of the row / column kernels, per precision
-# (see DESIGN.md "Kernel configuration"); override for experiments with
-# PM_LGR="f32row,f32col,f64row,f64col".
-DEFAULT_LGR = {"f32": (4, 4), "f64": (4, 3)}
+# log2 points per thread of the row / column kernels and the persistent
+# kernel's CTA size, per precision and size (DESIGN.md "Kernel
+# configuration"); override every size at once for experiments with
+# PM_LGR="f32row,f32col,f64row,f64col" and PM_SOLVE_NT="f32,f64".
+# Measured on B200 (profiles/): radix-32 rows and columns with a
+# 256-thread persistent CTA up to 1024^2 fp32; radix-16 and 512 threads for
+# the HBM-resident 2048^2 / 4096^2 grids and for fp64.
+def default_config(tag: str, lg: int) -> tuple[int, int, int]:
+    """(log2 points per thread of rows, of columns, persistent CTA size)."""
+    if tag == "f32":
+        return (5, 5, 256) if lg <= 10 else (4, 4, 512)
+    return (4, 3, 512)
 
 
-def _lgr():
+def _config(tag: str, lg: int) -> tuple[int, int, int]:
+    row, col, nt = default_config(tag, lg)
     env = os.environ.get("PM_LGR")
     if env:
         a = [int(x) for x in env.split(",")]
-        return {"f32": (a[0], a[1]), "f64": (a[2], a[3])}
-    return DEFAULT_LGR
+        row, col = (a[0], a[1]) if tag == "f32" else (a[2], a[3])
+    env = os.environ.get("PM_SOLVE_NT")
+    if env:
+        a = [int(x) for x in env.split(",")]
+        nt = a[0] if tag == "f32" else a[-1]
+    return row, col, nt
 
 
 def _units(build_dir):
     units = []
-    lgr = _lgr()
-    nt = int(os.environ.get("PM_SOLVE_NT", "512"))
     for f64 in (0, 1):
         tag = "f64" if f64 else "f32"
-        row, col = lgr[tag]
         for lg in range(MAX_LG + 1):
+            row, col, nt = _config(tag, lg)
             units.append((CSRC / "pm_inst.cu", build_dir / f"pm_inst_{tag}_{lg}_{row}{col}_{nt}.o",
                           [f"-DPM_F64={f64}", f"-DPM_LG={lg}", f"-DPM_LGR_ROW={row}", f"-DPM_LGR_COL={col}",
                            f"-DPM_SOLVE_NT={nt}"]))

@@ -369,7 +369,7 @@ RowCfg row_config(const pm_plan* pl) {
 ColCfg col_config(const pm_plan* pl) {
     const AxisShape& k = kset(pl->prec, pl->lgy).col;
     ColCfg c;
-    const int maxt = k.TG <= 64 ? 256 : 512;
+    const int maxt = col_max_threads_for(k.lgR, k.TG);
     c.C = std::max(1, maxt / k.TG);
     c.C = std::min(c.C, pl->nx);
     c.threads = c.C * k.TG;

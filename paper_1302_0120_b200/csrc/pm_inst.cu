@@ -44,7 +44,7 @@ KernelSet PM_CAT3(make_set_, PM_TAG, PM_LG)() {
     if constexpr (PM_LG >= 7 && FR::TG <= kSolveThreads && FC::TG <= kSolveThreads) {
         s.solve = (const void*)&solve_kernel<PM_T, PM_LG, PM_LGR_ROW, PM_LGR_COL, 0>;
         s.solve_raar = (const void*)&solve_kernel<PM_T, PM_LG, PM_LGR_ROW, PM_LGR_COL, 1>;
-        s.solve_smem = solve_smem_bytes<PM_T, PM_LG, PM_LGR_ROW, PM_LGR_COL>();
+        s.solve_smem = SolveSmem<PM_T, PM_LG, PM_LGR_ROW, PM_LGR_COL>::BYTES;
         s.solve_threads = kSolveThreads;
     }
     s.row = AxisShape{FR::lgR, FR::TG, FR::NP, FR::SM, FR::TW};

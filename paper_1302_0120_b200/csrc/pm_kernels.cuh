@@ -357,23 +357,71 @@ template <typename C> __device__ __forceinline__ C ld_field(const C* p) { return
 // host (exact for power-of-two grids, where S is a power of two), because
 // P_S(v) = P_S(v / S).
 
-// A row task: the TG threads of group g transform one row. `act` == false
-// runs the same instruction stream on zeros without touching memory, so
-// group barriers stay aligned when a CTA has fewer rows than groups.
+// ------------------------------------------------------- shared staging
+// cp.async copies of a task's real grid (p or m) into shared memory, issued
+// with the field loads so their latency overlaps the first transform
+// (persistent kernel; the sweep kernels read the grid from global memory).
+template <int BYTES>
+__device__ __forceinline__ void cp_async(void* dst, const void* src) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    if constexpr (BYTES == 16)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(d), "l"(src), "n"(BYTES) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// Copy `rows` runs of `run` contiguous elements (global stride `gstride`)
+// into a dense [rows][run] shared array, with `nthr` threads (thread `t`),
+// in copies of CH bytes (CH divides run * sizeof(T)).
+template <typename T, int CH>
+__device__ __forceinline__ void stage_runs(T* dst, const T* src, int rows, int run, size_t gstride, int t,
+                                           int nthr) {
+    constexpr int EPC = CH / (int)sizeof(T);                     // elements per copy
+    const int cpr = run / EPC;                                   // copies per run
+    for (int i = t; i < rows * cpr; i += nthr) {
+        const int r = i / cpr, q = i - r * cpr;
+        cp_async<CH>(dst + (size_t)r * run + q * EPC, src + r * gstride + q * EPC);
+    }
+}
+
+// A row task: the TG threads of group g transform one row. `inb` == false
+// (row beyond the batch) runs the same instruction stream on zeros without
+// touching memory, so group barriers stay aligned when a CTA has fewer rows
+// than groups; `live` == false (mask already stopped) loads but stores
+// nothing. `twf` / `twi` are the row tables (shared copies when TS); `ps`,
+// when PS, is this row's slice of p staged in shared memory.
 // ALG selects the code compiled in: 0 GS modes only, 1 RAAR modes only,
 // -1 both (the persistent kernel instantiates one algorithm at a time so the
 // other's registers do not count against it).
-template <typename T, int LG_L, int LG_R, class Sync, int ALG = -1>
-__device__ __forceinline__ void row_task(const RowArgs<T>& a, int b, int row, int j, cx<T>* sm, bool act,
+template <typename T, int LG_L, int LG_R, class Sync, int ALG = -1, bool TS = false, bool PS = false>
+__device__ __forceinline__ void row_task(const RowArgs<T>& a, int b, int row, int j, cx<T>* sm,
+                                         const twe<T>* twf, const twe<T>* twi, T* ps, bool inb, bool live,
                                          Sync sync) {
     using F = FftShape<LG_L, LG_R>;
     const size_t N = (size_t)a.nx * a.ny;
+    const bool act = inb && live;
     cx<T>* f = a.field + b * N + (size_t)row * a.nx + j;
     const T* p = a.p + b * a.p_stride + (size_t)row * a.nx + j;
     cx<T> v[F::R];
 #pragma unroll
-    for (int k = 0; k < F::R; ++k) v[k] = act ? ld_field(f + F::TG * k) : mk<T>(T(0), T(0));
-    fft1d<T, LG_L, LG_R, +1>(v, sm, a.twi, j, sync);                 // v' = RowIFFT(z')
+    for (int k = 0; k < F::R; ++k) v[k] = inb ? ld_field(f + F::TG * k) : mk<T>(T(0), T(0));
+    if constexpr (PS) {
+        if (inb && a.mode != kRowInit) {
+            stage_runs<T, 16>(ps, p - j, 1, 1 << LG_L, 0, j, F::TG);
+            cp_async_commit();
+        }
+    }
+    fft1d<T, LG_L, LG_R, +1, TS>(v, sm, twi, j, sync);              // v' = RowIFFT(z')
+    if constexpr (PS) {
+        cp_async_wait_all();
+        sync();
+    }
+    auto p_at = [&](int k) -> T {
+        if constexpr (PS) return ps[j + F::TG * k];
+        else return p[F::TG * k];
+    };
     if (ALG != 1 && a.mode == kRowGS) {
         // u = P_S v = P_S v' (src/projections.py:69-74), threshold pre-scaled
         const T thr = T(a.thr_p[b]);
@@ -381,7 +429,7 @@ __device__ __forceinline__ void row_task(const RowArgs<T>& a, int b, int row, in
 #pragma unroll
         for (int k = 0; k < F::R; ++k) {
             T s2;
-            v[k] = replace_mod(v[k], act ? p[F::TG * k] : T(0), thr, s2);
+            v[k] = replace_mod(v[k], inb ? p_at(k) : T(0), thr, s2);
             chk += s2;                              // non-finite detector (reference Field checks)
         }
         if (act && !isfinite(chk)) atomicMax(&a.st[b].bad, a.it);
@@ -405,8 +453,8 @@ __device__ __forceinline__ void row_task(const RowArgs<T>& a, int b, int row, in
 #pragma unroll
         for (int k = 0; k < F::R; ++k) {
             const cx<T> vv = cscale(v[k], a.scale);
-            const cx<T> xo = act ? ld_field(xp + F::TG * k) : mk<T>(T(0), T(0));
-            const T pk = act ? p[F::TG * k] : T(0);
+            const cx<T> xo = inb ? ld_field(xp + F::TG * k) : mk<T>(T(0), T(0));
+            const T pk = inb ? p_at(k) : T(0);
             if (gneed) g2 += norm_sq_d(csub_rn(replace_mod(xo, pk, thr), vv));
             if (upd) {
                 const cx<T> py = replace_mod(csub_rn(cscale(vv, T(2)), xo), pk, thr);
@@ -418,9 +466,12 @@ __device__ __forceinline__ void row_task(const RowArgs<T>& a, int b, int row, in
         }
         if (upd && act && !isfinite(e2)) atomicMax(&a.st[b].bad, a.it);
         row_partials<F::TG>(g2, e2, a.rpart + ((size_t)b * a.ny + row) * a.wpr * 2, j, act);
-        if (!upd) return;
+        if (!upd) {
+            if constexpr (PS) sync();              // ps is restaged by the next task
+            return;
+        }
     }
-    fft1d<T, LG_L, LG_R, -1>(v, sm, a.twf, j, sync);                 // w' = RowFFT(u)
+    fft1d<T, LG_L, LG_R, -1, TS>(v, sm, twf, j, sync);              // w' = RowFFT(u)
     if (act) {
         cx<T>* o = a.out + (f - a.field);
 #pragma unroll
@@ -431,9 +482,9 @@ __device__ __forceinline__ void row_task(const RowArgs<T>& a, int b, int row, in
 // Best-approximation pair for one row: v* = P_M u_K = S * RowIFFT(z'),
 // u* = P_S v*, mask = phases_of(u*, zero_tol_p)
 // (src/solver.py:201-206, src/grid.py:168-176).
-template <typename T, int LG_L, int LG_R, class Sync>
-__device__ __forceinline__ void final_task(const FinalArgs<T>& a, int b, int row, int j, cx<T>* sm, bool act,
-                                           Sync sync) {
+template <typename T, int LG_L, int LG_R, bool TS = false, class Sync>
+__device__ __forceinline__ void final_task(const FinalArgs<T>& a, int b, int row, int j, cx<T>* sm,
+                                           const twe<T>* twi, bool act, Sync sync) {
     using F = FftShape<LG_L, LG_R>;
     const size_t N = (size_t)a.nx * a.ny;
     const size_t o = b * N + (size_t)row * a.nx + j;
@@ -441,7 +492,7 @@ __device__ __forceinline__ void final_task(const FinalArgs<T>& a, int b, int row
     cx<T> v[F::R];
 #pragma unroll
     for (int k = 0; k < F::R; ++k) v[k] = act ? ld_field(a.field + o + F::TG * k) : mk<T>(T(0), T(0));
-    fft1d<T, LG_L, LG_R, +1>(v, sm, a.twi, j, sync);
+    fft1d<T, LG_L, LG_R, +1, TS>(v, sm, twi, j, sync);
     if (a.x) {
         // RAAR: gap of the last iterate, ||P_S x_K - P_M x_K|| with P_M x_K = v*
         const int i = a.ctl.max_iters;
@@ -478,8 +529,11 @@ __device__ __forceinline__ void final_task(const FinalArgs<T>& a, int b, int row
 // A column task: C interleaved transforms (thread c + C*j) over columns
 // col0..col0+C-1 of mask b. NX > 0 fixes n_x at compile time (square
 // persistent path) so every column access is base + immediate offset.
-template <typename T, int LG_L, int LG_R, int NX>
-__device__ __forceinline__ void col_task(const ColArgs<T>& a, int b, int col0, int C, cx<T>* smbase, bool act,
+// `twf` / `twi` are the column tables (shared copies when TS); `ms`, when
+// PS, receives this task's [n_y][C] slice of m through cp.async.
+template <typename T, int LG_L, int LG_R, int NX, bool TS = false, bool PS = false, int CH = 16>
+__device__ __forceinline__ void col_task(const ColArgs<T>& a, int b, int col0, int C, cx<T>* smbase,
+                                         const twe<T>* twf, const twe<T>* twi, T* ms, bool live,
                                          double (&acc)[3]) {
     using F = FftShape<LG_L, LG_R>;
     const int c = threadIdx.x % C, j = threadIdx.x / C;
@@ -489,37 +543,49 @@ __device__ __forceinline__ void col_task(const ColArgs<T>& a, int b, int col0, i
     cx<T>* sm = smbase + c * col_stride<T, F::SM>(C);
     cx<T>* f = a.field + b * N + (size_t)j * nx + col0 + c;
     const T* m = a.m + b * a.m_stride + (size_t)j * nx + col0 + c;
+    const bool act = live;
     acc[0] = acc[1] = acc[2] = 0.0;
 
     cx<T> v[F::R];
     if (a.mode == 0) {
 #pragma unroll
-        for (int k = 0; k < F::R; ++k) v[k] = mk<T>(act ? m[k * rs] : T(0), T(0));
+        for (int k = 0; k < F::R; ++k) v[k] = mk<T>(m[k * rs], T(0));
     } else {
         const cx<T>* src = (a.mode == 2 ? a.in : a.field) + (f - a.field);
 #pragma unroll
-        for (int k = 0; k < F::R; ++k) v[k] = act ? ld_field(src + k * rs) : mk<T>(T(0), T(0));
+        for (int k = 0; k < F::R; ++k) v[k] = ld_field(src + k * rs);
     }
     if (a.mode < 2) {
         // initial iterate u0 = F^-1(m e^{i0}): unnormalised column half
         // (src/solver.py:93-108); the row phase applies S
-        fft1d<T, LG_L, LG_R, +1>(v, sm, a.twi, j, SyncBlock{});
+        fft1d<T, LG_L, LG_R, +1, TS>(v, sm, twi, j, SyncBlock{});
         if (act) {
 #pragma unroll
             for (int k = 0; k < F::R; ++k) f[k * rs] = v[k];
         }
         return;
     }
-    fft1d<T, LG_L, LG_R, -1>(v, sm, a.twf, j, SyncBlock{});
+    if constexpr (PS) {
+        stage_runs<T, CH>(ms, a.m + b * a.m_stride + col0, a.ny, C, nx, threadIdx.x, blockDim.x);
+        cp_async_commit();
+    }
+    fft1d<T, LG_L, LG_R, -1, TS>(v, sm, twf, j, SyncBlock{});
 #pragma unroll
     for (int k = 0; k < F::R; ++k) v[k] = cscale(v[k], a.scale);     // u^ = F(u) = S * ColFFT(w')
 
     const bool metr = a.u_iter >= 1;
     const bool rec = metr && ((a.u_iter - 1) % a.ctl.record_every == 0);
     const T thr = T(a.thr_m[b]);
+    if constexpr (PS) {
+        cp_async_wait_all();
+        __syncthreads();
+    }
     T mm[F::R];
 #pragma unroll
-    for (int k = 0; k < F::R; ++k) mm[k] = act ? m[k * rs] : T(0);
+    for (int k = 0; k < F::R; ++k) {
+        if constexpr (PS) mm[k] = ms[(j + F::TG * k) * C + c];
+        else mm[k] = m[k * rs];
+    }
     if (rec && act) {
         // reconstructed intensity and physical error (src/metrics.py:74-112);
         // the energy scale is sum m^2 / sum |u|^2 (Parseval: sum |F u|^2 = sum |u|^2).
@@ -560,7 +626,7 @@ __device__ __forceinline__ void col_task(const ColArgs<T>& a, int b, int col0, i
         v[k] = vh;
     }
     acc[0] = act ? (double)g2 : 0.0;
-    fft1d<T, LG_L, LG_R, +1>(v, sm, a.twi, j, SyncBlock{});         // z' = ColIFFT(v^)
+    fft1d<T, LG_L, LG_R, +1, TS>(v, sm, twi, j, SyncBlock{});         // z' = ColIFFT(v^)
     if (act) {
 #pragma unroll
         for (int k = 0; k < F::R; ++k) f[k * rs] = v[k];
@@ -621,8 +687,8 @@ __global__ void __launch_bounds__(256) row_iter_kernel(RowArgs<T> a) {
     const bool dec = a.mode >= kRowRaar && gi >= 1 && st->decided < gi;
     const int G = blockDim.x / F::TG;
     const int g = threadIdx.x / F::TG, j = threadIdx.x % F::TG;
-    row_task<T, LG_L, LG_R>(a, b, blockIdx.x * G + g, j, reinterpret_cast<cx<T>*>(smraw) + g * F::SM, true,
-                            group_sync<F::TG>(g));
+    row_task<T, LG_L, LG_R>(a, b, blockIdx.x * G + g, j, reinterpret_cast<cx<T>*>(smraw) + g * F::SM, a.twf,
+                            a.twi, nullptr, true, true, group_sync<F::TG>(g));
     if (dec && cta_ticket(a.ctr + b, a.nblk) && threadIdx.x < 32)
         decide_raar_warp(st, a.hist, a.hist_stride, a.ctl, b, gi, a.rpart + (size_t)b * a.ny * a.wpr * 2,
                          a.ny * a.wpr, nullptr, 0);
@@ -640,17 +706,19 @@ __global__ void __launch_bounds__(256) row_final_kernel(FinalArgs<T> a, double* 
     const bool dec = a.x && !st->stop && st->decided < K;
     const int G = blockDim.x / F::TG;
     const int g = threadIdx.x / F::TG, j = threadIdx.x % F::TG;
-    final_task<T, LG_L, LG_R>(a, b, blockIdx.x * G + g, j, reinterpret_cast<cx<T>*>(smraw) + g * F::SM, true,
-                              group_sync<F::TG>(g));
+    final_task<T, LG_L, LG_R>(a, b, blockIdx.x * G + g, j, reinterpret_cast<cx<T>*>(smraw) + g * F::SM, a.twi,
+                              true, group_sync<F::TG>(g));
     if (dec && cta_ticket(ctr + b, nblk) && threadIdx.x < 32)
         decide_raar_warp(st, hist, hist_stride, a.ctl, b, K, a.rpart + (size_t)b * a.ny * a.wpr * 2,
                          a.ny * a.wpr, nullptr, 0);
 }
 
 // Largest CTA a column kernel is launched with (see col_config in pm_capi.cu):
-// 256 threads while a transform needs <= 64 threads, else 512.
+// 256 threads while a transform needs <= 64 threads or holds >= 32 points per
+// thread (register budget), else 512.
+__host__ __device__ constexpr int col_max_threads_for(int lgR, int TG) { return (TG <= 64 || lgR >= 5) ? 256 : 512; }
 template <int LG_L, int LG_R>
-constexpr int col_max_threads() { return FftShape<LG_L, LG_R>::TG <= 64 ? 256 : 512; }
+constexpr int col_max_threads() { return col_max_threads_for(FftShape<LG_L, LG_R>::lgR, FftShape<LG_L, LG_R>::TG); }
 
 template <typename T, int LG_L, int LG_R>
 __global__ void __launch_bounds__(col_max_threads<LG_L, LG_R>()) col_iter_kernel(ColArgs<T> a) {
@@ -661,7 +729,8 @@ __global__ void __launch_bounds__(col_max_threads<LG_L, LG_R>()) col_iter_kernel
     if (st->stop | st->done) return;
     const int C = blockDim.x / F::TG;
     double acc[3];
-    col_task<T, LG_L, LG_R, 0>(a, b, blockIdx.x * C, C, reinterpret_cast<cx<T>*>(smraw), true, acc);
+    col_task<T, LG_L, LG_R, 0>(a, b, blockIdx.x * C, C, reinterpret_cast<cx<T>*>(smraw), a.twf, a.twi, nullptr,
+                               true, acc);
     if (a.mode < 2 || a.u_iter < 1) return;
     double tot[3];
     if (a.raar) {
@@ -704,21 +773,16 @@ __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// Grid barrier: every CTA releases one arrival (no returned atomic), CTA 0
-// alone polls the arrival count and publishes the epoch, the others poll the
-// epoch word. `epoch` counts this launch's barriers (identical in all CTAs).
+// Grid barrier: every CTA releases one arrival (no returned atomic) and
+// polls the monotonic arrival count until the whole grid has arrived at this
+// epoch; `epoch` counts this launch's barriers (identical in all CTAs).
 __device__ __forceinline__ void grid_sync(GridBar* bar, unsigned& epoch) {
     __syncthreads();
     ++epoch;
     if (threadIdx.x == 0) {
         red_release_add(&bar->count, 1u);
-        if (blockIdx.x == 0) {
-            const unsigned target = epoch * gridDim.x;
-            while (ld_acquire(&bar->count) < target) {
-            }
-            st_release(&bar->gen, epoch);
-        } else {
-            while (ld_acquire(&bar->gen) < epoch) __nanosleep(16);
+        const unsigned target = epoch * gridDim.x;
+        while (ld_acquire(&bar->count) < target) {
         }
     }
     __syncthreads();
@@ -754,24 +818,109 @@ __device__ __forceinline__ bool mask_live(const MaskState* st) {
     return !(__ldcg(&st->stop) | __ldcg(&st->done));
 }
 
+#ifndef PM_SOLVE_NT
+#define PM_SOLVE_NT 512
+#endif
+constexpr int kSolveThreads = PM_SOLVE_NT;
+
+// Shared-memory layout of solve_kernel: the FFT exchange buffers (the larger
+// of the row phase's G transforms and the column phase's C interleaved ones),
+// then, while they fit, the staged real grid of a task (p rows / m columns,
+// PS) and copies of the twiddle tables (TS; L1 does not survive the grid
+// barrier's acquire, so tables read through L1 would miss once per pass).
+template <typename T, int LG, int LGR_R, int LGR_C>
+struct SolveSmem {
+    using FR = FftShape<LG, LGR_R>;
+    using FC = FftShape<LG, LGR_C>;
+    static constexpr int G = kSolveThreads / FR::TG > 0 ? kSolveThreads / FR::TG : 1;
+    static constexpr int C = kSolveThreads / FC::TG > 0 ? kSolveThreads / FC::TG : 1;
+    static constexpr int rows = G * FR::SM;
+    static constexpr int pad = 128 / (int)(sizeof(cx<T>) * C) > 0 ? 128 / (int)(sizeof(cx<T>) * C) : 1;
+    static constexpr int cols = FC::SM ? C * (FC::SM + pad) : 0;
+    static constexpr int up16(int x) { return (x + 15) / 16 * 16; }
+    static constexpr int EX = up16((int)sizeof(cx<T>) * (rows > cols ? rows : cols));
+    static constexpr int ST = up16((int)sizeof(T) * ((G > C ? G : C) << LG));
+    static constexpr bool F32 = sizeof(T) == 4;
+    static constexpr bool SAME = LGR_R == LGR_C;
+    static constexpr int NTAB = F32 ? 2 : 1;                      // fp64 inverts with the forward table
+    static constexpr int TWR = FR::TW * NTAB;                     // entries
+    static constexpr int TWC = SAME ? 0 : FC::TW * NTAB;
+    static constexpr int TWB = up16((TWR + TWC) * (int)sizeof(twe<T>));
+    static constexpr int LIMIT = 220 * 1024;
+    static constexpr bool TS = EX + TWB <= LIMIT;
+    static constexpr bool PS = EX + (TS ? TWB : 0) + ST <= LIMIT;
+    static constexpr int OFF_ST = EX;
+    static constexpr int OFF_TW = EX + (PS ? ST : 0);
+    static constexpr int BYTES = OFF_TW + (TS ? TWB : 0);
+    static constexpr int CB = C * (int)sizeof(T);                 // bytes per m run of a column task
+    static constexpr int CH = CB >= 16 ? 16 : CB;                 // cp.async size for it
+};
+
+template <typename T>
+struct Tables {
+    const twe<T>* rf;   // row forward / inverse, column forward / inverse
+    const twe<T>* ri;
+    const twe<T>* cf;
+    const twe<T>* ci;
+};
+
+// The solve's twiddle tables: shared copies (made once per launch) or global.
+template <typename T, int LG, int LGR_R, int LGR_C>
+__device__ __forceinline__ Tables<T> load_tables(const RowArgs<T>& r, const ColArgs<T>& c, unsigned char* smraw) {
+    using L = SolveSmem<T, LG, LGR_R, LGR_C>;
+    if constexpr (!L::TS) {
+        return Tables<T>{r.twf, r.twi, c.twf, c.twi};
+    } else {
+        twe<T>* t = reinterpret_cast<twe<T>*>(smraw + L::OFF_TW);
+        constexpr int nr = L::FR::TW, nc = L::FC::TW;
+        twe<T>* rf = t;
+        twe<T>* ri = L::F32 ? t + nr : t;
+        twe<T>* cf = L::SAME ? rf : t + L::TWR;
+        twe<T>* ci = L::SAME ? ri : (L::F32 ? cf + nc : cf);
+        for (int i = threadIdx.x; i < nr; i += blockDim.x) {
+            rf[i] = r.twf[i];
+            if constexpr (L::F32) ri[i] = r.twi[i];
+        }
+        if constexpr (!L::SAME) {
+            for (int i = threadIdx.x; i < nc; i += blockDim.x) {
+                cf[i] = c.twf[i];
+                if constexpr (L::F32) ci[i] = c.twi[i];
+            }
+        }
+        __syncthreads();
+        return Tables<T>{rf, ri, cf, ci};
+    }
+}
+
+// Row phase: CTA x takes rows x*G .. x*G+G-1, then strides by the grid. The
+// field loads of a task are issued before its mask state is known, so the
+// state's L2 round trip overlaps them.
 template <typename T, int LG, int LGR_R, int LGR_C, int ALG>
-__device__ __forceinline__ void row_phase(const RowArgs<T>& a, int batch, cx<T>* smem) {
+__device__ __forceinline__ void row_phase(const RowArgs<T>& a, int batch, unsigned char* smraw,
+                                          const Tables<T>& tw) {
+    using L = SolveSmem<T, LG, LGR_R, LGR_C>;
     using F = FftShape<LG, LGR_R>;
+    cx<T>* smem = reinterpret_cast<cx<T>*>(smraw);
     const int G = blockDim.x / F::TG;
     const int g = threadIdx.x / F::TG, j = threadIdx.x % F::TG;
+    T* ps = reinterpret_cast<T*>(smraw + L::OFF_ST) + ((size_t)g << LG);
     const int total = batch << LG;
     for (int base = blockIdx.x * G; base < total; base += gridDim.x * G) {
         const int r = base + g;
-        const int b = r >> LG;
-        const bool act = r < total && mask_live(a.st + (r < total ? b : 0));
-        row_task<T, LG, LGR_R, decltype(group_sync<F::TG>(g)), ALG>(a, r < total ? b : 0, r & ((1 << LG) - 1), j,
-                                                                   smem + g * F::SM, act, group_sync<F::TG>(g));
+        const bool inb = r < total;
+        const int b = inb ? (r >> LG) : 0;
+        const bool live = inb && mask_live(a.st + b);
+        row_task<T, LG, LGR_R, decltype(group_sync<F::TG>(g)), ALG, L::TS, L::PS>(
+            a, b, r & ((1 << LG) - 1), j, smem + g * F::SM, tw.rf, tw.ri, ps, inb, live, group_sync<F::TG>(g));
     }
 }
 
 template <typename T, int LG, int LGR_R, int LGR_C>
-__device__ __forceinline__ void final_phase(const FinalArgs<T>& a, int batch, cx<T>* smem) {
+__device__ __forceinline__ void final_phase(const FinalArgs<T>& a, int batch, unsigned char* smraw,
+                                            const Tables<T>& tw) {
+    using L = SolveSmem<T, LG, LGR_R, LGR_C>;
     using F = FftShape<LG, LGR_R>;
+    cx<T>* smem = reinterpret_cast<cx<T>*>(smraw);
     const int G = blockDim.x / F::TG;
     const int g = threadIdx.x / F::TG, j = threadIdx.x % F::TG;
     const int total = batch << LG;
@@ -779,7 +928,8 @@ __device__ __forceinline__ void final_phase(const FinalArgs<T>& a, int batch, cx
         const int r = base + g;
         const int b = r < total ? (r >> LG) : 0;
         const bool act = r < total && !__ldcg(&a.st[b].done);
-        final_task<T, LG, LGR_R>(a, b, r & ((1 << LG) - 1), j, smem + g * F::SM, act, group_sync<F::TG>(g));
+        final_task<T, LG, LGR_R, L::TS>(a, b, r & ((1 << LG) - 1), j, smem + g * F::SM, tw.ri, act,
+                                        group_sync<F::TG>(g));
     }
 }
 
@@ -787,8 +937,12 @@ __device__ __forceinline__ void final_phase(const FinalArgs<T>& a, int batch, cx
 // part[b][t] so the per-mask total is combined in task order (independent of
 // which CTA ran which task, hence of batch size and grid size).
 template <typename T, int LG, int LGR_R, int LGR_C>
-__device__ __forceinline__ void col_phase(const ColArgs<T>& a, int batch, cx<T>* smem) {
+__device__ __forceinline__ void col_phase(const ColArgs<T>& a, int batch, unsigned char* smraw,
+                                          const Tables<T>& tw) {
+    using L = SolveSmem<T, LG, LGR_R, LGR_C>;
     using F = FftShape<LG, LGR_C>;
+    cx<T>* smem = reinterpret_cast<cx<T>*>(smraw);
+    T* ms = reinterpret_cast<T*>(smraw + L::OFF_ST);
     const int C = blockDim.x / F::TG;
     const int tpm = (1 << LG) / C;          // tasks per mask
     const int total = batch * tpm;
@@ -801,7 +955,7 @@ __device__ __forceinline__ void col_phase(const ColArgs<T>& a, int batch, cx<T>*
         const int b = t / tpm, tt = t - b * tpm;
         const bool act = mask_live(a.st + b);
         double acc[3];
-        col_task<T, LG, LGR_C, (1 << LG)>(a, b, tt * C, C, smem, act, acc);
+        col_task<T, LG, LGR_C, (1 << LG), L::TS, L::PS, L::CH>(a, b, tt * C, C, smem, tw.cf, tw.ci, ms, act, acc);
         if (metr && act) {
             double tot[3];
             block_reduce<3>(acc, tot);
@@ -855,44 +1009,26 @@ __device__ __forceinline__ void decide_phase_raar(const RowArgs<T>& r, int batch
     }
 }
 
-#ifndef PM_SOLVE_NT
-#define PM_SOLVE_NT 512
-#endif
-constexpr int kSolveThreads = PM_SOLVE_NT;
-
-// Dynamic shared memory of solve_kernel: the larger of the row phase
-// (512/TG_row transforms) and the column phase (512/TG_col interleaved).
-template <typename T, int LG, int LGR_R, int LGR_C>
-__host__ __device__ constexpr int solve_smem_bytes() {
-    using FR = FftShape<LG, LGR_R>;
-    using FC = FftShape<LG, LGR_C>;
-    constexpr int rows = (kSolveThreads / FR::TG > 0 ? kSolveThreads / FR::TG : 1) * FR::SM;
-    constexpr int C = kSolveThreads / FC::TG > 0 ? kSolveThreads / FC::TG : 1;
-    constexpr int pad = 128 / (int)(sizeof(cx<T>) * C) > 0 ? 128 / (int)(sizeof(cx<T>) * C) : 1;
-    constexpr int cols = FC::SM ? C * (FC::SM + pad) : 0;
-    return (int)sizeof(cx<T>) * (rows > cols ? rows : cols);
-}
-
 template <typename T, int LG, int LGR_R, int LGR_C, int ALG>
 __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(SolveArgs<T> a) {
     extern __shared__ __align__(16) unsigned char smraw[];
-    cx<T>* smem = reinterpret_cast<cx<T>*>(smraw);
     const int B = a.batch;
     int si = 0;
     unsigned epoch = 0;
     stamp(a.stamps, si);
+    const Tables<T> tw = load_tables<T, LG, LGR_R, LGR_C>(a.row, a.col, smraw);
     if (a.do_init) {
         ColArgs<T> c = a.col;
         c.mode = a.init_mode;
         c.u_iter = 0;
-        col_phase<T, LG, LGR_R, LGR_C>(c, B, smem);       // u0 column half
+        col_phase<T, LG, LGR_R, LGR_C>(c, B, smraw, tw);          // u0 column half
         grid_sync(a.bar, epoch);
         RowArgs<T> r = a.row;
         r.mode = kRowInit;
-        row_phase<T, LG, LGR_R, LGR_C, ALG>(r, B, smem);       // u0 row half, w0 (RAAR: and x_0)
+        row_phase<T, LG, LGR_R, LGR_C, ALG>(r, B, smraw, tw);     // u0 row half, w0 (RAAR: and x_0)
         grid_sync(a.bar, epoch);
         c.mode = 2;
-        col_phase<T, LG, LGR_R, LGR_C>(c, B, smem);       // z1
+        col_phase<T, LG, LGR_R, LGR_C>(c, B, smraw, tw);          // z1
         grid_sync(a.bar, epoch);
     }
     const bool early = a.col.ctl.early_tol >= 0.0;
@@ -902,50 +1038,50 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(SolveArgs<T> a)
             RowArgs<T> r = a.row;
             r.mode = kRowRaar;
             r.it = it;
-            row_phase<T, LG, LGR_R, LGR_C, ALG>(r, B, smem);   // gap of x_{it-1}, x_it, w_it
+            row_phase<T, LG, LGR_R, LGR_C, ALG>(r, B, smraw, tw);   // gap of x_{it-1}, x_it, w_it
             grid_sync(a.bar, epoch);
             decide_phase_raar<T>(r, B, it - 1);
             if (early) grid_sync(a.bar, epoch);
             ColArgs<T> c = a.col;
             c.mode = 2;
             c.u_iter = it;
-            col_phase<T, LG, LGR_R, LGR_C>(c, B, smem);   // lit/dark of x_it, z_{it+1}
+            col_phase<T, LG, LGR_R, LGR_C>(c, B, smraw, tw);        // lit/dark of x_it, z_{it+1}
             grid_sync(a.bar, epoch);
         }
         if (a.do_probe) {
             RowArgs<T> r = a.row;
             r.mode = kRowProbe;
             r.it = a.it_end;
-            row_phase<T, LG, LGR_R, LGR_C, ALG>(r, B, smem);   // gap of x_{it_end-1}
+            row_phase<T, LG, LGR_R, LGR_C, ALG>(r, B, smraw, tw);   // gap of x_{it_end-1}
             grid_sync(a.bar, epoch);
             decide_phase_raar<T>(r, B, a.it_end - 1);
             grid_sync(a.bar, epoch);
         }
         if (a.do_final) {
-            final_phase<T, LG, LGR_R, LGR_C>(a.fin, B, smem);   // pair, mask, gap of x_K
+            final_phase<T, LG, LGR_R, LGR_C>(a.fin, B, smraw, tw);   // pair, mask, gap of x_K
             grid_sync(a.bar, epoch);
             decide_phase_raar<T>(a.row, B, a.fin.ctl.max_iters);
         }
     } else {
-    for (int it = a.it_begin; it < a.it_end; ++it) {
-        RowArgs<T> r = a.row;
-        r.mode = kRowGS;
-        r.it = it;
-        row_phase<T, LG, LGR_R, LGR_C, ALG>(r, B, smem);       // u_it, w_it
-        stamp(a.stamps, si);
-        grid_sync(a.bar, epoch);
-        stamp(a.stamps, si);
-        ColArgs<T> c = a.col;
-        c.mode = 2;
-        c.u_iter = it;
-        col_phase<T, LG, LGR_R, LGR_C>(c, B, smem);       // metrics of u_it, z_{it+1}
-        stamp(a.stamps, si);
-        grid_sync(a.bar, epoch);
-        stamp(a.stamps, si);
-        decide_phase<T, LG, LGR_C>(c, B);
-        if (early) grid_sync(a.bar, epoch);                      // stop flags must be seen by every CTA
-    }
-    if (a.do_final) final_phase<T, LG, LGR_R, LGR_C>(a.fin, B, smem);
+        for (int it = a.it_begin; it < a.it_end; ++it) {
+            RowArgs<T> r = a.row;
+            r.mode = kRowGS;
+            r.it = it;
+            row_phase<T, LG, LGR_R, LGR_C, ALG>(r, B, smraw, tw);   // u_it, w_it
+            stamp(a.stamps, si);
+            grid_sync(a.bar, epoch);
+            stamp(a.stamps, si);
+            ColArgs<T> c = a.col;
+            c.mode = 2;
+            c.u_iter = it;
+            col_phase<T, LG, LGR_R, LGR_C>(c, B, smraw, tw);        // metrics of u_it, z_{it+1}
+            stamp(a.stamps, si);
+            grid_sync(a.bar, epoch);
+            stamp(a.stamps, si);
+            decide_phase<T, LG, LGR_C>(c, B);
+            if (early) grid_sync(a.bar, epoch);                        // stop flags must be seen by every CTA
+        }
+        if (a.do_final) final_phase<T, LG, LGR_R, LGR_C>(a.fin, B, smraw, tw);
     }
     stamp(a.stamps, si);
 }
