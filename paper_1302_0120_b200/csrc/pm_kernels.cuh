@@ -345,6 +345,12 @@ template <typename C> __device__ __forceinline__ double norm_sq_d(C u) {
     return (double)u.x * (double)u.x + (double)u.y * (double)u.y;
 }
 
+// Record the first iteration whose iterate went non-finite (decisions may be
+// taken only every few iterations; the reference reports the first).
+__device__ __forceinline__ void first_bad(int* bad, int it) {
+    if (__ldcg(bad) == 0) atomicCAS(bad, 0, it);
+}
+
 // Cross-CTA field loads bypass L1 (the field is rewritten between phases).
 template <typename C> __device__ __forceinline__ C ld_field(const C* p) { return __ldcg(p); }
 
@@ -432,7 +438,7 @@ __device__ __forceinline__ void row_task(const RowArgs<T>& a, int b, int row, in
             v[k] = replace_mod(v[k], inb ? p_at(k) : T(0), thr, s2);
             chk += s2;                              // non-finite detector (reference Field checks)
         }
-        if (act && !isfinite(chk)) atomicMax(&a.st[b].bad, a.it);
+        if (act && !isfinite(chk)) first_bad(&a.st[b].bad, a.it);
     } else if (a.mode == kRowInit) {
         cx<T>* xp = (ALG != 0 && a.x) ? a.x + b * N + (size_t)row * a.nx + j : nullptr;
 #pragma unroll
@@ -464,7 +470,7 @@ __device__ __forceinline__ void row_task(const RowArgs<T>& a, int b, int row, in
                 v[k] = xn;
             }
         }
-        if (upd && act && !isfinite(e2)) atomicMax(&a.st[b].bad, a.it);
+        if (upd && act && !isfinite(e2)) first_bad(&a.st[b].bad, a.it);
         row_partials<F::TG>(g2, e2, a.rpart + ((size_t)b * a.ny + row) * a.wpr * 2, j, act);
         if (!upd) {
             if constexpr (PS) sync();              // ps is restaged by the next task
@@ -574,7 +580,8 @@ __device__ __forceinline__ void col_task(const ColArgs<T>& a, int b, int col0, i
     for (int k = 0; k < F::R; ++k) v[k] = cscale(v[k], a.scale);     // u^ = F(u) = S * ColFFT(w')
 
     const bool metr = a.u_iter >= 1;
-    const bool rec = metr && ((a.u_iter - 1) % a.ctl.record_every == 0);
+    const bool rec = metr && recorded(a.ctl, a.u_iter);
+    const bool gneed = metr && !a.raar && gap_needed(a.ctl, a.u_iter);
     const T thr = T(a.thr_m[b]);
     if constexpr (PS) {
         cp_async_wait_all();
@@ -622,7 +629,7 @@ __device__ __forceinline__ void col_task(const ColArgs<T>& a, int b, int col0, i
     for (int k = 0; k < F::R; ++k) {
         const cx<T> vh = replace_mod(v[k], mm[k], thr);     // v^ = replace_m(u^)
         // G(u) = ||P_S u - P_M u|| = ||u^ - v^||  (Parseval; u is on S)
-        g2 += norm_sq(csub(v[k], vh));
+        if (gneed) g2 += norm_sq(csub(v[k], vh));
         v[k] = vh;
     }
     acc[0] = act ? (double)g2 : 0.0;
@@ -892,9 +899,18 @@ __device__ __forceinline__ Tables<T> load_tables(const RowArgs<T>& r, const ColA
     }
 }
 
-// Row phase: CTA x takes rows x*G .. x*G+G-1, then strides by the grid. The
-// field loads of a task are issued before its mask state is known, so the
-// state's L2 round trip overlaps them.
+// Contiguous share of `total` rows for this CTA: the first total % grid CTAs
+// take one row more, so no CTA does more than ceil(total / grid).
+__device__ __forceinline__ void row_share(int total, int& start, int& count) {
+    const int q = total / (int)gridDim.x, rem = total % (int)gridDim.x;
+    count = q + ((int)blockIdx.x < rem ? 1 : 0);
+    start = (int)blockIdx.x * q + min((int)blockIdx.x, rem);
+}
+
+// Row phase: each CTA runs its contiguous share of the batch's rows, G at a
+// time. The field loads of a task are issued before its mask state is known,
+// so the state's L2 round trip overlaps them. Groups of whole warps with no
+// row left skip the round (their barriers are their own).
 template <typename T, int LG, int LGR_R, int LGR_C, int ALG>
 __device__ __forceinline__ void row_phase(const RowArgs<T>& a, int batch, unsigned char* smraw,
                                           const Tables<T>& tw) {
@@ -904,11 +920,13 @@ __device__ __forceinline__ void row_phase(const RowArgs<T>& a, int batch, unsign
     const int G = blockDim.x / F::TG;
     const int g = threadIdx.x / F::TG, j = threadIdx.x % F::TG;
     T* ps = reinterpret_cast<T*>(smraw + L::OFF_ST) + ((size_t)g << LG);
-    const int total = batch << LG;
-    for (int base = blockIdx.x * G; base < total; base += gridDim.x * G) {
-        const int r = base + g;
-        const bool inb = r < total;
-        const int b = inb ? (r >> LG) : 0;
+    int start, count;
+    row_share(batch << LG, start, count);
+    for (int r0 = 0; r0 < count; r0 += G) {
+        const bool inb = r0 + g < count;
+        if (F::TG >= 32 && !inb) break;
+        const int r = start + (inb ? r0 + g : 0);
+        const int b = r >> LG;
         const bool live = inb && mask_live(a.st + b);
         row_task<T, LG, LGR_R, decltype(group_sync<F::TG>(g)), ALG, L::TS, L::PS>(
             a, b, r & ((1 << LG) - 1), j, smem + g * F::SM, tw.rf, tw.ri, ps, inb, live, group_sync<F::TG>(g));
@@ -923,11 +941,14 @@ __device__ __forceinline__ void final_phase(const FinalArgs<T>& a, int batch, un
     cx<T>* smem = reinterpret_cast<cx<T>*>(smraw);
     const int G = blockDim.x / F::TG;
     const int g = threadIdx.x / F::TG, j = threadIdx.x % F::TG;
-    const int total = batch << LG;
-    for (int base = blockIdx.x * G; base < total; base += gridDim.x * G) {
-        const int r = base + g;
-        const int b = r < total ? (r >> LG) : 0;
-        const bool act = r < total && !__ldcg(&a.st[b].done);
+    int start, count;
+    row_share(batch << LG, start, count);
+    for (int r0 = 0; r0 < count; r0 += G) {
+        const bool inb = r0 + g < count;
+        if (F::TG >= 32 && !inb) break;
+        const int r = start + (inb ? r0 + g : 0);
+        const int b = r >> LG;
+        const bool act = inb && !__ldcg(&a.st[b].done);
         final_task<T, LG, LGR_R, L::TS>(a, b, r & ((1 << LG) - 1), j, smem + g * F::SM, tw.ri, act,
                                         group_sync<F::TG>(g));
     }
@@ -949,7 +970,8 @@ __device__ __forceinline__ void col_phase(const ColArgs<T>& a, int batch, unsign
     // RAAR keeps only lit/dark (the gap comes from the row sweep), in a
     // parity-selected buffer: the decision on x_{it-1} reads it while this
     // phase of iteration it may already run
-    const bool metr = a.mode == 2 && a.u_iter >= 1 && (!a.raar || recorded(a.ctl, a.u_iter));
+    const bool metr = a.mode == 2 && a.u_iter >= 1 &&
+                      (a.raar ? recorded(a.ctl, a.u_iter) : gap_needed(a.ctl, a.u_iter));
     double* const part = a.part + ((a.raar && (a.u_iter & 1)) ? a.part_alt : 0);
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
         const int b = t / tpm, tt = t - b * tpm;
@@ -976,17 +998,21 @@ __device__ __forceinline__ void decide_phase(const ColArgs<T>& a, int batch) {
     const int tpm = (1 << LG) / C;
     const int lane = threadIdx.x & 31;
     if (threadIdx.x >= 32) return;
-    for (int b = blockIdx.x; b < batch; b += gridDim.x) {
+    const bool metr = gap_needed(a.ctl, a.u_iter);
+    // the last CTAs decide: the row share puts the fewest rows on them
+    for (int b = gridDim.x - 1 - blockIdx.x; b < batch; b += gridDim.x) {
         MaskState* st = a.st + b;
         if (!mask_live(st)) continue;
-        double tot[3];
+        double tot[3] = {0.0, 0.0, 0.0};
+        if (metr) {
 #pragma unroll
-        for (int v = 0; v < 3; ++v) {
-            double x = 0.0;
-            for (int i = lane; i < tpm; i += 32) x += __ldcg(&a.part[((size_t)b * tpm + i) * 3 + v]);
+            for (int v = 0; v < 3; ++v) {
+                double x = 0.0;
+                for (int i = lane; i < tpm; i += 32) x += __ldcg(&a.part[((size_t)b * tpm + i) * 3 + v]);
 #pragma unroll
-            for (int o = 16; o >= 1; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-            tot[v] = x;
+                for (int o = 16; o >= 1; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+                tot[v] = x;
+            }
         }
         if (lane == 0) {
             const int i = a.u_iter;
@@ -1001,7 +1027,7 @@ __device__ __forceinline__ void decide_phase(const ColArgs<T>& a, int batch) {
 template <typename T>
 __device__ __forceinline__ void decide_phase_raar(const RowArgs<T>& r, int batch, int i) {
     if (threadIdx.x >= 32 || i < 1) return;
-    for (int b = blockIdx.x; b < batch; b += gridDim.x) {
+    for (int b = gridDim.x - 1 - blockIdx.x; b < batch; b += gridDim.x) {
         MaskState* st = r.st + b;
         if (!mask_live(st)) continue;
         decide_raar_warp(st, r.hist, r.hist_stride, r.ctl, b, i, r.rpart + (size_t)b * r.ny * r.wpr * 2,
@@ -1078,7 +1104,9 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(SolveArgs<T> a)
             stamp(a.stamps, si);
             grid_sync(a.bar, epoch);
             stamp(a.stamps, si);
-            decide_phase<T, LG, LGR_C>(c, B);
+            // decisions: records, early stop, max_iters, and the last iterate
+            // of this launch (the stepping API reads state after every launch)
+            if (gap_needed(c.ctl, it) || it >= c.ctl.max_iters || it == a.it_end - 1) decide_phase<T, LG, LGR_C>(c, B);
             if (early) grid_sync(a.bar, epoch);                        // stop flags must be seen by every CTA
         }
         if (a.do_final) final_phase<T, LG, LGR_R, LGR_C>(a.fin, B, smraw, tw);
