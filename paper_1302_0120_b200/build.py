@@ -80,9 +80,10 @@ def _units(build_dir):
         tag = "f64" if f64 else "f32"
         for lg in range(MAX_LG + 1):
             row, col, nt = _config(tag, lg)
-            units.append((CSRC / "pm_inst.cu", build_dir / f"pm_inst_{tag}_{lg}_{row}{col}_{nt}.o",
+            roll = int(os.environ.get("PM_ROLL", "0"))
+            units.append((CSRC / "pm_inst.cu", build_dir / f"pm_inst_{tag}_{lg}_{row}{col}_{nt}_r{roll}.o",
                           [f"-DPM_F64={f64}", f"-DPM_LG={lg}", f"-DPM_LGR_ROW={row}", f"-DPM_LGR_COL={col}",
-                           f"-DPM_SOLVE_NT={nt}"]))
+                           f"-DPM_SOLVE_NT={nt}", f"-DPM_ROLL={roll}"]))
     units.append((CSRC / "pm_table.cu", build_dir / "pm_table.o", []))
     units.append((CSRC / "pm_capi.cu", build_dir / "pm_capi.o", []))
     return units

@@ -521,7 +521,7 @@ FinalArgs<T> final_args(pm_plan* pl) {
     a.field = (const cx<T>*)pl->field;
     a.p = (const T*)pl->s.p;
     a.p_stride = pl->s.p_stride;
-    a.twi = (const twe<T>*)pl->tw_row_i;
+    a.tw = (const twe<T>*)pl->tw_row;
     a.nx = pl->nx;
     a.ny = pl->ny;
     a.scale = (T)(1.0 / std::sqrt((double)pl->N));

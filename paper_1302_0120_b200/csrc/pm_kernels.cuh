@@ -25,6 +25,12 @@
 #pragma once
 #include "pm_fft.cuh"
 
+// PM_ROLL=1: one rolled copy of the transform per task (half the code);
+// 0 (default, measured faster on B200): both trips unrolled.
+#ifndef PM_ROLL
+#define PM_ROLL 0
+#endif
+
 namespace pm {
 
 constexpr double kTwoPi = 6.283185307179586;   // float64(2*np.pi)
@@ -109,7 +115,7 @@ struct FinalArgs {
     const cx<T>* field;
     const T* p;
     long long p_stride;
-    const twe<T>* twi;
+    const twe<T>* tw;         // forward row twiddles
     int nx, ny;
     T scale;
     const double* tol_p;      // [batch] reference zero_tol (compared to |u|)
@@ -392,19 +398,29 @@ __device__ __forceinline__ void stage_runs(T* dst, const T* src, int rows, int r
     }
 }
 
+// Conjugate storage. Between a column sweep and the next row sweep the field
+// holds conj(z'), z' = ColIFFT(v^) unnormalised; both sweeps then run only
+// FORWARD transforms, because IFFT(x) = conj(FFT(conj(x))):
+//   row:    y = RowFFT(conj z') = conj(v')   -> u = conj(P_S(y)) = P_S(v')
+//           (the conjugation folds into the projection's multiply) -> RowFFT(u)
+//   column: u^ = S ColFFT(w') -> conj(v^) = conj(replace_m(u^)) (folded again)
+//           -> ColFFT(conj v^) = conj(ColIFFT(v^)) = conj(z').
+// One transform direction means one copy of the FFT code per task (a
+// two-trip loop, not unrolled, keeps the hot loop inside the instruction
+// cache) and one twiddle table.
+
 // A row task: the TG threads of group g transform one row. `inb` == false
 // (row beyond the batch) runs the same instruction stream on zeros without
 // touching memory, so group barriers stay aligned when a CTA has fewer rows
 // than groups; `live` == false (mask already stopped) loads but stores
-// nothing. `twf` / `twi` are the row tables (shared copies when TS); `ps`,
-// when PS, is this row's slice of p staged in shared memory.
+// nothing. `tw` is the forward row table (a shared copy when TS); `ps`, when
+// PS, is this row's slice of p staged in shared memory.
 // ALG selects the code compiled in: 0 GS modes only, 1 RAAR modes only,
 // -1 both (the persistent kernel instantiates one algorithm at a time so the
 // other's registers do not count against it).
 template <typename T, int LG_L, int LG_R, class Sync, int ALG = -1, bool TS = false, bool PS = false>
 __device__ __forceinline__ void row_task(const RowArgs<T>& a, int b, int row, int j, cx<T>* sm,
-                                         const twe<T>* twf, const twe<T>* twi, T* ps, bool inb, bool live,
-                                         Sync sync) {
+                                         const twe<T>* tw, T* ps, bool inb, bool live, Sync sync) {
     using F = FftShape<LG_L, LG_R>;
     const size_t N = (size_t)a.nx * a.ny;
     const bool act = inb && live;
@@ -412,72 +428,83 @@ __device__ __forceinline__ void row_task(const RowArgs<T>& a, int b, int row, in
     const T* p = a.p + b * a.p_stride + (size_t)row * a.nx + j;
     cx<T> v[F::R];
 #pragma unroll
-    for (int k = 0; k < F::R; ++k) v[k] = inb ? ld_field(f + F::TG * k) : mk<T>(T(0), T(0));
+    for (int k = 0; k < F::R; ++k) v[k] = inb ? ld_field(f + F::TG * k) : mk<T>(T(0), T(0));   // conj(z')
     if constexpr (PS) {
         if (inb && a.mode != kRowInit) {
             stage_runs<T, 16>(ps, p - j, 1, 1 << LG_L, 0, j, F::TG);
             cp_async_commit();
         }
     }
-    fft1d<T, LG_L, LG_R, +1, TS>(v, sm, twi, j, sync);              // v' = RowIFFT(z')
-    if constexpr (PS) {
-        cp_async_wait_all();
-        sync();
-    }
     auto p_at = [&](int k) -> T {
         if constexpr (PS) return ps[j + F::TG * k];
         else return p[F::TG * k];
     };
-    if (ALG != 1 && a.mode == kRowGS) {
-        // u = P_S v = P_S v' (src/projections.py:69-74), threshold pre-scaled
-        const T thr = T(a.thr_p[b]);
-        T chk = T(0);
+    // two trips through one copy of the transform; the trip count is opaque
+    // to the compiler (a.ny >= 1 at run time) so it keeps the loop rolled
+#if PM_ROLL
+    const int trips = 1 + (a.ny > 0);
+#pragma unroll 1
+#else
+    constexpr int trips = 2;
 #pragma unroll
-        for (int k = 0; k < F::R; ++k) {
-            T s2;
-            v[k] = replace_mod(v[k], inb ? p_at(k) : T(0), thr, s2);
-            chk += s2;                              // non-finite detector (reference Field checks)
+#endif
+    for (int h = 0; h < trips; ++h) {
+        fft1d<T, LG_L, LG_R, -1, TS>(v, sm, tw, j, sync);     // h = 0: y = conj(v'); h = 1: w' = RowFFT(u)
+        if (h) break;
+        if constexpr (PS) {
+            cp_async_wait_all();
+            sync();
         }
-        if (act && !isfinite(chk)) first_bad(&a.st[b].bad, a.it);
-    } else if (a.mode == kRowInit) {
-        cx<T>* xp = (ALG != 0 && a.x) ? a.x + b * N + (size_t)row * a.nx + j : nullptr;
+        if (ALG != 1 && a.mode == kRowGS) {
+            // u = P_S v = P_S v' = conj(P_S y) (src/projections.py:69-74), threshold pre-scaled
+            const T thr = T(a.thr_p[b]);
+            T chk = T(0);
 #pragma unroll
-        for (int k = 0; k < F::R; ++k) {
-            v[k] = cscale(v[k], a.scale);                             // u0 = S * v'
-            if (xp && act) xp[F::TG * k] = v[k];                      // RAAR: x_0 = u0
-        }
-    } else if (ALG != 0) {
-        // RAAR, v = P_M x_{it-1} = S * v':
-        //   gap of x_{it-1} = ||P_S x_{it-1} - v|| (src/metrics.py:67-71), when needed;
-        //   x_it = beta x + beta P_S(2v - x) + (1 - 2 beta) v, numpy's operation order.
-        const int gi = a.it - 1;
-        const bool gneed = act && gi >= 1 && gap_needed(a.ctl, gi) && __ldcg(&a.st[b].decided) < gi;
-        const bool upd = a.mode == kRowRaar;
-        const T thr = T(a.thr_x[b]);
-        cx<T>* xp = a.x + b * N + (size_t)row * a.nx + j;
-        double g2 = 0.0, e2 = 0.0;
+            for (int k = 0; k < F::R; ++k) {
+                T s2;
+                v[k] = replace_mod<true>(v[k], inb ? p_at(k) : T(0), thr, s2);
+                chk += s2;                              // non-finite detector (reference Field checks)
+            }
+            if (act && !isfinite(chk)) first_bad(&a.st[b].bad, a.it);
+        } else if (a.mode == kRowInit) {
+            cx<T>* xp = (ALG != 0 && a.x) ? a.x + b * N + (size_t)row * a.nx + j : nullptr;
 #pragma unroll
-        for (int k = 0; k < F::R; ++k) {
-            const cx<T> vv = cscale(v[k], a.scale);
-            const cx<T> xo = inb ? ld_field(xp + F::TG * k) : mk<T>(T(0), T(0));
-            const T pk = inb ? p_at(k) : T(0);
-            if (gneed) g2 += norm_sq_d(csub_rn(replace_mod(xo, pk, thr), vv));
-            if (upd) {
-                const cx<T> py = replace_mod(csub_rn(cscale(vv, T(2)), xo), pk, thr);
-                const cx<T> xn = cadd_rn(cadd_rn(cmul_rn(xo, a.beta), cmul_rn(py, a.beta)), cmul_rn(vv, a.c1));
-                if (act) xp[F::TG * k] = xn;
-                e2 += norm_sq_d(xn);
-                v[k] = xn;
+            for (int k = 0; k < F::R; ++k) {
+                v[k] = cscale_conj(v[k], a.scale);                        // u0 = S * v'
+                if (xp && act) xp[F::TG * k] = v[k];                      // RAAR: x_0 = u0
+            }
+        } else if (ALG != 0) {
+            // RAAR, v = P_M x_{it-1} = S * v' = S * conj(y):
+            //   gap of x_{it-1} = ||P_S x_{it-1} - v|| (src/metrics.py:67-71), when needed;
+            //   x_it = beta x + beta P_S(2v - x) + (1 - 2 beta) v, numpy's operation order.
+            const int gi = a.it - 1;
+            const bool gneed = act && gi >= 1 && gap_needed(a.ctl, gi) && __ldcg(&a.st[b].decided) < gi;
+            const bool upd = a.mode == kRowRaar;
+            const T thr = T(a.thr_x[b]);
+            cx<T>* xp = a.x + b * N + (size_t)row * a.nx + j;
+            double g2 = 0.0, e2 = 0.0;
+#pragma unroll
+            for (int k = 0; k < F::R; ++k) {
+                const cx<T> vv = cscale_conj(v[k], a.scale);
+                const cx<T> xo = inb ? ld_field(xp + F::TG * k) : mk<T>(T(0), T(0));
+                const T pk = inb ? p_at(k) : T(0);
+                if (gneed) g2 += norm_sq_d(csub_rn(replace_mod(xo, pk, thr), vv));
+                if (upd) {
+                    const cx<T> py = replace_mod(csub_rn(cscale(vv, T(2)), xo), pk, thr);
+                    const cx<T> xn = cadd_rn(cadd_rn(cmul_rn(xo, a.beta), cmul_rn(py, a.beta)), cmul_rn(vv, a.c1));
+                    if (act) xp[F::TG * k] = xn;
+                    e2 += norm_sq_d(xn);
+                    v[k] = xn;
+                }
+            }
+            if (upd && act && !isfinite(e2)) first_bad(&a.st[b].bad, a.it);
+            row_partials<F::TG>(g2, e2, a.rpart + ((size_t)b * a.ny + row) * a.wpr * 2, j, act);
+            if (!upd) {
+                if constexpr (PS) sync();              // ps is restaged by the next task
+                return;
             }
         }
-        if (upd && act && !isfinite(e2)) first_bad(&a.st[b].bad, a.it);
-        row_partials<F::TG>(g2, e2, a.rpart + ((size_t)b * a.ny + row) * a.wpr * 2, j, act);
-        if (!upd) {
-            if constexpr (PS) sync();              // ps is restaged by the next task
-            return;
-        }
     }
-    fft1d<T, LG_L, LG_R, -1, TS>(v, sm, twf, j, sync);              // w' = RowFFT(u)
     if (act) {
         cx<T>* o = a.out + (f - a.field);
 #pragma unroll
@@ -485,12 +512,12 @@ __device__ __forceinline__ void row_task(const RowArgs<T>& a, int b, int row, in
     }
 }
 
-// Best-approximation pair for one row: v* = P_M u_K = S * RowIFFT(z'),
-// u* = P_S v*, mask = phases_of(u*, zero_tol_p)
+// Best-approximation pair for one row: v* = P_M u_K = S * RowIFFT(z')
+// = S * conj(RowFFT(conj z')), u* = P_S v*, mask = phases_of(u*, zero_tol_p)
 // (src/solver.py:201-206, src/grid.py:168-176).
 template <typename T, int LG_L, int LG_R, bool TS = false, class Sync>
 __device__ __forceinline__ void final_task(const FinalArgs<T>& a, int b, int row, int j, cx<T>* sm,
-                                           const twe<T>* twi, bool act, Sync sync) {
+                                           const twe<T>* tw, bool act, Sync sync) {
     using F = FftShape<LG_L, LG_R>;
     const size_t N = (size_t)a.nx * a.ny;
     const size_t o = b * N + (size_t)row * a.nx + j;
@@ -498,7 +525,9 @@ __device__ __forceinline__ void final_task(const FinalArgs<T>& a, int b, int row
     cx<T> v[F::R];
 #pragma unroll
     for (int k = 0; k < F::R; ++k) v[k] = act ? ld_field(a.field + o + F::TG * k) : mk<T>(T(0), T(0));
-    fft1d<T, LG_L, LG_R, +1, TS>(v, sm, twi, j, sync);
+    fft1d<T, LG_L, LG_R, -1, TS>(v, sm, tw, j, sync);
+#pragma unroll
+    for (int k = 0; k < F::R; ++k) v[k] = cscale_conj(v[k], a.scale);     // v*
     if (a.x) {
         // RAAR: gap of the last iterate, ||P_S x_K - P_M x_K|| with P_M x_K = v*
         const int i = a.ctl.max_iters;
@@ -508,8 +537,7 @@ __device__ __forceinline__ void final_task(const FinalArgs<T>& a, int b, int row
             const T thr = T(a.thr_x[b]);
 #pragma unroll
             for (int k = 0; k < F::R; ++k)
-                g2 += norm_sq_d(csub_rn(replace_mod(ld_field(a.x + o + F::TG * k), p[F::TG * k], thr),
-                                        cscale(v[k], a.scale)));
+                g2 += norm_sq_d(csub_rn(replace_mod(ld_field(a.x + o + F::TG * k), p[F::TG * k], thr), v[k]));
         }
         row_partials<F::TG>(g2, 0.0, a.rpart + ((size_t)b * a.ny + row) * a.wpr * 2, j, gneed);
     }
@@ -518,7 +546,7 @@ __device__ __forceinline__ void final_task(const FinalArgs<T>& a, int b, int row
 #pragma unroll
     for (int k = 0; k < F::R; ++k) {
         const size_t x = o + F::TG * k;
-        const cx<T> vs = cscale(v[k], a.scale);
+        const cx<T> vs = v[k];
         if (a.v_star) a.v_star[x] = vs;
         const cx<T> us = replace_mod_exact<T>(vs, p[F::TG * k], tol);
         if (a.u_star) a.u_star[x] = us;
@@ -535,12 +563,11 @@ __device__ __forceinline__ void final_task(const FinalArgs<T>& a, int b, int row
 // A column task: C interleaved transforms (thread c + C*j) over columns
 // col0..col0+C-1 of mask b. NX > 0 fixes n_x at compile time (square
 // persistent path) so every column access is base + immediate offset.
-// `twf` / `twi` are the column tables (shared copies when TS); `ms`, when
-// PS, receives this task's [n_y][C] slice of m through cp.async.
+// `tw` is the forward column table (a shared copy when TS); `ms`, when PS,
+// receives this task's [n_y][C] slice of m through cp.async.
 template <typename T, int LG_L, int LG_R, int NX, bool TS = false, bool PS = false, int CH = 16>
 __device__ __forceinline__ void col_task(const ColArgs<T>& a, int b, int col0, int C, cx<T>* smbase,
-                                         const twe<T>* twf, const twe<T>* twi, T* ms, bool live,
-                                         double (&acc)[3]) {
+                                         const twe<T>* tw, T* ms, bool live, double (&acc)[3]) {
     using F = FftShape<LG_L, LG_R>;
     const int c = threadIdx.x % C, j = threadIdx.x / C;
     const size_t nx = NX > 0 ? (size_t)NX : (size_t)a.nx;
@@ -554,17 +581,21 @@ __device__ __forceinline__ void col_task(const ColArgs<T>& a, int b, int col0, i
 
     cx<T> v[F::R];
     if (a.mode == 0) {
+        // u0 = F^-1(m e^{i0}) (src/solver.py:93-108): m is real, so the stored
+        // conj(ColIFFT(m)) is ColFFT(m); the row phase finishes u0
 #pragma unroll
         for (int k = 0; k < F::R; ++k) v[k] = mk<T>(m[k * rs], T(0));
     } else {
         const cx<T>* src = (a.mode == 2 ? a.in : a.field) + (f - a.field);
 #pragma unroll
         for (int k = 0; k < F::R; ++k) v[k] = ld_field(src + k * rs);
+        if (a.mode == 1) {
+#pragma unroll
+            for (int k = 0; k < F::R; ++k) v[k] = cconj(v[k]);          // complex start: conj in, conj(IFFT) out
+        }
     }
     if (a.mode < 2) {
-        // initial iterate u0 = F^-1(m e^{i0}): unnormalised column half
-        // (src/solver.py:93-108); the row phase applies S
-        fft1d<T, LG_L, LG_R, +1, TS>(v, sm, twi, j, SyncBlock{});
+        fft1d<T, LG_L, LG_R, -1, TS>(v, sm, tw, j, SyncBlock{});
         if (act) {
 #pragma unroll
             for (int k = 0; k < F::R; ++k) f[k * rs] = v[k];
@@ -575,65 +606,73 @@ __device__ __forceinline__ void col_task(const ColArgs<T>& a, int b, int col0, i
         stage_runs<T, CH>(ms, a.m + b * a.m_stride + col0, a.ny, C, nx, threadIdx.x, blockDim.x);
         cp_async_commit();
     }
-    fft1d<T, LG_L, LG_R, -1, TS>(v, sm, twf, j, SyncBlock{});
-#pragma unroll
-    for (int k = 0; k < F::R; ++k) v[k] = cscale(v[k], a.scale);     // u^ = F(u) = S * ColFFT(w')
-
     const bool metr = a.u_iter >= 1;
     const bool rec = metr && recorded(a.ctl, a.u_iter);
     const bool gneed = metr && !a.raar && gap_needed(a.ctl, a.u_iter);
     const T thr = T(a.thr_m[b]);
-    if constexpr (PS) {
-        cp_async_wait_all();
-        __syncthreads();
-    }
-    T mm[F::R];
+#if PM_ROLL
+    const int trips = 1 + (a.ny > 0);         // 2, opaque: one rolled copy of the transform
+#pragma unroll 1
+#else
+    constexpr int trips = 2;
 #pragma unroll
-    for (int k = 0; k < F::R; ++k) {
-        if constexpr (PS) mm[k] = ms[(j + F::TG * k) * C + c];
-        else mm[k] = m[k * rs];
-    }
-    if (rec && act) {
-        // reconstructed intensity and physical error (src/metrics.py:74-112);
-        // the energy scale is sum m^2 / sum |u|^2 (Parseval: sum |F u|^2 = sum |u|^2).
-        // GS: u is on S, so sum |u|^2 = sum p^2 (precomputed). RAAR: sum |x|^2
-        // from the row sweep's partials, in a fixed order.
-        double sc;
-        if (a.raar) {
-            __shared__ double s_sc;
-            if (threadIdx.x < 32) {
-                const double e = warp_sum_strided(a.xpart + (size_t)b * a.xparts * 2 + 1, a.xparts, 2);
-                if (threadIdx.x == 0) s_sc = a.energy[b] / e;
-            }
+#endif
+    for (int h = 0; h < trips; ++h) {
+        fft1d<T, LG_L, LG_R, -1, TS>(v, sm, tw, j, SyncBlock{});   // h = 0: ColFFT(w'); h = 1: conj(z')
+        if (h) break;
+#pragma unroll
+        for (int k = 0; k < F::R; ++k) v[k] = cscale(v[k], a.scale);     // u^ = F(u) = S * ColFFT(w')
+        if constexpr (PS) {
+            cp_async_wait_all();
             __syncthreads();
-            sc = s_sc;
-            __syncthreads();
-        } else {
-            sc = a.escale[b];
         }
+        T mm[F::R];
 #pragma unroll
         for (int k = 0; k < F::R; ++k) {
-            const double inten = (double)norm_sq(v[k]) * sc;
-            const double m2 = (double)mm[k] * (double)mm[k];
-            if (m2 > 0.0) {
-                const double dev = fabs(m2 - inten);
-                if (dev > a.ctl.t_lit * m2 && dev / m2 > a.ctl.t_lit)
-                    acc[1] += a.ctl.t_dark * dev / (a.ctl.t_lit * m2) - a.ctl.t_dark;
-            } else if (inten > a.ctl.t_dark) {
-                acc[2] += inten - a.ctl.t_dark;
+            if constexpr (PS) mm[k] = ms[(j + F::TG * k) * C + c];
+            else mm[k] = m[k * rs];
+        }
+        if (rec && act) {
+            // reconstructed intensity and physical error (src/metrics.py:74-112);
+            // the energy scale is sum m^2 / sum |u|^2 (Parseval: sum |F u|^2 = sum |u|^2).
+            // GS: u is on S, so sum |u|^2 = sum p^2 (precomputed). RAAR: sum |x|^2
+            // from the row sweep's partials, in a fixed order.
+            double sc;
+            if (a.raar) {
+                __shared__ double s_sc;
+                if (threadIdx.x < 32) {
+                    const double e = warp_sum_strided(a.xpart + (size_t)b * a.xparts * 2 + 1, a.xparts, 2);
+                    if (threadIdx.x == 0) s_sc = a.energy[b] / e;
+                }
+                __syncthreads();
+                sc = s_sc;
+                __syncthreads();
+            } else {
+                sc = a.escale[b];
+            }
+#pragma unroll
+            for (int k = 0; k < F::R; ++k) {
+                const double inten = (double)norm_sq(v[k]) * sc;
+                const double m2 = (double)mm[k] * (double)mm[k];
+                if (m2 > 0.0) {
+                    const double dev = fabs(m2 - inten);
+                    if (dev > a.ctl.t_lit * m2 && dev / m2 > a.ctl.t_lit)
+                        acc[1] += a.ctl.t_dark * dev / (a.ctl.t_lit * m2) - a.ctl.t_dark;
+                } else if (inten > a.ctl.t_dark) {
+                    acc[2] += inten - a.ctl.t_dark;
+                }
             }
         }
-    }
-    T g2 = T(0);
+        T g2 = T(0);
 #pragma unroll
-    for (int k = 0; k < F::R; ++k) {
-        const cx<T> vh = replace_mod(v[k], mm[k], thr);     // v^ = replace_m(u^)
-        // G(u) = ||P_S u - P_M u|| = ||u^ - v^||  (Parseval; u is on S)
-        if (gneed) g2 += norm_sq(csub(v[k], vh));
-        v[k] = vh;
+        for (int k = 0; k < F::R; ++k) {
+            const cx<T> vh = replace_mod<true>(v[k], mm[k], thr);     // conj(v^), v^ = replace_m(u^)
+            // G(u) = ||P_S u - P_M u|| = ||u^ - v^||  (Parseval; u is on S)
+            if (gneed) g2 += norm_sq(csub(v[k], cconj(vh)));
+            v[k] = vh;
+        }
+        acc[0] = act ? (double)g2 : 0.0;
     }
-    acc[0] = act ? (double)g2 : 0.0;
-    fft1d<T, LG_L, LG_R, +1, TS>(v, sm, twi, j, SyncBlock{});         // z' = ColIFFT(v^)
     if (act) {
 #pragma unroll
         for (int k = 0; k < F::R; ++k) f[k * rs] = v[k];
@@ -695,7 +734,7 @@ __global__ void __launch_bounds__(256) row_iter_kernel(RowArgs<T> a) {
     const int G = blockDim.x / F::TG;
     const int g = threadIdx.x / F::TG, j = threadIdx.x % F::TG;
     row_task<T, LG_L, LG_R>(a, b, blockIdx.x * G + g, j, reinterpret_cast<cx<T>*>(smraw) + g * F::SM, a.twf,
-                            a.twi, nullptr, true, true, group_sync<F::TG>(g));
+                            nullptr, true, true, group_sync<F::TG>(g));
     if (dec && cta_ticket(a.ctr + b, a.nblk) && threadIdx.x < 32)
         decide_raar_warp(st, a.hist, a.hist_stride, a.ctl, b, gi, a.rpart + (size_t)b * a.ny * a.wpr * 2,
                          a.ny * a.wpr, nullptr, 0);
@@ -713,7 +752,7 @@ __global__ void __launch_bounds__(256) row_final_kernel(FinalArgs<T> a, double* 
     const bool dec = a.x && !st->stop && st->decided < K;
     const int G = blockDim.x / F::TG;
     const int g = threadIdx.x / F::TG, j = threadIdx.x % F::TG;
-    final_task<T, LG_L, LG_R>(a, b, blockIdx.x * G + g, j, reinterpret_cast<cx<T>*>(smraw) + g * F::SM, a.twi,
+    final_task<T, LG_L, LG_R>(a, b, blockIdx.x * G + g, j, reinterpret_cast<cx<T>*>(smraw) + g * F::SM, a.tw,
                               true, group_sync<F::TG>(g));
     if (dec && cta_ticket(ctr + b, nblk) && threadIdx.x < 32)
         decide_raar_warp(st, hist, hist_stride, a.ctl, b, K, a.rpart + (size_t)b * a.ny * a.wpr * 2,
@@ -736,8 +775,8 @@ __global__ void __launch_bounds__(col_max_threads<LG_L, LG_R>()) col_iter_kernel
     if (st->stop | st->done) return;
     const int C = blockDim.x / F::TG;
     double acc[3];
-    col_task<T, LG_L, LG_R, 0>(a, b, blockIdx.x * C, C, reinterpret_cast<cx<T>*>(smraw), a.twf, a.twi, nullptr,
-                               true, acc);
+    col_task<T, LG_L, LG_R, 0>(a, b, blockIdx.x * C, C, reinterpret_cast<cx<T>*>(smraw), a.twf, nullptr, true,
+                               acc);
     if (a.mode < 2 || a.u_iter < 1) return;
     double tot[3];
     if (a.raar) {
@@ -849,7 +888,7 @@ struct SolveSmem {
     static constexpr int ST = up16((int)sizeof(T) * ((G > C ? G : C) << LG));
     static constexpr bool F32 = sizeof(T) == 4;
     static constexpr bool SAME = LGR_R == LGR_C;
-    static constexpr int NTAB = F32 ? 2 : 1;                      // fp64 inverts with the forward table
+    static constexpr int NTAB = 1;                                // forward transforms only (conjugate storage)
     static constexpr int TWR = FR::TW * NTAB;                     // entries
     static constexpr int TWC = SAME ? 0 : FC::TW * NTAB;
     static constexpr int TWB = up16((TWR + TWC) * (int)sizeof(twe<T>));
@@ -865,10 +904,8 @@ struct SolveSmem {
 
 template <typename T>
 struct Tables {
-    const twe<T>* rf;   // row forward / inverse, column forward / inverse
-    const twe<T>* ri;
+    const twe<T>* rf;   // forward row / column tables
     const twe<T>* cf;
-    const twe<T>* ci;
 };
 
 // The solve's twiddle tables: shared copies (made once per launch) or global.
@@ -876,26 +913,18 @@ template <typename T, int LG, int LGR_R, int LGR_C>
 __device__ __forceinline__ Tables<T> load_tables(const RowArgs<T>& r, const ColArgs<T>& c, unsigned char* smraw) {
     using L = SolveSmem<T, LG, LGR_R, LGR_C>;
     if constexpr (!L::TS) {
-        return Tables<T>{r.twf, r.twi, c.twf, c.twi};
+        return Tables<T>{r.twf, c.twf};
     } else {
         twe<T>* t = reinterpret_cast<twe<T>*>(smraw + L::OFF_TW);
         constexpr int nr = L::FR::TW, nc = L::FC::TW;
         twe<T>* rf = t;
-        twe<T>* ri = L::F32 ? t + nr : t;
         twe<T>* cf = L::SAME ? rf : t + L::TWR;
-        twe<T>* ci = L::SAME ? ri : (L::F32 ? cf + nc : cf);
-        for (int i = threadIdx.x; i < nr; i += blockDim.x) {
-            rf[i] = r.twf[i];
-            if constexpr (L::F32) ri[i] = r.twi[i];
-        }
+        for (int i = threadIdx.x; i < nr; i += blockDim.x) rf[i] = r.twf[i];
         if constexpr (!L::SAME) {
-            for (int i = threadIdx.x; i < nc; i += blockDim.x) {
-                cf[i] = c.twf[i];
-                if constexpr (L::F32) ci[i] = c.twi[i];
-            }
+            for (int i = threadIdx.x; i < nc; i += blockDim.x) cf[i] = c.twf[i];
         }
         __syncthreads();
-        return Tables<T>{rf, ri, cf, ci};
+        return Tables<T>{rf, cf};
     }
 }
 
@@ -929,7 +958,7 @@ __device__ __forceinline__ void row_phase(const RowArgs<T>& a, int batch, unsign
         const int b = r >> LG;
         const bool live = inb && mask_live(a.st + b);
         row_task<T, LG, LGR_R, decltype(group_sync<F::TG>(g)), ALG, L::TS, L::PS>(
-            a, b, r & ((1 << LG) - 1), j, smem + g * F::SM, tw.rf, tw.ri, ps, inb, live, group_sync<F::TG>(g));
+            a, b, r & ((1 << LG) - 1), j, smem + g * F::SM, tw.rf, ps, inb, live, group_sync<F::TG>(g));
     }
 }
 
@@ -949,7 +978,7 @@ __device__ __forceinline__ void final_phase(const FinalArgs<T>& a, int batch, un
         const int r = start + (inb ? r0 + g : 0);
         const int b = r >> LG;
         const bool act = inb && !__ldcg(&a.st[b].done);
-        final_task<T, LG, LGR_R, L::TS>(a, b, r & ((1 << LG) - 1), j, smem + g * F::SM, tw.ri, act,
+        final_task<T, LG, LGR_R, L::TS>(a, b, r & ((1 << LG) - 1), j, smem + g * F::SM, tw.rf, act,
                                         group_sync<F::TG>(g));
     }
 }
@@ -977,7 +1006,7 @@ __device__ __forceinline__ void col_phase(const ColArgs<T>& a, int batch, unsign
         const int b = t / tpm, tt = t - b * tpm;
         const bool act = mask_live(a.st + b);
         double acc[3];
-        col_task<T, LG, LGR_C, (1 << LG), L::TS, L::PS, L::CH>(a, b, tt * C, C, smem, tw.cf, tw.ci, ms, act, acc);
+        col_task<T, LG, LGR_C, (1 << LG), L::TS, L::PS, L::CH>(a, b, tt * C, C, smem, tw.cf, ms, act, acc);
         if (metr && act) {
             double tot[3];
             block_reduce<3>(acc, tot);
