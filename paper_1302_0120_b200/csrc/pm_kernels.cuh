@@ -420,9 +420,11 @@ __device__ __forceinline__ void stage_runs(T* dst, const T* src, int rows, int r
 // other's registers do not count against it).
 template <typename T, int LG_L, int LG_R, class Sync, int ALG = -1, bool TS = false, bool PS = false>
 __device__ __forceinline__ void row_task(const RowArgs<T>& a, int b, int row, int j, cx<T>* sm,
-                                         const twe<T>* tw, T* ps, bool inb, bool live, Sync sync) {
+                                         const twe<T>* tw, T* ps, bool inb_arg, bool live, Sync sync) {
     using F = FftShape<LG_L, LG_R>;
     const size_t N = (size_t)a.nx * a.ny;
+    // whole-warp groups never run out of bounds (the row phase skips them)
+    const bool inb = F::TG >= 32 ? true : inb_arg;
     const bool act = inb && live;
     cx<T>* f = a.field + b * N + (size_t)row * a.nx + j;
     const T* p = a.p + b * a.p_stride + (size_t)row * a.nx + j;
