@@ -81,9 +81,10 @@ def _units(build_dir):
         for lg in range(MAX_LG + 1):
             row, col, nt = _config(tag, lg)
             roll = int(os.environ.get("PM_ROLL", "0"))
-            units.append((CSRC / "pm_inst.cu", build_dir / f"pm_inst_{tag}_{lg}_{row}{col}_{nt}_r{roll}.o",
+            pf = int(os.environ.get("PM_PF", "0"))
+            units.append((CSRC / "pm_inst.cu", build_dir / f"pm_inst_{tag}_{lg}_{row}{col}_{nt}_r{roll}_p{pf}.o",
                           [f"-DPM_F64={f64}", f"-DPM_LG={lg}", f"-DPM_LGR_ROW={row}", f"-DPM_LGR_COL={col}",
-                           f"-DPM_SOLVE_NT={nt}", f"-DPM_ROLL={roll}"]))
+                           f"-DPM_SOLVE_NT={nt}", f"-DPM_ROLL={roll}", f"-DPM_PF={pf}"]))
     units.append((CSRC / "pm_table.cu", build_dir / "pm_table.o", []))
     units.append((CSRC / "pm_capi.cu", build_dir / "pm_capi.o", []))
     return units

@@ -383,6 +383,15 @@ __device__ __forceinline__ void cp_async(void* dst, const void* src) {
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+// Wait until at most N of this thread's most recent groups are pending
+// (groups complete in commit order).
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// No prefetch: the sweep kernels and single-task phases.
+struct NoPrefetch {
+    __device__ __forceinline__ void operator()() const {}
+};
 
 // Copy `rows` runs of `run` contiguous elements (global stride `gstride`)
 // into a dense [rows][run] shared array, with `nthr` threads (thread `t`),
@@ -409,6 +418,22 @@ __device__ __forceinline__ void stage_runs(T* dst, const T* src, int rows, int r
 // two-trip loop, not unrolled, keeps the hot loop inside the instruction
 // cache) and one twiddle table.
 
+// stage_runs with every extent known at compile time (power-of-two copies per
+// run): no division, a fixed trip count per thread.
+template <typename E, int ROWS, int RUN, int NTHR>
+__device__ __forceinline__ void stage_tile(E* dst, const E* src, size_t gstride, int t) {
+    constexpr int CH = RUN * (int)sizeof(E) >= 16 ? 16 : RUN * (int)sizeof(E);
+    constexpr int EPC = CH / (int)sizeof(E);
+    constexpr int CPR = RUN / EPC;
+    constexpr int TOT = ROWS * CPR;
+    static_assert(CPR * EPC == RUN && (CPR & (CPR - 1)) == 0, "runs must split into power-of-two copies");
+#pragma unroll 4
+    for (int i = t; i < TOT; i += NTHR) {
+        const int r = i / CPR, q = i % CPR;
+        cp_async<CH>(dst + (size_t)r * RUN + q * EPC, src + r * gstride + q * EPC);
+    }
+}
+
 // A row task: the TG threads of group g transform one row. `inb` == false
 // (row beyond the batch) runs the same instruction stream on zeros without
 // touching memory, so group barriers stay aligned when a CTA has fewer rows
@@ -418,9 +443,17 @@ __device__ __forceinline__ void stage_runs(T* dst, const T* src, int rows, int r
 // ALG selects the code compiled in: 0 GS modes only, 1 RAAR modes only,
 // -1 both (the persistent kernel instantiates one algorithm at a time so the
 // other's registers do not count against it).
-template <typename T, int LG_L, int LG_R, class Sync, int ALG = -1, bool TS = false, bool PS = false>
+//
+// Cross-task prefetch (persistent kernel, PF): when `tile` is non-null the
+// row's input was copied into shared memory by the previous task through
+// cp.async; `prefetch()` starts the copy of the next task's input. cp.async
+// groups per task, in commit order: [p of this task] [next task's field],
+// so the projection waits for one group and leaves the prefetch in flight.
+template <typename T, int LG_L, int LG_R, class Sync, int ALG = -1, bool TS = false, bool PS = false,
+          class Prefetch = NoPrefetch>
 __device__ __forceinline__ void row_task(const RowArgs<T>& a, int b, int row, int j, cx<T>* sm,
-                                         const twe<T>* tw, T* ps, bool inb_arg, bool live, Sync sync) {
+                                         const twe<T>* tw, T* ps, bool inb_arg, bool live, Sync sync,
+                                         const cx<T>* tile = nullptr, Prefetch prefetch = Prefetch{}) {
     using F = FftShape<LG_L, LG_R>;
     const size_t N = (size_t)a.nx * a.ny;
     // whole-warp groups never run out of bounds (the row phase skips them)
@@ -429,14 +462,22 @@ __device__ __forceinline__ void row_task(const RowArgs<T>& a, int b, int row, in
     cx<T>* f = a.field + b * N + (size_t)row * a.nx + j;
     const T* p = a.p + b * a.p_stride + (size_t)row * a.nx + j;
     cx<T> v[F::R];
+    if (tile) {
+        cp_async_wait<0>();
+        sync();
 #pragma unroll
-    for (int k = 0; k < F::R; ++k) v[k] = inb ? ld_field(f + F::TG * k) : mk<T>(T(0), T(0));   // conj(z')
-    if constexpr (PS) {
-        if (inb && a.mode != kRowInit) {
-            stage_runs<T, 16>(ps, p - j, 1, 1 << LG_L, 0, j, F::TG);
-            cp_async_commit();
-        }
+        for (int k = 0; k < F::R; ++k) v[k] = tile[j + F::TG * k];                           // conj(z')
+        sync();                                                                               // tile free
+    } else {
+#pragma unroll
+        for (int k = 0; k < F::R; ++k) v[k] = inb ? ld_field(f + F::TG * k) : mk<T>(T(0), T(0));   // conj(z')
     }
+    if constexpr (PS) {
+        if (inb && a.mode != kRowInit) stage_runs<T, 16>(ps, p - j, 1, 1 << LG_L, 0, j, F::TG);
+        cp_async_commit();
+    }
+    prefetch();
+    cp_async_commit();
     auto p_at = [&](int k) -> T {
         if constexpr (PS) return ps[j + F::TG * k];
         else return p[F::TG * k];
@@ -454,7 +495,7 @@ __device__ __forceinline__ void row_task(const RowArgs<T>& a, int b, int row, in
         fft1d<T, LG_L, LG_R, -1, TS>(v, sm, tw, j, sync);     // h = 0: y = conj(v'); h = 1: w' = RowFFT(u)
         if (h) break;
         if constexpr (PS) {
-            cp_async_wait_all();
+            cp_async_wait<1>();                      // p of this task (the prefetch may stay in flight)
             sync();
         }
         if (ALG != 1 && a.mode == kRowGS) {
@@ -567,9 +608,13 @@ __device__ __forceinline__ void final_task(const FinalArgs<T>& a, int b, int row
 // persistent path) so every column access is base + immediate offset.
 // `tw` is the forward column table (a shared copy when TS); `ms`, when PS,
 // receives this task's [n_y][C] slice of m through cp.async.
-template <typename T, int LG_L, int LG_R, int NX, bool TS = false, bool PS = false, int CH = 16>
+// `tile` / `prefetch()`: cross-task prefetch as in row_task (the tile holds
+// this task's [n_y][C] input, written by the previous task's cp.async).
+template <typename T, int LG_L, int LG_R, int NX, bool TS = false, bool PS = false, int CH = 16,
+          class Prefetch = NoPrefetch>
 __device__ __forceinline__ void col_task(const ColArgs<T>& a, int b, int col0, int C, cx<T>* smbase,
-                                         const twe<T>* tw, T* ms, bool live, double (&acc)[3]) {
+                                         const twe<T>* tw, T* ms, bool live, double (&acc)[3],
+                                         const cx<T>* tile = nullptr, Prefetch prefetch = Prefetch{}) {
     using F = FftShape<LG_L, LG_R>;
     const int c = threadIdx.x % C, j = threadIdx.x / C;
     const size_t nx = NX > 0 ? (size_t)NX : (size_t)a.nx;
@@ -587,6 +632,12 @@ __device__ __forceinline__ void col_task(const ColArgs<T>& a, int b, int col0, i
         // conj(ColIFFT(m)) is ColFFT(m); the row phase finishes u0
 #pragma unroll
         for (int k = 0; k < F::R; ++k) v[k] = mk<T>(m[k * rs], T(0));
+    } else if (tile) {
+        cp_async_wait<0>();
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < F::R; ++k) v[k] = tile[(j + F::TG * k) * C + c];
+        __syncthreads();                                                         // tile free
     } else {
         const cx<T>* src = (a.mode == 2 ? a.in : a.field) + (f - a.field);
 #pragma unroll
@@ -608,6 +659,8 @@ __device__ __forceinline__ void col_task(const ColArgs<T>& a, int b, int col0, i
         stage_runs<T, CH>(ms, a.m + b * a.m_stride + col0, a.ny, C, nx, threadIdx.x, blockDim.x);
         cp_async_commit();
     }
+    prefetch();
+    cp_async_commit();
     const bool metr = a.u_iter >= 1;
     const bool rec = metr && recorded(a.ctl, a.u_iter);
     const bool gneed = metr && !a.raar && gap_needed(a.ctl, a.u_iter);
@@ -625,7 +678,7 @@ __device__ __forceinline__ void col_task(const ColArgs<T>& a, int b, int col0, i
 #pragma unroll
         for (int k = 0; k < F::R; ++k) v[k] = cscale(v[k], a.scale);     // u^ = F(u) = S * ColFFT(w')
         if constexpr (PS) {
-            cp_async_wait_all();
+            cp_async_wait<1>();                      // m of this task (the prefetch may stay in flight)
             __syncthreads();
         }
         T mm[F::R];
@@ -894,11 +947,23 @@ struct SolveSmem {
     static constexpr int TWR = FR::TW * NTAB;                     // entries
     static constexpr int TWC = SAME ? 0 : FC::TW * NTAB;
     static constexpr int TWB = up16((TWR + TWC) * (int)sizeof(twe<T>));
-    static constexpr int LIMIT = 220 * 1024;
-    static constexpr bool TS = EX + TWB <= LIMIT;
-    static constexpr bool PS = EX + (TS ? TWB : 0) + ST <= LIMIT;
+    static constexpr int TILE = up16((int)sizeof(cx<T>) * ((G > C ? G : C) << LG));   // one task's input
+    static constexpr int LIMIT = 225 * 1024;
+    // Cross-task prefetch (PM_PF=1) needs the staging, a tile and (measured:
+    // without them the twiddle loads are hoisted into spills) the shared
+    // twiddles. It is off by default: on B200 the sweeps are issue-bound, not
+    // load-latency-bound, once p/m and twiddles are in shared memory (batch-32
+    // 1024^2 +2%, 2048^2 -9%; scripts/sweep_perf.py). Without it: twiddles
+    // first (they are on every pass), then staging.
+#ifndef PM_PF
+#define PM_PF 0
+#endif
+    static constexpr bool PF = PM_PF && EX + ST + TILE + TWB <= LIMIT;
+    static constexpr bool TS = PF ? (EX + ST + TILE + TWB <= LIMIT) : (EX + TWB <= LIMIT);
+    static constexpr bool PS = PF || (EX + (TS ? TWB : 0) + ST <= LIMIT);
     static constexpr int OFF_ST = EX;
-    static constexpr int OFF_TW = EX + (PS ? ST : 0);
+    static constexpr int OFF_TILE = EX + (PS ? ST : 0);
+    static constexpr int OFF_TW = OFF_TILE + (PF ? TILE : 0);
     static constexpr int BYTES = OFF_TW + (TS ? TWB : 0);
     static constexpr int CB = C * (int)sizeof(T);                 // bytes per m run of a column task
     static constexpr int CH = CB >= 16 ? 16 : CB;                 // cp.async size for it
@@ -951,16 +1016,27 @@ __device__ __forceinline__ void row_phase(const RowArgs<T>& a, int batch, unsign
     const int G = blockDim.x / F::TG;
     const int g = threadIdx.x / F::TG, j = threadIdx.x % F::TG;
     T* ps = reinterpret_cast<T*>(smraw + L::OFF_ST) + ((size_t)g << LG);
+    cx<T>* tile = reinterpret_cast<cx<T>*>(smraw + L::OFF_TILE) + ((size_t)g << LG);
+    constexpr int NX = 1 << LG;
     int start, count;
     row_share(batch << LG, start, count);
+    // prefetch the next round's row while this one computes (whole-warp
+    // groups, more than one round in this CTA's share)
+    const bool pf = L::PF && F::TG >= 32 && count > G;
     for (int r0 = 0; r0 < count; r0 += G) {
         const bool inb = r0 + g < count;
         if (F::TG >= 32 && !inb) break;
         const int r = start + (inb ? r0 + g : 0);
         const int b = r >> LG;
         const bool live = inb && mask_live(a.st + b);
+        const int rn = r0 + G + g;                 // this group's next row in the share
+        auto prefetch = [&]() {
+            if (pf && rn < count)
+                stage_tile<cx<T>, 1, NX, F::TG>(tile, a.field + (size_t)(start + rn) * NX, 0, j);
+        };
         row_task<T, LG, LGR_R, decltype(group_sync<F::TG>(g)), ALG, L::TS, L::PS>(
-            a, b, r & ((1 << LG) - 1), j, smem + g * F::SM, tw.rf, ps, inb, live, group_sync<F::TG>(g));
+            a, b, r & (NX - 1), j, smem + g * F::SM, tw.rf, ps, inb, live, group_sync<F::TG>(g),
+            (pf && r0 > 0) ? tile : nullptr, prefetch);
     }
 }
 
@@ -995,8 +1071,10 @@ __device__ __forceinline__ void col_phase(const ColArgs<T>& a, int batch, unsign
     using F = FftShape<LG, LGR_C>;
     cx<T>* smem = reinterpret_cast<cx<T>*>(smraw);
     T* ms = reinterpret_cast<T*>(smraw + L::OFF_ST);
+    cx<T>* tile = reinterpret_cast<cx<T>*>(smraw + L::OFF_TILE);
+    constexpr int NX = 1 << LG;
     const int C = blockDim.x / F::TG;
-    const int tpm = (1 << LG) / C;          // tasks per mask
+    const int tpm = NX / C;                 // tasks per mask
     const int total = batch * tpm;
     // RAAR keeps only lit/dark (the gap comes from the row sweep), in a
     // parity-selected buffer: the decision on x_{it-1} reads it while this
@@ -1004,11 +1082,22 @@ __device__ __forceinline__ void col_phase(const ColArgs<T>& a, int batch, unsign
     const bool metr = a.mode == 2 && a.u_iter >= 1 &&
                       (a.raar ? recorded(a.ctl, a.u_iter) : gap_needed(a.ctl, a.u_iter));
     double* const part = a.part + ((a.raar && (a.u_iter & 1)) ? a.part_alt : 0);
+    // prefetch the next task's columns while this one computes (iterate mode,
+    // more than one task for this CTA)
+    const bool pf = L::PF && a.mode == 2 && (int)blockIdx.x + (int)gridDim.x < total;
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
         const int b = t / tpm, tt = t - b * tpm;
         const bool act = mask_live(a.st + b);
+        const int tn = t + gridDim.x;
+        auto prefetch = [&]() {
+            if (pf && tn < total) {
+                const int bn = tn / tpm, cn = (tn - bn * tpm) * C;
+                stage_tile<cx<T>, NX, L::C, kSolveThreads>(tile, a.in + (size_t)bn * NX * NX + cn, NX, threadIdx.x);
+            }
+        };
         double acc[3];
-        col_task<T, LG, LGR_C, (1 << LG), L::TS, L::PS, L::CH>(a, b, tt * C, C, smem, tw.cf, ms, act, acc);
+        col_task<T, LG, LGR_C, NX, L::TS, L::PS, L::CH>(a, b, tt * C, C, smem, tw.cf, ms, act, acc,
+                                                        (pf && t != (int)blockIdx.x) ? tile : nullptr, prefetch);
         if (metr && act) {
             double tot[3];
             block_reduce<3>(acc, tot);
