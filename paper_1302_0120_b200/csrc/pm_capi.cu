@@ -320,6 +320,7 @@ struct pm_plan {
     double* tolp = nullptr;           // cap: reference zero_tol of p
     double* thrp = nullptr;           // cap: decision thresholds (fp32: on |u|^2)
     double* thrm = nullptr;
+    double* thrms = nullptr;          // cap: column thresholds on the unscaled transform
     double* escale = nullptr;         // cap: sum m^2 / sum p^2
     double* energy = nullptr;         // cap: sum m^2 (host-provided)
     double* psum = nullptr;           // cap * kPsumBlocks partial sums of p^2
@@ -348,7 +349,7 @@ struct pm_plan {
         void* levels = nullptr;
         void* ustar = nullptr;
         void* vstar = nullptr;
-        std::vector<double> h_tolp, h_thrp, h_thrm, h_en, h_thrx;
+        std::vector<double> h_tolp, h_thrp, h_thrm, h_thrms, h_en, h_thrx;
         bool energy_on_device = false;
     } s;
 };
@@ -382,7 +383,7 @@ ColCfg col_config(const pm_plan* pl) {
 void free_buffers(pm_plan* pl) {
     void* bufs[] = {pl->field, pl->tmp, pl->pbuf, pl->mbuf, pl->phases, pl->levels, pl->ustar,
                     pl->vstar, pl->st, pl->hist, pl->part, pl->ctr, pl->tolp, pl->thrp,
-                    pl->thrm, pl->escale, pl->energy, pl->psum};
+                    pl->thrm, pl->thrms, pl->escale, pl->energy, pl->psum};
     for (void* b : bufs)
         if (b) cudaFree(b);
     void* rbufs[] = {pl->field2, pl->xbuf, pl->rpart, pl->thrx};
@@ -395,7 +396,7 @@ void free_buffers(pm_plan* pl) {
     pl->phases = nullptr;
     pl->levels = nullptr;
     pl->st = nullptr;
-    pl->hist = pl->part = pl->tolp = pl->thrp = pl->thrm = pl->escale = pl->energy = pl->psum = nullptr;
+    pl->hist = pl->part = pl->tolp = pl->thrp = pl->thrm = pl->thrms = pl->escale = pl->energy = pl->psum = nullptr;
     pl->ctr = nullptr;
     pl->cap = 0;
     pl->hist_cap = 0;
@@ -426,6 +427,7 @@ int ensure_capacity(pm_plan* pl, int batch, int max_iters) {
     CK(cudaMalloc((void**)&pl->tolp, cap * sizeof(double)));
     CK(cudaMalloc((void**)&pl->thrp, cap * sizeof(double)));
     CK(cudaMalloc((void**)&pl->thrm, cap * sizeof(double)));
+    CK(cudaMalloc((void**)&pl->thrms, cap * sizeof(double)));
     CK(cudaMalloc((void**)&pl->escale, cap * sizeof(double)));
     CK(cudaMalloc((void**)&pl->energy, cap * sizeof(double)));
     CK(cudaMalloc((void**)&pl->psum, (size_t)2 * cap * 32 * sizeof(double)));
@@ -565,6 +567,8 @@ ColArgs<T> col_args(pm_plan* pl, int mode, int u_iter) {
     a.ny = pl->ny;
     a.scale = (T)(1.0 / std::sqrt((double)pl->N));
     a.thr_m = pl->thrm;
+    a.thr_ms = pl->thrms;
+    a.scale_free = ((pl->lgx + pl->lgy) % 2 == 0) ? 1 : 0;
     a.escale = pl->escale;
     a.mode = mode;
     a.u_iter = u_iter;
@@ -737,6 +741,7 @@ int session_setup(pm_plan* pl, const void* d_p, const void* d_m, int batch, cons
     s.h_tolp.resize(batch);
     s.h_thrp.resize(batch);
     s.h_thrm.resize(batch);
+    s.h_thrms.resize(batch);
     s.h_en.resize(batch);
     s.h_thrx.resize(batch);
     for (int b = 0; b < batch; ++b) {
@@ -746,6 +751,8 @@ int session_setup(pm_plan* pl, const void* d_p, const void* d_m, int batch, cons
         s.h_thrp[b] = pl->prec == PM_SINGLE ? fp32_sq_threshold(tp) * (double)pl->N
                                             : tp * std::sqrt((double)pl->N);
         s.h_thrm[b] = pl->prec == PM_SINGLE ? fp32_sq_threshold(tol_m[b]) : tol_m[b];
+        // on S^-1 u^ (exact when N is a power of 4, the only case it is used)
+        s.h_thrms[b] = pl->prec == PM_SINGLE ? s.h_thrm[b] * (double)pl->N : s.h_thrm[b] * std::sqrt((double)pl->N);
         s.h_en[b] = energy ? energy[b] : 0.0;
         s.h_thrx[b] = pl->prec == PM_SINGLE ? fp32_sq_threshold(tp) : tp;   // RAAR P_S on true scale
     }
@@ -753,6 +760,7 @@ int session_setup(pm_plan* pl, const void* d_p, const void* d_m, int batch, cons
     CK(cudaMemcpyAsync(pl->tolp, s.h_tolp.data(), batch * sizeof(double), cudaMemcpyHostToDevice, pl->stream));
     CK(cudaMemcpyAsync(pl->thrp, s.h_thrp.data(), batch * sizeof(double), cudaMemcpyHostToDevice, pl->stream));
     CK(cudaMemcpyAsync(pl->thrm, s.h_thrm.data(), batch * sizeof(double), cudaMemcpyHostToDevice, pl->stream));
+    CK(cudaMemcpyAsync(pl->thrms, s.h_thrms.data(), batch * sizeof(double), cudaMemcpyHostToDevice, pl->stream));
     CK(cudaMemcpyAsync(pl->energy, s.h_en.data(), batch * sizeof(double), cudaMemcpyHostToDevice, pl->stream));
     if (pl->thrx)
         CK(cudaMemcpyAsync(pl->thrx, s.h_thrx.data(), batch * sizeof(double), cudaMemcpyHostToDevice, pl->stream));

@@ -147,7 +147,9 @@ struct ColArgs {
     const twe<T>* twi;
     int nx, ny;
     T scale;                  // S = 1/sqrt(nx*ny)
-    const double* thr_m;      // [batch] zero-branch threshold (as thr_p)
+    const double* thr_m;      // [batch] zero-branch threshold on u^ (fp32: on |u^|^2, fp64: on |u^|)
+    const double* thr_ms;     // [batch] the same on S^-1 u^ (used when scale_free)
+    int scale_free;           // N is a power of 4: S is a power of two and the replace is scale-invariant
     const double* escale;     // [batch] sum m^2 / sum |u|^2 (reconstructed-intensity scale)
     int mode;                 // 0: init from real m, 1: init from complex field, 2: iterate
     int u_iter;               // metrics of iterate u_{u_iter} (0 = none)
@@ -664,7 +666,6 @@ __device__ __forceinline__ void col_task(const ColArgs<T>& a, int b, int col0, i
     const bool metr = a.u_iter >= 1;
     const bool rec = metr && recorded(a.ctl, a.u_iter);
     const bool gneed = metr && !a.raar && gap_needed(a.ctl, a.u_iter);
-    const T thr = T(a.thr_m[b]);
 #if PM_ROLL
     const int trips = 1 + (a.ny > 0);         // 2, opaque: one rolled copy of the transform
 #pragma unroll 1
@@ -675,8 +676,14 @@ __device__ __forceinline__ void col_task(const ColArgs<T>& a, int b, int col0, i
     for (int h = 0; h < trips; ++h) {
         fft1d<T, LG_L, LG_R, -1, TS>(v, sm, tw, j, SyncBlock{});   // h = 0: ColFFT(w'); h = 1: conj(z')
         if (h) break;
+        // u^ = F(u) = S * ColFFT(w'): the replace is invariant to the exact
+        // power-of-two S (threshold pre-scaled), so only metrics need u^ itself
+        const bool scaled = rec || gneed || !a.scale_free;
+        if (scaled) {
 #pragma unroll
-        for (int k = 0; k < F::R; ++k) v[k] = cscale(v[k], a.scale);     // u^ = F(u) = S * ColFFT(w')
+            for (int k = 0; k < F::R; ++k) v[k] = cscale(v[k], a.scale);
+        }
+        const T thr = T(scaled ? a.thr_m[b] : a.thr_ms[b]);
         if constexpr (PS) {
             cp_async_wait<1>();                      // m of this task (the prefetch may stay in flight)
             __syncthreads();
