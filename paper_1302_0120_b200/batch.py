@@ -51,16 +51,18 @@ class BatchResult:
     err_dark: np.ndarray        # (B, K)
     iters_run: np.ndarray       # (B,)
     device_ms: float = 0.0      # device time of the slowest shard
+    levels: np.ndarray | None = None   # (B, n_y, n_x) uint8 SLM levels (PhaseMask.to_uint8), when asked
 
     @staticmethod
     def concat(parts: list["BatchResult"]) -> "BatchResult":
         parts = [q for q in parts if q.phases.shape[0]]
+        levels = None if any(q.levels is None for q in parts) else np.concatenate([q.levels for q in parts])
         return BatchResult(np.concatenate([q.phases for q in parts]),
                            np.concatenate([q.gap for q in parts]),
                            np.concatenate([q.err_lit for q in parts]),
                            np.concatenate([q.err_dark for q in parts]),
                            np.concatenate([q.iters_run for q in parts]),
-                           max(q.device_ms for q in parts))
+                           max(q.device_ms for q in parts), levels)
 
 
 def _maxes(a: np.ndarray, k: int) -> np.ndarray:
@@ -68,14 +70,15 @@ def _maxes(a: np.ndarray, k: int) -> np.ndarray:
 
 
 def solve_stack(p: np.ndarray, m_stack: np.ndarray, cfg: SolveConfig, device: int = 0,
-                out_phases: np.ndarray | None = None) -> BatchResult:
+                out_phases: np.ndarray | None = None, levels: bool = False) -> BatchResult:
     """Solve a stack of targets on one device in one launch.
 
     p: (n_y, n_x) shared amplitude or (B, n_y, n_x) per mask; m_stack:
     (B, n_y, n_x) target moduli in DFT order. Arrays already in the
     precision's dtype are used without a host copy (pass pinned buffers for
     full-speed transfers); ``out_phases`` (B, n_y, n_x) float64 may be a
-    caller-owned (e.g. pinned) buffer for the mask. The per-mask energy
+    caller-owned (e.g. pinned) buffer for the mask; ``levels=True`` also
+    returns the 8-bit SLM levels computed on the device. The per-mask energy
     sum(m^2) is reduced on the device.
     """
     m_stack = np.asarray(m_stack)
@@ -114,6 +117,10 @@ def solve_stack(p: np.ndarray, m_stack: np.ndarray, cfg: SolveConfig, device: in
     res.phases = _lib.ptr(out.phases)
     res.gap, res.err_lit, res.err_dark = _lib.ptr(out.gap), _lib.ptr(out.err_lit), _lib.ptr(out.err_dark)
     res.iters_run, res.diverged_iter, res.device_ms = _lib.ptr(out.iters_run), _lib.ptr(div), _lib.ptr(ms)
+    if levels:
+        # 8-bit SLM levels computed on the device (reference src/grid.py:152-154)
+        out.levels = np.empty((B, ny, nx), dtype=np.uint8)
+        res.levels = _lib.ptr(out.levels)
     prm = _params(cfg, per_mask, False)
     with plan.lock:
         code = plan.lib.pm_solve(plan.handle, _lib.ptr(pp), _lib.ptr(mm), None, B, prm, _lib.ptr(tol_p),

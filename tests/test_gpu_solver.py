@@ -174,6 +174,21 @@ def test_batch_per_mask_amplitude_and_early_stop():
         np.testing.assert_array_equal(r.mask.phases, res.phases[i])
 
 
+@pytest.mark.parametrize("tag", ["double", "single"])
+def test_device_slm_levels_match_to_uint8(tag):
+    """uint8 levels computed on the device equal PhaseMask.to_uint8 of the
+    float64 mask bitwise (reference src/grid.py:152-154)."""
+    prec = pm.Precision.from_tag(tag)
+    p, _ = make_problem(256, 8, 7)
+    ms = np.stack([make_problem(256, 8, s)[1] for s in (3, 4)])
+    res = solve_stack(p.astype(prec.float_dtype), ms.astype(prec.float_dtype),
+                      pm.SolveConfig(max_iters=20, precision=prec), levels=True)
+    spec = pm.GridSpec(256, 256)
+    for i in range(2):
+        np.testing.assert_array_equal(res.levels[i], pm.PhaseMask(spec, res.phases[i]).to_uint8())
+    assert res.levels.dtype == np.uint8 and res.levels.max() <= 255
+
+
 @pytest.mark.slow
 @pytest.mark.parametrize("n", [2048, 4096])
 def test_large_field_properties(n):
