@@ -475,7 +475,7 @@ __device__ __forceinline__ void row_task(const RowArgs<T>& a, int b, int row, in
         for (int k = 0; k < F::R; ++k) v[k] = inb ? ld_field(f + F::TG * k) : mk<T>(T(0), T(0));   // conj(z')
     }
     if constexpr (PS) {
-        if (inb && a.mode != kRowInit) stage_runs<T, 16>(ps, p - j, 1, 1 << LG_L, 0, j, F::TG);
+        if (inb && a.mode != kRowInit) stage_tile<T, 1, (1 << LG_L), F::TG>(ps, p - j, 0, j);
         cp_async_commit();
     }
     prefetch();
@@ -612,7 +612,7 @@ __device__ __forceinline__ void final_task(const FinalArgs<T>& a, int b, int row
 // receives this task's [n_y][C] slice of m through cp.async.
 // `tile` / `prefetch()`: cross-task prefetch as in row_task (the tile holds
 // this task's [n_y][C] input, written by the previous task's cp.async).
-template <typename T, int LG_L, int LG_R, int NX, bool TS = false, bool PS = false, int CH = 16,
+template <typename T, int LG_L, int LG_R, int NX, bool TS = false, bool PS = false, int CC = 0,
           class Prefetch = NoPrefetch>
 __device__ __forceinline__ void col_task(const ColArgs<T>& a, int b, int col0, int C, cx<T>* smbase,
                                          const twe<T>* tw, T* ms, bool live, double (&acc)[3],
@@ -658,7 +658,9 @@ __device__ __forceinline__ void col_task(const ColArgs<T>& a, int b, int col0, i
         return;
     }
     if constexpr (PS) {
-        stage_runs<T, CH>(ms, a.m + b * a.m_stride + col0, a.ny, C, nx, threadIdx.x, blockDim.x);
+        // CC: the persistent kernel's compile-time column count (division-free copy loop)
+        static_assert(CC > 0, "staged m needs the compile-time column count");
+        stage_tile<T, (1 << LG_L), CC, CC * F::TG>(ms, a.m + b * a.m_stride + col0, nx, threadIdx.x);
         cp_async_commit();
     }
     prefetch();
@@ -1103,7 +1105,7 @@ __device__ __forceinline__ void col_phase(const ColArgs<T>& a, int batch, unsign
             }
         };
         double acc[3];
-        col_task<T, LG, LGR_C, NX, L::TS, L::PS, L::CH>(a, b, tt * C, C, smem, tw.cf, ms, act, acc,
+        col_task<T, LG, LGR_C, NX, L::TS, L::PS, L::C>(a, b, tt * C, C, smem, tw.cf, ms, act, acc,
                                                         (pf && t != (int)blockIdx.x) ? tile : nullptr, prefetch);
         if (metr && act) {
             double tot[3];
