@@ -1147,8 +1147,9 @@ static int replace_dev(pm_plan* pl, const void* in, const void* target, int per_
     const long long n = (long long)pl->N;
     const int blocks = (int)std::min<long long>((n + 255) / 256, 1184);
     if (pl->prec == PM_SINGLE)
+        // fp32 decides on |u|^2 against the exact squared threshold (as the solve does)
         replace_kernel<float><<<dim3(blocks, batch), 256, 0, pl->stream>>>(
-            (const float2*)in, (const float*)target, per_field ? n : 0, (float)tol, (float2*)out, n);
+            (const float2*)in, (const float*)target, per_field ? n : 0, (float)fp32_sq_threshold(tol), (float2*)out, n);
     else
         replace_kernel<double><<<dim3(blocks, batch), 256, 0, pl->stream>>>(
             (const double2*)in, (const double*)target, per_field ? n : 0, tol, (double2*)out, n);
@@ -1234,8 +1235,9 @@ int pm_gap(pm_plan* pl, const void* u, const void* p, const void* m, double zero
     CKR(project_fourier_dev(pl, pl->tmp, pl->mbuf, zero_tol_m, pl->field));
     if (pl->prec == PM_SINGLE)
         gap_partial_kernel<float><<<nb, 256, 0, pl->stream>>>((const float2*)pl->tmp, (const float2*)pl->field,
-                                                               (const float*)pl->pbuf, (float)zero_tol_p, n,
-                                                               chunk, pl->red);
+                                                               (const float*)pl->pbuf,
+                                                               (float)fp32_sq_threshold(zero_tol_p), n, chunk,
+                                                               pl->red);
     else
         gap_partial_kernel<double><<<nb, 256, 0, pl->stream>>>((const double2*)pl->tmp,
                                                                 (const double2*)pl->field,

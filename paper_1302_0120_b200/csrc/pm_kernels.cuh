@@ -359,6 +359,10 @@ __device__ __forceinline__ void first_bad(int* bad, int it) {
     if (__ldcg(bad) == 0) atomicCAS(bad, 0, it);
 }
 
+template <typename T> __device__ __forceinline__ T min_normal();
+template <> __device__ __forceinline__ float min_normal<float>() { return 1.17549435e-38f; }
+template <> __device__ __forceinline__ double min_normal<double>() { return 2.2250738585072014e-308; }
+
 // Cross-CTA field loads bypass L1 (the field is rewritten between phases).
 template <typename C> __device__ __forceinline__ C ld_field(const C* p) { return __ldcg(p); }
 
@@ -504,11 +508,20 @@ __device__ __forceinline__ void row_task(const RowArgs<T>& a, int b, int row, in
             // u = P_S v = P_S v' = conj(P_S y) (src/projections.py:69-74), threshold pre-scaled
             const T thr = T(a.thr_p[b]);
             T chk = T(0);
+            if (thr >= min_normal<T>()) {
 #pragma unroll
-            for (int k = 0; k < F::R; ++k) {
-                T s2;
-                v[k] = replace_mod<true>(v[k], inb ? p_at(k) : T(0), thr, s2);
-                chk += s2;                              // non-finite detector (reference Field checks)
+                for (int k = 0; k < F::R; ++k) {
+                    T s2;
+                    v[k] = replace_mod<true, true>(v[k], inb ? p_at(k) : T(0), thr, s2);
+                    chk += s2;                          // non-finite detector (reference Field checks)
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < F::R; ++k) {
+                    T s2;
+                    v[k] = replace_mod<true>(v[k], inb ? p_at(k) : T(0), thr, s2);
+                    chk += s2;
+                }
             }
             if (act && !isfinite(chk)) first_bad(&a.st[b].bad, a.it);
         } else if (a.mode == kRowInit) {
@@ -728,12 +741,21 @@ __device__ __forceinline__ void col_task(const ColArgs<T>& a, int b, int col0, i
             }
         }
         T g2 = T(0);
+        if (thr >= min_normal<T>()) {
 #pragma unroll
-        for (int k = 0; k < F::R; ++k) {
-            const cx<T> vh = replace_mod<true>(v[k], mm[k], thr);     // conj(v^), v^ = replace_m(u^)
-            // G(u) = ||P_S u - P_M u|| = ||u^ - v^||  (Parseval; u is on S)
-            if (gneed) g2 += norm_sq(csub(v[k], cconj(vh)));
-            v[k] = vh;
+            for (int k = 0; k < F::R; ++k) {
+                const cx<T> vh = replace_mod<true, true>(v[k], mm[k], thr);   // conj(v^), v^ = replace_m(u^)
+                // G(u) = ||P_S u - P_M u|| = ||u^ - v^||  (Parseval; u is on S)
+                if (gneed) g2 += norm_sq(csub(v[k], cconj(vh)));
+                v[k] = vh;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < F::R; ++k) {
+                const cx<T> vh = replace_mod<true>(v[k], mm[k], thr);
+                if (gneed) g2 += norm_sq(csub(v[k], cconj(vh)));
+                v[k] = vh;
+            }
         }
         acc[0] = act ? (double)g2 : 0.0;
     }

@@ -29,6 +29,36 @@ def test_project_slm_kats():
     assert project_slm(pm.Field(spec, np.zeros((1, 1))), slm(spec, np.full((1, 1), 2.0))).data[0, 0] == 2 + 0j
 
 
+@pytest.mark.parametrize("fn", ["slm", "modulus", "gap"])
+def test_single_precision_threshold_is_on_the_modulus(fn):
+    """fp32 zero-branch decision is |u| >= zero_tol (src/projections.py:46-55),
+    including moduli between zero_tol and sqrt(zero_tol), where a test on |u|^2
+    would differ; checked bitwise against the oracle restatement."""
+    spec = pm.GridSpec(8, 8)
+    t = np.ones(spec.shape)                        # zero_tol = 1024 eps32 = 1.22e-4
+    rng = np.random.default_rng(5)
+    phase = np.exp(1j * rng.uniform(0, 2 * np.pi, spec.shape))
+    mags = np.full(spec.shape, 1e-3)               # >= tol, but |u|^2 = 1e-6 < tol
+    mags[0, :4] = [5e-5, 1.2e-4, 1.25e-4, 0.0]     # below / at the threshold / zero
+    u = (mags * phase).astype(np.complex64)
+    tol = orc.zero_tol("single", t)
+    if fn == "slm":
+        got = project_slm(pm.Field(spec, u), pm.SlmConstraint(pm.RealGrid(spec, t), pm.SINGLE)).data
+    elif fn == "modulus":
+        got = project_modulus(pm.Field(spec, u, FOURIER_PLANE),
+                              pm.FourierConstraint(pm.RealGrid(spec, t), pm.SINGLE)).data
+    else:
+        m = np.abs(random_field(spec, rng))
+        g = gap(pm.Field(spec, u), pm.SlmConstraint(pm.RealGrid(spec, t), pm.SINGLE),
+                pm.FourierConstraint(pm.RealGrid(spec, m), pm.SINGLE), pm.FftProvider(spec, pm.SINGLE))
+        assert g == pytest.approx(orc.gap(u, t, m, "single"), rel=1e-5)
+        return
+    want = orc.replace_modulus(u, t, tol, "single")
+    zero = np.abs(want - t) == 0
+    np.testing.assert_array_equal(zero, np.abs(got - t) == 0)          # same branch everywhere
+    np.testing.assert_allclose(got, want, rtol=2e-7, atol=0)
+
+
 def test_project_modulus_kats():
     spec = pm.GridSpec(1, 1)
     c = pm.FourierConstraint(pm.RealGrid(spec, np.full((1, 1), math.sqrt(2))))
