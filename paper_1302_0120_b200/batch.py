@@ -70,7 +70,8 @@ def _maxes(a: np.ndarray, k: int) -> np.ndarray:
 
 
 def solve_stack(p: np.ndarray, m_stack: np.ndarray, cfg: SolveConfig, device: int = 0,
-                out_phases: np.ndarray | None = None, levels: bool = False) -> BatchResult:
+                out_phases: np.ndarray | None = None, levels: bool = False,
+                init: np.ndarray | None = None) -> BatchResult:
     """Solve a stack of targets on one device in one launch.
 
     p: (n_y, n_x) shared amplitude or (B, n_y, n_x) per mask; m_stack:
@@ -78,7 +79,9 @@ def solve_stack(p: np.ndarray, m_stack: np.ndarray, cfg: SolveConfig, device: in
     precision's dtype are used without a host copy (pass pinned buffers for
     full-speed transfers); ``out_phases`` (B, n_y, n_x) float64 may be a
     caller-owned (e.g. pinned) buffer for the mask; ``levels=True`` also
-    returns the 8-bit SLM levels computed on the device. The per-mask energy
+    returns the 8-bit SLM levels computed on the device; ``init`` (B, n_y, n_x)
+    complex are Fourier-plane starts m e^{i phi} (random-phase init,
+    src/solver.py:100-103) instead of m. The per-mask energy
     sum(m^2) is reduced on the device.
     """
     m_stack = np.asarray(m_stack)
@@ -121,10 +124,15 @@ def solve_stack(p: np.ndarray, m_stack: np.ndarray, cfg: SolveConfig, device: in
         # 8-bit SLM levels computed on the device (reference src/grid.py:152-154)
         out.levels = np.empty((B, ny, nx), dtype=np.uint8)
         res.levels = _lib.ptr(out.levels)
-    prm = _params(cfg, per_mask, False)
+    init_c = None
+    if init is not None:
+        init_c = np.ascontiguousarray(init, dtype=prec.complex_dtype)
+        if init_c.shape != (B, ny, nx):
+            raise ValueError("init must be a (batch, n_y, n_x) complex stack")
+    prm = _params(cfg, per_mask, init_c is not None)
     with plan.lock:
-        code = plan.lib.pm_solve(plan.handle, _lib.ptr(pp), _lib.ptr(mm), None, B, prm, _lib.ptr(tol_p),
-                                 _lib.ptr(tol_m), None, res)
+        code = plan.lib.pm_solve(plan.handle, _lib.ptr(pp), _lib.ptr(mm), _lib.ptr(init_c), B, prm,
+                                 _lib.ptr(tol_p), _lib.ptr(tol_m), None, res)
     if code == _lib.PM_ERR_DIVERGED or div.any():
         raise SolveDivergedError(int(div[div > 0][0]) if div.any() else 1)
     _lib.check(code, "pm_solve")
@@ -133,8 +141,12 @@ def solve_stack(p: np.ndarray, m_stack: np.ndarray, cfg: SolveConfig, device: in
 
 
 def solve_batch(p: np.ndarray, m_stack: np.ndarray, cfg: SolveConfig,
-                devices: list[int] | None = None) -> BatchResult:
-    """Shard a stack of masks across local GPUs (one host thread per device)."""
+                devices: list[int] | None = None, **kw) -> BatchResult:
+    """Shard a stack of masks across local GPUs (one host thread per device).
+
+    Extra keyword arguments (``levels``, ``init``) go to :func:`solve_stack`;
+    a per-mask ``init`` stack is split with the masks.
+    """
     if devices is None:
         devices = list(range(max(1, _lib.device_count())))
     m_stack = np.asarray(m_stack)
@@ -143,9 +155,12 @@ def solve_batch(p: np.ndarray, m_stack: np.ndarray, cfg: SolveConfig,
     G = len(devices)
     bounds = [shard_bounds(B, G, r) for r in range(G)]
 
+    init = kw.pop("init", None)
+
     def run(r):
         lo, hi = bounds[r]
-        return solve_stack(p[lo:hi] if per_mask else p, m_stack[lo:hi], cfg, devices[r])
+        return solve_stack(p[lo:hi] if per_mask else p, m_stack[lo:hi], cfg, devices[r],
+                           init=None if init is None else init[lo:hi], **kw)
 
     if G == 1:
         return run(0)
