@@ -642,7 +642,7 @@ int launch_solve(pm_plan* pl, int do_init, int it_begin, int it_end, int do_fina
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(pl->solve_grid);
     cfg.blockDim = dim3(k.solve_threads);
-    cfg.dynamicSmemBytes = (size_t)k.solve_smem;
+    cfg.dynamicSmemBytes = (size_t)(pl->s.prm.algorithm == PM_ALGO_RAAR ? k.solve_smem_raar : k.solve_smem);
     cfg.stream = pl->stream;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeCooperative;
@@ -1026,13 +1026,13 @@ int pm_plan_create(int device, int n_x, int n_y, int precision, int max_batch, p
             // one grid size for both algorithms' kernels: the smaller occupancy
             int per_sm_raar = 0;
             cudaError_t e4 = allow_smem(ks.solve, ks.solve_smem);
-            if (e4 == cudaSuccess) e4 = allow_smem(ks.solve_raar, ks.solve_smem);
+            if (e4 == cudaSuccess) e4 = allow_smem(ks.solve_raar, ks.solve_smem_raar);
             if (e4 == cudaSuccess)
                 e4 = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ks.solve, ks.solve_threads,
                                                                    ks.solve_smem);
             if (e4 == cudaSuccess)
                 e4 = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_raar, ks.solve_raar,
-                                                                   ks.solve_threads, ks.solve_smem);
+                                                                   ks.solve_threads, ks.solve_smem_raar);
             per_sm = std::min(per_sm, per_sm_raar);
             if (e4 == cudaSuccess && per_sm > 0) pl->solve_grid = per_sm * nsm;
             cudaGetLastError();

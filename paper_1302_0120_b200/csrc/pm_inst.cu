@@ -39,12 +39,14 @@ KernelSet PM_CAT3(make_set_, PM_TAG, PM_LG)() {
     s.solve = nullptr;
     s.solve_raar = nullptr;
     s.solve_smem = 0;
+    s.solve_smem_raar = 0;
     s.solve_threads = 0;
     // persistent kernel: square grids n >= 128 whose transforms fit one CTA
     if constexpr (PM_LG >= 7 && FR::TG <= kSolveThreads && FC::TG <= kSolveThreads) {
         s.solve = (const void*)&solve_kernel<PM_T, PM_LG, PM_LGR_ROW, PM_LGR_COL, 0>;
         s.solve_raar = (const void*)&solve_kernel<PM_T, PM_LG, PM_LGR_ROW, PM_LGR_COL, 1>;
         s.solve_smem = SolveSmem<PM_T, PM_LG, PM_LGR_ROW, PM_LGR_COL>::BYTES;
+        s.solve_smem_raar = SolveSmem<PM_T, PM_LG, PM_LGR_ROW, PM_LGR_COL>::BYTES_RAAR;
         s.solve_threads = kSolveThreads;
     }
     s.row = AxisShape{FR::lgR, FR::TG, FR::NP, FR::SM, FR::TW};

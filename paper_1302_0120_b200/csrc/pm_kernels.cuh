@@ -455,11 +455,13 @@ __device__ __forceinline__ void stage_tile(E* dst, const E* src, size_t gstride,
 // cp.async; `prefetch()` starts the copy of the next task's input. cp.async
 // groups per task, in commit order: [p of this task] [next task's field],
 // so the projection waits for one group and leaves the prefetch in flight.
+// `xs` (XS, RAAR): this row's slice of x staged with p.
 template <typename T, int LG_L, int LG_R, class Sync, int ALG = -1, bool TS = false, bool PS = false,
-          class Prefetch = NoPrefetch>
+          class Prefetch = NoPrefetch, bool XS = false>
 __device__ __forceinline__ void row_task(const RowArgs<T>& a, int b, int row, int j, cx<T>* sm,
                                          const twe<T>* tw, T* ps, bool inb_arg, bool live, Sync sync,
-                                         const cx<T>* tile = nullptr, Prefetch prefetch = Prefetch{}) {
+                                         const cx<T>* tile = nullptr, Prefetch prefetch = Prefetch{},
+                                         cx<T>* xs = nullptr) {
     using F = FftShape<LG_L, LG_R>;
     const size_t N = (size_t)a.nx * a.ny;
     // whole-warp groups never run out of bounds (the row phase skips them)
@@ -480,6 +482,10 @@ __device__ __forceinline__ void row_task(const RowArgs<T>& a, int b, int row, in
     }
     if constexpr (PS) {
         if (inb && a.mode != kRowInit) stage_tile<T, 1, (1 << LG_L), F::TG>(ps, p - j, 0, j);
+        if constexpr (XS) {
+            if (inb && (a.mode == kRowRaar || a.mode == kRowProbe))
+                stage_tile<cx<T>, 1, (1 << LG_L), F::TG>(xs, a.x + b * N + (size_t)row * a.nx, 0, j);
+        }
         cp_async_commit();
     }
     prefetch();
@@ -544,7 +550,9 @@ __device__ __forceinline__ void row_task(const RowArgs<T>& a, int b, int row, in
 #pragma unroll
             for (int k = 0; k < F::R; ++k) {
                 const cx<T> vv = cscale_conj(v[k], a.scale);
-                const cx<T> xo = inb ? ld_field(xp + F::TG * k) : mk<T>(T(0), T(0));
+                cx<T> xo;
+                if constexpr (XS) xo = inb ? xs[j + F::TG * k] : mk<T>(T(0), T(0));
+                else xo = inb ? ld_field(xp + F::TG * k) : mk<T>(T(0), T(0));
                 const T pk = inb ? p_at(k) : T(0);
                 if (gneed) g2 += norm_sq_d(csub_rn(replace_mod(xo, pk, thr), vv));
                 if (upd) {
@@ -996,6 +1004,11 @@ struct SolveSmem {
     static constexpr int OFF_TILE = EX + (PS ? ST : 0);
     static constexpr int OFF_TW = OFF_TILE + (PF ? TILE : 0);
     static constexpr int BYTES = OFF_TW + (TS ? TWB : 0);
+    // RAAR kernel: the row's iterate x staged with p (cp.async) when it fits
+    static constexpr int XSB = up16((int)sizeof(cx<T>) * (G << LG));
+    static constexpr bool XS = PS && BYTES + XSB <= LIMIT;
+    static constexpr int OFF_XS = BYTES;
+    static constexpr int BYTES_RAAR = BYTES + (XS ? XSB : 0);
     static constexpr int CB = C * (int)sizeof(T);                 // bytes per m run of a column task
     static constexpr int CH = CB >= 16 ? 16 : CB;                 // cp.async size for it
 };
@@ -1065,9 +1078,11 @@ __device__ __forceinline__ void row_phase(const RowArgs<T>& a, int batch, unsign
             if (pf && rn < count)
                 stage_tile<cx<T>, 1, NX, F::TG>(tile, a.field + (size_t)(start + rn) * NX, 0, j);
         };
-        row_task<T, LG, LGR_R, decltype(group_sync<F::TG>(g)), ALG, L::TS, L::PS>(
+        constexpr bool XS = ALG == 1 && L::XS;
+        row_task<T, LG, LGR_R, decltype(group_sync<F::TG>(g)), ALG, L::TS, L::PS, decltype(prefetch), XS>(
             a, b, r & (NX - 1), j, smem + g * F::SM, tw.rf, ps, inb, live, group_sync<F::TG>(g),
-            (pf && r0 > 0) ? tile : nullptr, prefetch);
+            (pf && r0 > 0) ? tile : nullptr, prefetch,
+            XS ? reinterpret_cast<cx<T>*>(smraw + L::OFF_XS) + ((size_t)g << LG) : nullptr);
     }
 }
 

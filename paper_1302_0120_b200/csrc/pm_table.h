@@ -23,6 +23,7 @@ struct KernelSet {
     const void* solve;      // solve_kernel<T, lg, lgR_row, lgR_col, GS> (square grids, lg >= 7) or null
     const void* solve_raar; // the same for RAAR
     int solve_smem;         // its dynamic shared memory (bytes)
+    int solve_smem_raar;    // the RAAR kernel's (x staged as well)
     int solve_threads;      // its CTA size
     AxisShape row, col;
 };
