@@ -17,6 +17,7 @@
 #include <vector>
 
 #include "phasemask_b200.h"
+#include "pm_generic.cuh"
 #include "pm_kernels.cuh"
 #include "pm_table.h"
 
@@ -311,8 +312,15 @@ struct pm_plan {
     void* field2 = nullptr;           // RAAR: cap * N complex, second field buffer (w')
     void* xbuf = nullptr;             // RAAR: cap * N complex, the iterate x
     double* rpart = nullptr;          // RAAR: cap * ny * wpr * 2 row partials
-    double* thrx = nullptr;           // RAAR: cap P_S thresholds on true-scale values
+    double* thrx = nullptr;           // cap P_S thresholds on true-scale values (RAAR, mixed-radix path)
     int raar_cap = 0;
+    // mixed-radix path (a side that is not a power of two; pm_generic.cuh)
+    bool generic = false;
+    GenPlan gx{}, gy{};               // row (n_x) and column (n_y) transforms
+    void* gtwx = nullptr;             // exp(-2 pi i k / n_x), k < n_x, plan precision
+    void* gtwy = nullptr;
+    int gtc_r = 1, gtc_c = 1;         // transforms per CTA
+    size_t gsm_r = 0, gsm_c = 0;      // their shared memory
     MaskState* st = nullptr;          // cap
     double* hist = nullptr;           // cap * hist_cap * 4
     double* part = nullptr;           // column partial sums, 2 (parity) * cap * nb * 3
@@ -415,7 +423,7 @@ int ensure_capacity(pm_plan* pl, int batch, int max_iters) {
     drop_graphs(pl);
     free_buffers(pl);
     const size_t N = pl->N;
-    const int nb = std::max(pl->cc.nblk, pl->nx);   // >= tasks per mask of either path
+    const int nb = std::max(std::max(pl->cc.nblk, pl->nx), 148);   // >= tasks / blocks per mask of any path
     CK(cudaMalloc(&pl->field, cap * N * pl->csz));
     CK(cudaMalloc(&pl->tmp, cap * N * pl->csz));
     CK(cudaMalloc(&pl->pbuf, cap * N * pl->rsz));
@@ -428,6 +436,7 @@ int ensure_capacity(pm_plan* pl, int batch, int max_iters) {
     CK(cudaMalloc((void**)&pl->thrp, cap * sizeof(double)));
     CK(cudaMalloc((void**)&pl->thrm, cap * sizeof(double)));
     CK(cudaMalloc((void**)&pl->thrms, cap * sizeof(double)));
+    CK(cudaMalloc((void**)&pl->thrx, cap * sizeof(double)));
     CK(cudaMalloc((void**)&pl->escale, cap * sizeof(double)));
     CK(cudaMalloc((void**)&pl->energy, cap * sizeof(double)));
     CK(cudaMalloc((void**)&pl->psum, (size_t)2 * cap * 32 * sizeof(double)));
@@ -442,7 +451,7 @@ int ensure_capacity(pm_plan* pl, int batch, int max_iters) {
 int row_wpr(const pm_plan* pl) { return std::max(1, kset(pl->prec, pl->lgx).row.TG / 32); }
 
 // Elements of one parity half of `part`.
-size_t part_half(const pm_plan* pl) { return (size_t)pl->cap * std::max(pl->cc.nblk, pl->nx) * 3; }
+size_t part_half(const pm_plan* pl) { return (size_t)pl->cap * std::max(std::max(pl->cc.nblk, pl->nx), 148) * 3; }
 
 // Column tasks per mask of the persistent kernel.
 int solve_tpm(const pm_plan* pl) {
@@ -454,16 +463,15 @@ int solve_tpm(const pm_plan* pl) {
 // RAAR buffers (allocated on first use, sized to the batch capacity).
 int ensure_raar(pm_plan* pl) {
     if (pl->raar_cap >= pl->cap) return PM_OK;
-    for (void* b : {pl->field2, pl->xbuf, (void*)pl->rpart, (void*)pl->thrx})
+    for (void* b : {pl->field2, pl->xbuf, (void*)pl->rpart})
         if (b) cudaFree(b);
     pl->field2 = pl->xbuf = nullptr;
-    pl->rpart = pl->thrx = nullptr;
+    pl->rpart = nullptr;
     pl->raar_cap = 0;
     const size_t n = (size_t)pl->cap * pl->N;
     CK(cudaMalloc(&pl->field2, n * pl->csz));
     CK(cudaMalloc(&pl->xbuf, n * pl->csz));
     CK(cudaMalloc((void**)&pl->rpart, (size_t)pl->cap * pl->ny * row_wpr(pl) * 2 * sizeof(double)));
-    CK(cudaMalloc((void**)&pl->thrx, (size_t)pl->cap * sizeof(double)));
     pl->raar_cap = pl->cap;
     return PM_OK;
 }
@@ -698,7 +706,201 @@ int launch_fft2(pm_plan* pl, const void* in, void* out, int dir, int batch) {
     return PM_OK;
 }
 
+// ------------------------------------------------------- mixed-radix path
+// Factor n into passes of radix 4, 2, 3, 5, 7 (fails for other primes).
+bool gen_factor(int n, GenPlan* g) {
+    if (n < 1 || n > (1 << kMaxLg)) return false;
+    g->L = n;
+    g->np = 0;
+    int rest = n, ns = 1;
+    const int order[] = {4, 2, 3, 5, 7};
+    for (int r : order) {
+        while (rest % r == 0) {
+            if (g->np == kGenMaxPasses) return false;
+            g->radix[g->np] = r;
+            g->ns[g->np] = ns;
+            ++g->np;
+            ns *= r;
+            rest /= r;
+        }
+    }
+    return rest == 1;
+}
+
+// exp(-2 pi i k / n) in the plan precision, long-double accurate.
+int gen_twiddles(int prec, int n, void** out) {
+    const long double pi = 3.141592653589793238462643383279502884L;
+    if (prec == PM_SINGLE) {
+        std::vector<float2> t(n);
+        for (int k = 0; k < n; ++k) {
+            const long double a = 2.0L * pi * (long double)k / (long double)n;
+            t[k] = make_float2((float)cosl(a), (float)-sinl(a));
+        }
+        CK(cudaMalloc(out, n * sizeof(float2)));
+        CK(cudaMemcpy(*out, t.data(), n * sizeof(float2), cudaMemcpyHostToDevice));
+    } else {
+        std::vector<double2> t(n);
+        for (int k = 0; k < n; ++k) {
+            const long double a = 2.0L * pi * (long double)k / (long double)n;
+            t[k] = make_double2((double)cosl(a), (double)-sinl(a));
+        }
+        CK(cudaMalloc(out, n * sizeof(double2)));
+        CK(cudaMemcpy(*out, t.data(), n * sizeof(double2), cudaMemcpyHostToDevice));
+    }
+    return PM_OK;
+}
+
+constexpr size_t kGenSmem = 96 * 1024;   // two [L][TC] buffers per CTA
+
+int gen_setup(pm_plan* pl) {
+    CKR(gen_twiddles(pl->prec, pl->nx, &pl->gtwx));
+    CKR(gen_twiddles(pl->prec, pl->ny, &pl->gtwy));
+    pl->gtc_r = (int)std::max<size_t>(1, std::min<size_t>(16, kGenSmem / (2 * pl->nx * pl->csz)));
+    pl->gtc_c = (int)std::max<size_t>(1, std::min<size_t>(16, kGenSmem / (2 * pl->ny * pl->csz)));
+    pl->gsm_r = 2 * (size_t)pl->nx * pl->gtc_r * pl->csz;
+    pl->gsm_c = 2 * (size_t)pl->ny * pl->gtc_c * pl->csz;
+    const size_t mx = std::max(pl->gsm_r, pl->gsm_c);
+    cudaError_t e = pl->prec == PM_SINGLE ? allow_smem((const void*)&gen_fft_kernel<float>, mx)
+                                          : allow_smem((const void*)&gen_fft_kernel<double>, mx);
+    if (e != cudaSuccess) return cuda_err(e, "cudaFuncSetAttribute(gen_fft_kernel)");
+    return PM_OK;
+}
+
+// One axis (rows: axis 0, columns: axis 1) of the unitary 2-D DFT,
+// in -> out, for `batch` masks; masks that stopped are skipped unless
+// all_masks (st null: no mask state, stand-alone transform).
+template <typename T>
+int gen_axis(pm_plan* pl, const void* in, void* out, int axis, int dir, int batch, const MaskState* st,
+             int all_masks) {
+    const bool rows = axis == 0;
+    const GenPlan& g = rows ? pl->gx : pl->gy;
+    const int TC = rows ? pl->gtc_r : pl->gtc_c;
+    const int ntrans = rows ? pl->ny : pl->nx;
+    const long long tstride = rows ? pl->nx : 1, estride = rows ? 1 : pl->nx;
+    const T scale = (T)(1.0 / std::sqrt((double)g.L));
+    const dim3 grid((ntrans + TC - 1) / TC, batch);
+    gen_fft_kernel<T><<<grid, 256, rows ? pl->gsm_r : pl->gsm_c, pl->stream>>>(
+        (const cx<T>*)in, (cx<T>*)out, (const cx<T>*)(rows ? pl->gtwx : pl->gtwy), g, ntrans, tstride, estride,
+        (long long)pl->N, dir, scale, TC, st, all_masks);
+    CK(cudaGetLastError());
+    pl->launches++;
+    return PM_OK;
+}
+
+int gen_fft2(pm_plan* pl, const void* in, void* out, int dir, int batch, const MaskState* st = nullptr,
+             int all_masks = 1) {
+    if (pl->prec == PM_SINGLE) {
+        CKR(gen_axis<float>(pl, in, out, 0, dir, batch, st, all_masks));
+        return gen_axis<float>(pl, out, out, 1, dir, batch, st, all_masks);
+    }
+    CKR(gen_axis<double>(pl, in, out, 0, dir, batch, st, all_masks));
+    return gen_axis<double>(pl, out, out, 1, dir, batch, st, all_masks);
+}
+
+int gen_elem_blocks(const pm_plan* pl) {
+    return (int)std::max<long long>(1, std::min<long long>(((long long)pl->N + 1023) / 1024, 148));
+}
+
+GenSolveArgs gen_args(pm_plan* pl) {
+    const pm_params& prm = pl->s.prm;
+    GenSolveArgs g;
+    g.ctl.max_iters = prm.max_iters;
+    g.ctl.record_every = prm.record_every;
+    g.ctl.early_tol = prm.early_stop_tol;
+    g.ctl.t_lit = prm.t_lit;
+    g.ctl.t_dark = prm.t_dark;
+    g.st = pl->st;
+    g.hist = pl->hist;
+    g.hist_stride = pl->hist_cap;
+    g.part = pl->part;
+    g.ctr = pl->ctr;
+    g.nblk = gen_elem_blocks(pl);
+    g.n = (long long)pl->N;
+    return g;
+}
+
+template <typename T>
+int gen_replace(pm_plan* pl, int u_iter, int metrics_only, int all_masks) {
+    const dim3 grid(gen_elem_blocks(pl), pl->s.batch);
+    gen_replace_kernel<T><<<grid, 256, 0, pl->stream>>>((cx<T>*)pl->tmp, (const T*)pl->s.m, pl->thrm, pl->escale,
+                                                        gen_args(pl), u_iter, metrics_only, all_masks);
+    CK(cudaGetLastError());
+    pl->launches++;
+    return PM_OK;
+}
+
+// F^-1 replace_m F of the iterates (field -> tmp), with the metrics and
+// decision of iterate u_iter (0: none).
+int gen_half(pm_plan* pl, int u_iter, int metrics_only, int all_masks) {
+    const int B = pl->s.batch;
+    CKR(gen_fft2(pl, pl->field, pl->tmp, PM_FORWARD, B, pl->st, all_masks));
+    CKR(pl->prec == PM_SINGLE ? gen_replace<float>(pl, u_iter, metrics_only, all_masks)
+                              : gen_replace<double>(pl, u_iter, metrics_only, all_masks));
+    if (metrics_only) return PM_OK;
+    // inverse: columns then rows (any order gives the 2-D inverse)
+    return gen_fft2(pl, pl->tmp, pl->tmp, PM_INVERSE, B, pl->st, all_masks);
+}
+
+int gen_begin(pm_plan* pl) {
+    auto& s = pl->s;
+    const long long total = (long long)s.batch * pl->N;
+    if (!s.prm.init_complex) {
+        const int blocks = (int)std::min<long long>((total + 255) / 256, 4096);
+        if (pl->prec == PM_SINGLE)
+            gen_real_to_complex<float><<<blocks, 256, 0, pl->stream>>>((const float*)s.m, (float2*)pl->field, total);
+        else
+            gen_real_to_complex<double><<<blocks, 256, 0, pl->stream>>>((const double*)s.m, (double2*)pl->field,
+                                                                         total);
+        CK(cudaGetLastError());
+        pl->launches++;
+    }
+    return gen_fft2(pl, pl->field, pl->field, PM_INVERSE, s.batch, pl->st, 0);   // u0 = F^-1(m e^{i phi})
+}
+
+template <typename T>
+int gen_slm(pm_plan* pl, int it) {
+    const dim3 grid(gen_elem_blocks(pl), pl->s.batch);
+    gen_slm_kernel<T><<<grid, 256, 0, pl->stream>>>((const cx<T>*)pl->tmp, (cx<T>*)pl->field, (const T*)pl->s.p,
+                                                    pl->s.p_stride, pl->thrx, pl->st, (long long)pl->N, it);
+    CK(cudaGetLastError());
+    pl->launches++;
+    return PM_OK;
+}
+
+int gen_steps(pm_plan* pl, int n, bool probe) {
+    auto& s = pl->s;
+    bool any = false;
+    for (int i = 0; i < n && s.it < s.prm.max_iters; ++i) {
+        s.it += 1;
+        any = true;
+        CKR(gen_half(pl, s.it - 1, 0, 0));                                 // metrics of u_{it-1}
+        CKR(pl->prec == PM_SINGLE ? gen_slm<float>(pl, s.it) : gen_slm<double>(pl, s.it));   // u_it
+    }
+    if (any && probe) CKR(gen_half(pl, s.it, 1, 0));                       // gap + decision of u_it now
+    return PM_OK;
+}
+
+template <typename T>
+int gen_final_t(pm_plan* pl) {
+    auto& s = pl->s;
+    const dim3 grid(gen_elem_blocks(pl), s.batch);
+    gen_final_kernel<T><<<grid, 256, 0, pl->stream>>>((const cx<T>*)pl->tmp, (const T*)s.p, s.p_stride, pl->tolp,
+                                                      pl->st, (long long)pl->N, (cx<T>*)s.vstar, (cx<T>*)s.ustar,
+                                                      (double*)s.phases, (uint8_t*)s.levels);
+    CK(cudaGetLastError());
+    pl->launches++;
+    return PM_OK;
+}
+
+// v* = P_M u (every mask, decision of the last iterate if still pending),
+// then u*, the mask and the levels.
+int gen_finish(pm_plan* pl) {
+    CKR(gen_half(pl, pl->s.it, 0, 1));
+    return pl->prec == PM_SINGLE ? gen_final_t<float>(pl) : gen_final_t<double>(pl);
+}
+
 int fft2_dev(pm_plan* pl, const void* in, void* out, int dir, int batch) {
+    if (pl->generic) return gen_fft2(pl, in, out, dir, batch);
     return pl->prec == PM_SINGLE ? launch_fft2<float>(pl, in, out, dir, batch)
                                  : launch_fft2<double>(pl, in, out, dir, batch);
 }
@@ -726,6 +928,8 @@ int validate_params(const pm_params* prm, int batch) {
 int session_setup(pm_plan* pl, const void* d_p, const void* d_m, int batch, const pm_params* prm,
                   const double* tol_p, const double* tol_m, const double* energy) {
     CKR(validate_params(prm, batch));
+    if (pl->generic && prm->algorithm == PM_ALGO_RAAR)
+        return set_err(PM_ERR_UNSUPPORTED, "RAAR needs power-of-two grid sides (the mixed-radix path runs GS)");
     CKR(ensure_capacity(pl, batch, prm->max_iters));
     if (prm->algorithm == PM_ALGO_RAAR) CKR(ensure_raar(pl));
     auto& s = pl->s;
@@ -762,8 +966,7 @@ int session_setup(pm_plan* pl, const void* d_p, const void* d_m, int batch, cons
     CK(cudaMemcpyAsync(pl->thrm, s.h_thrm.data(), batch * sizeof(double), cudaMemcpyHostToDevice, pl->stream));
     CK(cudaMemcpyAsync(pl->thrms, s.h_thrms.data(), batch * sizeof(double), cudaMemcpyHostToDevice, pl->stream));
     CK(cudaMemcpyAsync(pl->energy, s.h_en.data(), batch * sizeof(double), cudaMemcpyHostToDevice, pl->stream));
-    if (pl->thrx)
-        CK(cudaMemcpyAsync(pl->thrx, s.h_thrx.data(), batch * sizeof(double), cudaMemcpyHostToDevice, pl->stream));
+    CK(cudaMemcpyAsync(pl->thrx, s.h_thrx.data(), batch * sizeof(double), cudaMemcpyHostToDevice, pl->stream));
     return PM_OK;
 }
 
@@ -811,6 +1014,7 @@ int enqueue_begin(pm_plan* pl) {
     CK(cudaMemsetAsync(pl->st, 0, s.batch * sizeof(MaskState), pl->stream));
     CK(cudaMemsetAsync(pl->hist, 0, (size_t)s.batch * pl->hist_cap * 4 * sizeof(double), pl->stream));
     CKR(enqueue_escale(pl));
+    if (pl->generic) return gen_begin(pl);
     if (persistent(pl)) return solve_launch(pl, 1, 1, 1, 0);
     CKR(col(pl, s.batch, s.prm.init_complex ? 1 : 0, 0));   // u0 column half
     CKR(row(pl, s.batch, kRowInit, 0));                     // u0 row half, w0 = RowFFT(u0)
@@ -823,6 +1027,7 @@ int enqueue_begin(pm_plan* pl) {
 // sweep, so its record is readable when the call returns.
 int enqueue_steps(pm_plan* pl, int n, bool probe = false) {
     auto& s = pl->s;
+    if (pl->generic) return gen_steps(pl, n, probe);
     const bool raar = s.prm.algorithm == PM_ALGO_RAAR;
     if (persistent(pl)) {
         const int first = s.it + 1, last = std::min(s.it + n, s.prm.max_iters);
@@ -842,6 +1047,7 @@ int enqueue_steps(pm_plan* pl, int n, bool probe = false) {
 }
 
 int enqueue_finish(pm_plan* pl) {
+    if (pl->generic) return gen_finish(pl);
     if (persistent(pl)) return solve_launch(pl, 0, 1, 1, 1);
     return final_pair(pl, pl->s.batch);
 }
@@ -965,10 +1171,17 @@ int pm_plan_create(int device, int n_x, int n_y, int precision, int max_batch, p
     *out = nullptr;
     if (precision != PM_SINGLE && precision != PM_DOUBLE)
         return set_err(PM_ERR_ARG, "precision must be 0 (single) or 1 (double)");
-    const int lgx = lg2_exact(n_x), lgy = lg2_exact(n_y);
-    if (lgx < 0 || lgy < 0 || lgx > kMaxLg || lgy > kMaxLg)
-        return set_err(PM_ERR_UNSUPPORTED, "grid " + std::to_string(n_x) + "x" + std::to_string(n_y) +
-                                               ": n_x and n_y must be powers of two in [1, 4096]");
+    int lgx = lg2_exact(n_x), lgy = lg2_exact(n_y);
+    GenPlan gx{}, gy{};
+    bool generic = false;
+    if (lgx < 0 || lgy < 0 || lgx > kMaxLg || lgy > kMaxLg) {
+        // mixed-radix path: every side a product of 2, 3, 5, 7, at most 4096
+        if (!gen_factor(n_x, &gx) || !gen_factor(n_y, &gy))
+            return set_err(PM_ERR_UNSUPPORTED, "grid " + std::to_string(n_x) + "x" + std::to_string(n_y) +
+                                                   ": n_x and n_y must be at most 4096 with prime factors 2, 3, 5, 7");
+        generic = true;
+        lgx = lgy = 0;                          // the power-of-two kernel sets are not used
+    }
     int ndev = 0;
     cudaError_t e = cudaGetDeviceCount(&ndev);
     if (e != cudaSuccess || ndev == 0) {
@@ -987,6 +1200,9 @@ int pm_plan_create(int device, int n_x, int n_y, int precision, int max_batch, p
     pl->N = (size_t)n_x * n_y;
     pl->csz = precision == PM_SINGLE ? sizeof(float2) : sizeof(double2);
     pl->rsz = precision == PM_SINGLE ? sizeof(float) : sizeof(double);
+    pl->generic = generic;
+    pl->gx = gx;
+    pl->gy = gy;
     pl->rc = row_config(pl);
     pl->cc = col_config(pl);
     auto fail = [&](int r) {
@@ -998,6 +1214,10 @@ int pm_plan_create(int device, int n_x, int n_y, int precision, int max_batch, p
     pl->own_stream = true;
     if (cudaEventCreate(&pl->ev0) != cudaSuccess || cudaEventCreate(&pl->ev1) != cudaSuccess)
         return fail(cuda_err(cudaGetLastError(), "cudaEventCreate"));
+    if (generic) {
+        int rg = gen_setup(pl);
+        if (rg != PM_OK) return fail(rg);
+    }
     // twiddle tables
     for (int axis = 0; axis < 2; ++axis) {
         const int lg = axis == 0 ? lgx : lgy;
@@ -1057,6 +1277,8 @@ int pm_plan_destroy(pm_plan* pl) {
     if (pl->tw_col_i && pl->tw_col_i != pl->tw_col) cudaFree(pl->tw_col_i);
     if (pl->tw_row) cudaFree(pl->tw_row);
     if (pl->tw_col) cudaFree(pl->tw_col);
+    if (pl->gtwx) cudaFree(pl->gtwx);
+    if (pl->gtwy) cudaFree(pl->gtwy);
     if (pl->red) cudaFree(pl->red);
     if (pl->bar) cudaFree(pl->bar);
     if (pl->stamps) cudaFree(pl->stamps);
@@ -1523,6 +1745,7 @@ int pm_solve_finish(pm_plan* pl, int abort, pm_result* res) {
 int pm_time_sweep(pm_plan* pl, int which, int batch, int reps, float* avg_ms) {
     CKR(check_plan(pl));
     if (!avg_ms || reps < 1 || batch < 1) return set_err(PM_ERR_ARG, "bad arguments");
+    if (pl->generic) return set_err(PM_ERR_UNSUPPORTED, "sweep timing exists for power-of-two grids only");
     std::lock_guard<std::mutex> lk(pl->mu);
     auto& s = pl->s;
     if (!s.p || !s.m || batch > pl->cap) return set_err(PM_ERR_ARG, "run a solve on this plan first");

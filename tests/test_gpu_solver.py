@@ -267,3 +267,44 @@ def test_acceptance_2_consistency_collapse():
     m = pm.FourierConstraint(pm.RealGrid(spec, np.abs(prov.forward(w).data)))
     r = pm.solve(c, m, pm.SolveConfig(max_iters=50, record_every=50), prov)
     assert r.final.gap <= math.sqrt(spec.n) * 100 * EPS
+
+
+@pytest.mark.parametrize("nx,ny,tag,K", [(800, 600, "single", 25), (60, 42, "double", 30), (100, 64, "double", 20)])
+def test_mixed_radix_solve_matches_oracle(nx, ny, tag, K):
+    """Non-power-of-two grids (the paper's 800x600 SLM) on the
+    mixed-radix path: GS against the oracle restatement of the reference."""
+    prec = pm.Precision.from_tag(tag)
+    p, m = make_problem(nx, 12, 7, n_y=ny)
+    spec = pm.GridSpec(nx, ny)
+    r = pm.solve(pm.SlmConstraint(pm.RealGrid(spec, p), prec), pm.FourierConstraint(pm.RealGrid(spec, m), prec),
+                 pm.SolveConfig(max_iters=K, precision=prec, record_every=5))
+    o = orc.solve(p, m, K, tag, record_every=5)
+    tol = 1e-10 if tag == "double" else 1e-4
+    assert r.iters_run == o["iters_run"]
+    assert orc.relative_l2(r.u_star.data, o["u_star"]) <= tol
+    assert orc.relative_l2(r.v_star.data, o["v_star"]) <= tol
+    h = np.array([(x.iter, x.gap, x.err_lit, x.err_dark) for x in r.history])
+    oh = np.array(o["records"])
+    np.testing.assert_array_equal(h[:, 0], oh[:, 0])
+    np.testing.assert_allclose(h[:, 1], oh[:, 1], rtol=1e-12 if tag == "double" else 1e-6)
+    np.testing.assert_allclose(h[:, 2:], oh[:, 2:], rtol=1e-6, atol=1e-9)
+
+
+def test_mixed_radix_early_stop_callbacks_and_batch():
+    p, m = make_problem(120, 6, 3, n_y=90)
+    spec = pm.GridSpec(120, 90)
+    c, mc = pm.SlmConstraint(pm.RealGrid(spec, p)), pm.FourierConstraint(pm.RealGrid(spec, m))
+    o = orc.solve(p, m, 300, "double", early_stop_tol=1e-6)
+    r = pm.solve(c, mc, pm.SolveConfig(max_iters=300, early_stop_tol=1e-6))
+    assert r.iters_run == o["iters_run"] < 300
+    assert orc.relative_l2(r.u_star.data, o["u_star"]) <= 1e-10
+    seen = []
+    rc = pm.solve(c, mc, pm.SolveConfig(max_iters=9, record_every=4), on_record=seen.append)
+    rn = pm.solve(c, mc, pm.SolveConfig(max_iters=9, record_every=4))
+    assert [x.iter for x in seen] == [1, 5, 9] and [x.gap for x in seen] == [x.gap for x in rn.history]
+    np.testing.assert_array_equal(rc.mask.phases, rn.mask.phases)
+    ms = np.stack([make_problem(120, 6, s, n_y=90)[1] for s in (3, 4)])
+    res = solve_stack(p, ms, pm.SolveConfig(max_iters=9, record_every=4))
+    np.testing.assert_array_equal(res.phases[0], rn.mask.phases)
+    with pytest.raises(NotImplementedError):
+        pm.solve(c, mc, pm.SolveConfig(max_iters=3, algorithm="raar"))

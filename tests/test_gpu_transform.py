@@ -10,6 +10,7 @@ import scipy.fft as sfft
 
 import paper_1302_0120_b200 as pm
 from conftest import golden, random_field
+from oracle import phasemask_oracle as orc
 from oracle.phasemask_oracle import naive_dft
 from paper_1302_0120_b200.grid import FOURIER_PLANE, SLM_PLANE
 
@@ -126,6 +127,24 @@ def test_batched_transform_matches_single(rng):
         np.testing.assert_array_equal(a, fft2(b))
 
 
-def test_non_power_of_two_is_not_implemented(rng):
-    with pytest.raises(NotImplementedError, match="powers of two"):
-        pm.FftProvider(pm.GridSpec(800, 600)).forward(pm.Field(pm.GridSpec(800, 600), np.zeros((600, 800))))
+def test_unsupported_prime_factor_is_not_implemented(rng):
+    with pytest.raises(NotImplementedError, match="prime factors 2, 3, 5, 7"):
+        pm.FftProvider(pm.GridSpec(22, 13)).forward(pm.Field(pm.GridSpec(22, 13), np.zeros((13, 22))))
+
+
+@pytest.mark.parametrize("nx,ny", [(800, 600), (6, 10), (15, 8), (49, 12), (1000, 90), (3, 1)])
+@pytest.mark.parametrize("tag", ["double", "single"])
+def test_mixed_radix_transform_matches_scipy(nx, ny, tag, rng):
+    """Sides with prime factors 2, 3, 5, 7 (the paper's 800x600 SLM) run the
+    mixed-radix path; unitary forward / inverse against scipy ortho."""
+    prec = pm.Precision.from_tag(tag)
+    spec = pm.GridSpec(nx, ny)
+    x = random_field(spec, rng, prec.complex_dtype)
+    prov = pm.FftProvider(spec, prec)
+    tol = 1e-12 if tag == "double" else 2e-6
+    fwd = prov.forward(pm.Field(spec, x)).data
+    assert orc.relative_l2(fwd, sfft.fft2(x.astype(np.complex128), norm="ortho")) <= tol
+    inv = prov.inverse(pm.Field(spec, fwd, FOURIER_PLANE)).data
+    assert orc.relative_l2(inv, x) <= tol
+    if nx * ny <= 4096:
+        assert np.abs(fwd - orc.naive_dft(x)).max() <= (1e-12 if tag == "double" else 1e-5)

@@ -62,7 +62,7 @@ def test_errors_without_gpu_are_loud():
 def test_invalid_arguments_rejected_before_device():
     lib = _lib.load()
     h = C.c_void_p()
-    assert lib.pm_plan_create(0, 100, 64, 0, 1, C.byref(h)) == _lib.PM_ERR_UNSUPPORTED
-    assert "powers of two" in _lib.last_error()
+    assert lib.pm_plan_create(0, 110, 64, 0, 1, C.byref(h)) == _lib.PM_ERR_UNSUPPORTED   # factor 11
+    assert "prime factors 2, 3, 5, 7" in _lib.last_error()
     assert lib.pm_plan_create(0, 64, 64, 7, 1, C.byref(h)) == _lib.PM_ERR_ARG
     assert lib.pm_plan_create(0, 8192, 64, 0, 1, C.byref(h)) == _lib.PM_ERR_UNSUPPORTED
