@@ -755,8 +755,15 @@ constexpr size_t kGenSmem = 96 * 1024;   // two [L][TC] buffers per CTA
 int gen_setup(pm_plan* pl) {
     CKR(gen_twiddles(pl->prec, pl->nx, &pl->gtwx));
     CKR(gen_twiddles(pl->prec, pl->ny, &pl->gtwy));
-    pl->gtc_r = (int)std::max<size_t>(1, std::min<size_t>(16, kGenSmem / (2 * pl->nx * pl->csz)));
-    pl->gtc_c = (int)std::max<size_t>(1, std::min<size_t>(16, kGenSmem / (2 * pl->ny * pl->csz)));
+    // transforms per CTA: a power of two, enough CTAs to cover the SMs,
+    // columns wide enough for >= 32-byte segments
+    auto tc_for = [&](int L, int ntrans, int want) {
+        int tc = want;
+        while (tc > 1 && (2 * (size_t)L * tc * pl->csz > kGenSmem || (ntrans + tc - 1) / tc < 148)) tc >>= 1;
+        return tc;
+    };
+    pl->gtc_r = tc_for(pl->nx, pl->ny, 4);
+    pl->gtc_c = tc_for(pl->ny, pl->nx, pl->csz == 8 ? 4 : 2);
     pl->gsm_r = 2 * (size_t)pl->nx * pl->gtc_r * pl->csz;
     pl->gsm_c = 2 * (size_t)pl->ny * pl->gtc_c * pl->csz;
     const size_t mx = std::max(pl->gsm_r, pl->gsm_c);
@@ -779,9 +786,11 @@ int gen_axis(pm_plan* pl, const void* in, void* out, int axis, int dir, int batc
     const long long tstride = rows ? pl->nx : 1, estride = rows ? 1 : pl->nx;
     const T scale = (T)(1.0 / std::sqrt((double)g.L));
     const dim3 grid((ntrans + TC - 1) / TC, batch);
+    int lgTC = 0;
+    while ((1 << lgTC) < TC) ++lgTC;
     gen_fft_kernel<T><<<grid, 256, rows ? pl->gsm_r : pl->gsm_c, pl->stream>>>(
         (const cx<T>*)in, (cx<T>*)out, (const cx<T>*)(rows ? pl->gtwx : pl->gtwy), g, ntrans, tstride, estride,
-        (long long)pl->N, dir, scale, TC, st, all_masks);
+        (long long)pl->N, dir, scale, lgTC, st, all_masks);
     CK(cudaGetLastError());
     pl->launches++;
     return PM_OK;

@@ -84,22 +84,28 @@ __device__ __forceinline__ void gen_dft(cx<T>* x) {
     }
 }
 
+// x / d for 0 <= x, d <= 2^20 without an integer division: the fp64
+// product is within 1e-12 of the quotient, far inside 1/d of the next integer.
+__device__ __forceinline__ int gen_div(int x, double inv_d) { return (int)((double)x * inv_d + 1e-9); }
+
 // One Stockham pass of radix R over the TC transforms held in `a`
-// ([L][TC] layout), into `b`. tw[k] = exp(-2 pi i k / L).
+// ([L][TC] layout, TC a power of two), into `b`. tw[k] = exp(-2 pi i k / L).
 template <typename T, int R>
 __device__ __forceinline__ void gen_pass(const cx<T>* a, cx<T>* b, const cx<T>* __restrict__ tw, int L, int Ns,
-                                         int TC, int dir) {
+                                         int lgTC, int dir) {
+    const int TC = 1 << lgTC;
     const int M = L / R;
-    const int step = L / (Ns * R);              // twiddle index step per (q * k)
+    const int step = L / (Ns * R);              // twiddle index step per (q * k); q * k * step < L
+    const double inv_ns = 1.0 / Ns;
     for (int idx = threadIdx.x; idx < M * TC; idx += blockDim.x) {
-        const int t = idx % TC, jb = idx / TC;
-        const int k = jb % Ns;
+        const int t = idx & (TC - 1), jb = idx >> lgTC;
+        const int g = gen_div(jb, inv_ns), k = jb - g * Ns;
         cx<T> x[R];
 #pragma unroll
         for (int q = 0; q < R; ++q) {
             cx<T> v = a[(jb + q * M) * TC + t];
             if (q > 0 && k > 0) {
-                const cx<T> w = __ldg(tw + (q * k * step) % L);
+                const cx<T> w = __ldg(tw + q * k * step);
                 const T ws = dir < 0 ? w.y : -w.y;
                 v = mk<T>(v.x * w.x - v.y * ws, v.x * ws + v.y * w.x);
             }
@@ -107,7 +113,7 @@ __device__ __forceinline__ void gen_pass(const cx<T>* a, cx<T>* b, const cx<T>* 
         }
         if (dir < 0) gen_dft<T, R, -1>(x);
         else gen_dft<T, R, +1>(x);
-        const int o = (jb / Ns) * Ns * R + k;
+        const int o = g * Ns * R + k;
 #pragma unroll
         for (int q = 0; q < R; ++q) b[(o + q * Ns) * TC + t] = x[q];
     }
@@ -118,8 +124,9 @@ __device__ __forceinline__ void gen_pass(const cx<T>* a, cx<T>* b, const cx<T>* 
 // bstride). Skips masks that are stopped (unless all_masks) or diverged.
 template <typename T>
 __global__ void gen_fft_kernel(const cx<T>* in, cx<T>* out, const cx<T>* __restrict__ tw, GenPlan gp, int ntrans,
-                               long long tstride, long long estride, long long bstride, int dir, T scale, int TC,
+                               long long tstride, long long estride, long long bstride, int dir, T scale, int lgTC,
                                const MaskState* st, int all_masks) {
+    const int TC = 1 << lgTC;
     extern __shared__ __align__(16) unsigned char smraw[];
     const int b = blockIdx.y;
     if (st && (st[b].done || (!all_masks && st[b].stop))) return;
@@ -131,28 +138,29 @@ __global__ void gen_fft_kernel(const cx<T>* in, cx<T>* out, const cx<T>* __restr
     const cx<T>* src = in + b * bstride;
     cx<T>* dst = out + b * bstride;
     const bool contig_e = estride == 1;          // rows: walk along n; columns: walk along t
+    const double inv_l = 1.0 / L;
     for (int idx = threadIdx.x; idx < L * TC; idx += blockDim.x) {
         int n, t;
-        if (contig_e) { t = idx / L; n = idx - t * L; }
-        else { n = idx / TC; t = idx - n * TC; }
+        if (contig_e) { t = gen_div(idx, inv_l); n = idx - t * L; }
+        else { n = idx >> lgTC; t = idx & (TC - 1); }
         A[n * TC + t] = t < tc ? src[(t0 + t) * tstride + n * estride] : mk<T>(T(0), T(0));
     }
     __syncthreads();
     for (int s = 0; s < gp.np; ++s) {
         switch (gp.radix[s]) {
-            case 2: gen_pass<T, 2>(A, B, tw, L, gp.ns[s], TC, dir); break;
-            case 3: gen_pass<T, 3>(A, B, tw, L, gp.ns[s], TC, dir); break;
-            case 4: gen_pass<T, 4>(A, B, tw, L, gp.ns[s], TC, dir); break;
-            case 5: gen_pass<T, 5>(A, B, tw, L, gp.ns[s], TC, dir); break;
-            default: gen_pass<T, 7>(A, B, tw, L, gp.ns[s], TC, dir); break;
+            case 2: gen_pass<T, 2>(A, B, tw, L, gp.ns[s], lgTC, dir); break;
+            case 3: gen_pass<T, 3>(A, B, tw, L, gp.ns[s], lgTC, dir); break;
+            case 4: gen_pass<T, 4>(A, B, tw, L, gp.ns[s], lgTC, dir); break;
+            case 5: gen_pass<T, 5>(A, B, tw, L, gp.ns[s], lgTC, dir); break;
+            default: gen_pass<T, 7>(A, B, tw, L, gp.ns[s], lgTC, dir); break;
         }
         __syncthreads();
         cx<T>* tmp = A; A = B; B = tmp;
     }
     for (int idx = threadIdx.x; idx < L * TC; idx += blockDim.x) {
         int n, t;
-        if (contig_e) { t = idx / L; n = idx - t * L; }
-        else { n = idx / TC; t = idx - n * TC; }
+        if (contig_e) { t = gen_div(idx, inv_l); n = idx - t * L; }
+        else { n = idx >> lgTC; t = idx & (TC - 1); }
         if (t < tc) dst[(t0 + t) * tstride + n * estride] = cscale(A[n * TC + t], scale);
     }
 }
