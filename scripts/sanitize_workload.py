@@ -1,0 +1,42 @@
+"""Small workload for compute-sanitizer (memcheck / racecheck / synccheck):
+every kernel family once — stand-alone transforms, projections, the sweep
+path, the persistent GS and RAAR kernels, the mixed-radix path, batches."""
+import sys
+sys.path.insert(0, '/root/repo')
+import numpy as np
+import paper_1302_0120_b200 as pm
+from paper_1302_0120_b200.batch import solve_stack
+from paper_1302_0120_b200.patterns import make_problem
+from paper_1302_0120_b200.projections import project_fourier
+
+
+def run(nx, ny, tag, algo="gs", K=3, path=0, batch=1):
+    prec = pm.Precision.from_tag(tag)
+    p, m = make_problem(nx, 4 if nx < 128 else 8, 7, n_y=ny)
+    spec = pm.GridSpec(nx, ny)
+    plan = pm.transform.get_plan(spec, prec)
+    plan.set_path(path)
+    cfg = pm.SolveConfig(max_iters=K, precision=prec, algorithm=algo, record_every=1)
+    if batch == 1:
+        r = pm.solve(pm.SlmConstraint(pm.RealGrid(spec, p), prec), pm.FourierConstraint(pm.RealGrid(spec, m), prec), cfg)
+        seen = []
+        pm.solve(pm.SlmConstraint(pm.RealGrid(spec, p), prec), pm.FourierConstraint(pm.RealGrid(spec, m), prec), cfg,
+                 on_record=seen.append)
+        u = pm.Field(spec, r.u_star.data)
+        project_fourier(u, pm.FourierConstraint(pm.RealGrid(spec, m), prec), pm.FftProvider(spec, prec))
+    else:
+        ms = np.stack([make_problem(nx, 4, s, n_y=ny)[1] for s in range(batch)])
+        solve_stack(p.astype(prec.float_dtype), ms.astype(prec.float_dtype), cfg, levels=True)
+    plan.set_path(0)
+    print("ok", nx, ny, tag, algo, path, batch, flush=True)
+
+
+run(64, 64, "double")
+run(64, 32, "single")
+run(128, 128, "single", path=1)
+run(128, 128, "double", path=2)
+run(128, 128, "single", algo="raar", path=1)
+run(64, 64, "double", algo="raar")
+run(128, 128, "single", batch=3)
+run(60, 42, "double")
+run(30, 40, "single", batch=2)
