@@ -16,7 +16,9 @@
  *  - Real inputs (p, m) are in the plan precision's float type.
  *  - Transforms are unitary (1/sqrt(N) split over both directions), standard
  *    unshifted frequency order (src/transform.py:1-7).
- *  - n_x and n_y must be powers of two in [1, 4096].
+ *  - n_x and n_y are at most 4096 with prime factors 2, 3, 5, 7; powers of
+ *    two run the fused register-resident kernels, other sides the
+ *    mixed-radix path (GS only).
  *  - Every function returns 0 on success or a negative PM_ERR_* code;
  *    pm_last_error() returns the calling thread's last message.
  *  - "_device" variants take device pointers on the plan's device and run
@@ -192,7 +194,10 @@ typedef struct pm_result {
  * and phases_of (:201-206); a batch replaces the sequential loop of
  * PhaseMaskTransformer.transform (src/estimator.py:85-93).
  *   p: real grid(s); m: real target moduli, batch grids;
- *   zero_tol_p / zero_tol_m: per-mask thresholds (1024*eps*max), host arrays;
+ *   zero_tol_p / zero_tol_m: per-mask thresholds (1024*eps*max), host arrays,
+ *           or both NULL to derive them on the device from p and m (an
+ *           identically zero p / all-dark m then fails with PM_ERR_ARG and
+ *           the reference's message, after the launch);
  *   energy: per-mask sum(m^2) in fp64 (reconstructed-intensity scale), or
  *           NULL to reduce it on the device from the (precision-cast) m;
  *   m_init: complex starts when params->init_complex, else NULL.

@@ -188,6 +188,80 @@ __global__ void escale_kernel(const double* part, int nb, int per_mask, double* 
     escale[b] = energy[b] / s;
 }
 
+// fp32 zero-branch decision on s = |u|^2: the least float s with
+// sqrtf(s) >= (float)tol (the host's fp32_sq_threshold, bit for bit).
+__device__ double fp32_sq_threshold_dev(double tol) {
+    const float tf = (float)tol;
+    if (!(tf > 0.f)) return 0.0;
+    float s = __fmul_rn(tf, tf);
+    while (s > 0.f && __fsqrt_rn(s) >= tf) s = nextafterf(s, 0.f);
+    while (__fsqrt_rn(s) < tf) s = nextafterf(s, INFINITY);
+    return (double)s;
+}
+
+// Per-mask zero tolerances 1024 eps max (src/grid.py:21,33-34) and the
+// decision thresholds derived from them, from the device-resident p and m
+// (the host's session_setup formulas); an identically zero p or all-dark m
+// marks the mask done and is reported as the reference's ValueError.
+// Stage 1: block maxima over fixed chunks (max is order-independent).
+template <typename T>
+__global__ void tol_max_kernel(const T* p, long long p_stride, const T* m, long long n, long long chunk,
+                               double* part, int nb) {
+    const int b = blockIdx.y;
+    const T* pb = p + b * p_stride;
+    const T* mb = m + b * n;
+    const long long lo = blockIdx.x * chunk, hi = min(n, lo + chunk);
+    T pmx = T(0), mmx = T(0);
+    for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+        pmx = max(pmx, pb[i]);
+        mmx = max(mmx, mb[i]);
+    }
+    __shared__ T sp[32], sm2[32];
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+        pmx = max(pmx, __shfl_xor_sync(0xffffffffu, pmx, o));
+        mmx = max(mmx, __shfl_xor_sync(0xffffffffu, mmx, o));
+    }
+    if ((threadIdx.x & 31) == 0) { sp[threadIdx.x >> 5] = pmx; sm2[threadIdx.x >> 5] = mmx; }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) { pmx = max(pmx, sp[w]); mmx = max(mmx, sm2[w]); }
+    part[((size_t)b * nb + blockIdx.x) * 2 + 0] = (double)pmx;
+    part[((size_t)b * nb + blockIdx.x) * 2 + 1] = (double)mmx;
+}
+
+// Stage 2: one thread per mask.
+__global__ void tol_final_kernel(const double* part, int nb, int batch, int single, double nn, double* tolp,
+                                 double* thrp, double* thrm, double* thrms, double* thrx, MaskState* st) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= batch) return;
+    double pmx = 0.0, mmx = 0.0;
+    for (int i = 0; i < nb; ++i) {
+        pmx = fmax(pmx, part[((size_t)b * nb + i) * 2 + 0]);
+        mmx = fmax(mmx, part[((size_t)b * nb + i) * 2 + 1]);
+    }
+    const double eps = single ? 1.1920928955078125e-07 : 2.220446049250313e-16;
+    const double tp = 1024.0 * eps * pmx, tm = 1024.0 * eps * mmx;
+    tolp[b] = tp;
+    if (single) {
+        const double qp = fp32_sq_threshold_dev(tp), qm = fp32_sq_threshold_dev(tm);
+        thrp[b] = qp * nn;
+        thrm[b] = qm;
+        thrms[b] = qm * nn;
+        thrx[b] = qp;
+    } else {
+        thrp[b] = tp * sqrt(nn);
+        thrm[b] = tm;
+        thrms[b] = tm * sqrt(nn);
+        thrx[b] = tp;
+    }
+    const int z = (pmx == 0.0 ? 1 : 0) | (mmx == 0.0 ? 2 : 0);
+    if (z) {
+        st[b].zero = z;
+        st[b].done = 1;
+    }
+}
+
 // Host abort (should_abort -> True): the current iterate becomes the last.
 __global__ void force_stop_kernel(MaskState* st, int batch, int it) {
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
@@ -359,6 +433,7 @@ struct pm_plan {
         void* vstar = nullptr;
         std::vector<double> h_tolp, h_thrp, h_thrm, h_thrms, h_en, h_thrx;
         bool energy_on_device = false;
+        bool tol_on_device = false;
     } s;
 };
 
@@ -933,6 +1008,18 @@ int validate_params(const pm_params* prm, int batch) {
     return PM_OK;
 }
 
+int ensure_red(pm_plan* pl, int nb) {
+    if (nb + 1 <= pl->red_cap) return PM_OK;
+    CK(cudaStreamSynchronize(pl->stream));
+    drop_graphs(pl);                  // captured graphs hold the old pointer
+    if (pl->red) cudaFree(pl->red);
+    pl->red = nullptr;
+    CK(cudaMalloc((void**)&pl->red, (nb + 1) * sizeof(double)));
+    pl->red_cap = nb + 1;
+    return PM_OK;
+}
+constexpr int kTolBlocks = 64;
+
 // Upload per-mask scalars and reset state; point the session at p/m.
 int session_setup(pm_plan* pl, const void* d_p, const void* d_m, int batch, const pm_params* prm,
                   const double* tol_p, const double* tol_m, const double* energy) {
@@ -951,11 +1038,20 @@ int session_setup(pm_plan* pl, const void* d_p, const void* d_m, int batch, cons
     s.p_stride = prm->p_per_mask ? (long long)pl->N : 0;
     // pinned-free small uploads: stage in the session's host vectors, which
     // must outlive the async copies -> keep them in the plan
+    s.h_en.resize(batch);
+    for (int b = 0; b < batch; ++b) s.h_en[b] = energy ? energy[b] : 0.0;
+    s.energy_on_device = energy == nullptr;
+    CK(cudaMemcpyAsync(pl->energy, s.h_en.data(), batch * sizeof(double), cudaMemcpyHostToDevice, pl->stream));
+    if (!tol_p) {
+        // tolerances from the device-resident p and m (no host pass over them);
+        // their partial maxima live in `red` (sized here, outside any capture)
+        s.tol_on_device = true;
+        return ensure_red(pl, 2 * kTolBlocks * batch);
+    }
     s.h_tolp.resize(batch);
     s.h_thrp.resize(batch);
     s.h_thrm.resize(batch);
     s.h_thrms.resize(batch);
-    s.h_en.resize(batch);
     s.h_thrx.resize(batch);
     for (int b = 0; b < batch; ++b) {
         const double tp = tol_p[prm->p_per_mask ? b : 0];
@@ -966,16 +1062,37 @@ int session_setup(pm_plan* pl, const void* d_p, const void* d_m, int batch, cons
         s.h_thrm[b] = pl->prec == PM_SINGLE ? fp32_sq_threshold(tol_m[b]) : tol_m[b];
         // on S^-1 u^ (exact when N is a power of 4, the only case it is used)
         s.h_thrms[b] = pl->prec == PM_SINGLE ? s.h_thrm[b] * (double)pl->N : s.h_thrm[b] * std::sqrt((double)pl->N);
-        s.h_en[b] = energy ? energy[b] : 0.0;
         s.h_thrx[b] = pl->prec == PM_SINGLE ? fp32_sq_threshold(tp) : tp;   // RAAR P_S on true scale
     }
-    s.energy_on_device = energy == nullptr;
     CK(cudaMemcpyAsync(pl->tolp, s.h_tolp.data(), batch * sizeof(double), cudaMemcpyHostToDevice, pl->stream));
     CK(cudaMemcpyAsync(pl->thrp, s.h_thrp.data(), batch * sizeof(double), cudaMemcpyHostToDevice, pl->stream));
     CK(cudaMemcpyAsync(pl->thrm, s.h_thrm.data(), batch * sizeof(double), cudaMemcpyHostToDevice, pl->stream));
     CK(cudaMemcpyAsync(pl->thrms, s.h_thrms.data(), batch * sizeof(double), cudaMemcpyHostToDevice, pl->stream));
-    CK(cudaMemcpyAsync(pl->energy, s.h_en.data(), batch * sizeof(double), cudaMemcpyHostToDevice, pl->stream));
     CK(cudaMemcpyAsync(pl->thrx, s.h_thrx.data(), batch * sizeof(double), cudaMemcpyHostToDevice, pl->stream));
+    return PM_OK;
+}
+
+// Device-side tolerances (after the mask state is cleared, before the solve).
+
+int enqueue_tolerances(pm_plan* pl) {
+    auto& s = pl->s;
+    if (!s.tol_on_device) return PM_OK;
+    const int single = pl->prec == PM_SINGLE;
+    const long long n = (long long)pl->N;
+    const int nb = (int)std::min<long long>(kTolBlocks, (n + 255) / 256);
+    const long long chunk = (n + nb - 1) / nb;
+    const dim3 grid(nb, s.batch);
+    if (single)
+        tol_max_kernel<float><<<grid, 256, 0, pl->stream>>>((const float*)s.p, s.p_stride, (const float*)s.m, n,
+                                                            chunk, pl->red, nb);
+    else
+        tol_max_kernel<double><<<grid, 256, 0, pl->stream>>>((const double*)s.p, s.p_stride, (const double*)s.m, n,
+                                                             chunk, pl->red, nb);
+    tol_final_kernel<<<(s.batch + 127) / 128, 128, 0, pl->stream>>>(pl->red, nb, s.batch, single, (double)pl->N,
+                                                                     pl->tolp, pl->thrp, pl->thrm, pl->thrms,
+                                                                     pl->thrx, pl->st);
+    CK(cudaGetLastError());
+    pl->launches += 2;
     return PM_OK;
 }
 
@@ -1022,6 +1139,7 @@ int enqueue_begin(pm_plan* pl) {
     auto& s = pl->s;
     CK(cudaMemsetAsync(pl->st, 0, s.batch * sizeof(MaskState), pl->stream));
     CK(cudaMemsetAsync(pl->hist, 0, (size_t)s.batch * pl->hist_cap * 4 * sizeof(double), pl->stream));
+    CKR(enqueue_tolerances(pl));
     CKR(enqueue_escale(pl));
     if (pl->generic) return gen_begin(pl);
     if (persistent(pl)) return solve_launch(pl, 1, 1, 1, 0);
@@ -1064,10 +1182,10 @@ int enqueue_finish(pm_plan* pl) {
 std::string graph_key(const pm_plan* pl) {
     const auto& s = pl->s;
     char buf[512];
-    snprintf(buf, sizeof buf, "%d|%d|%d|%d|%a|%a|%a|%d|%d|%a|%p|%p|%lld|%p|%p|%p|%p", s.batch,
+    snprintf(buf, sizeof buf, "%d|%d|%d|%d|%a|%a|%a|%d|%d|%a|%p|%p|%lld|%p|%p|%p|%p|%d", s.batch,
              s.prm.max_iters, s.prm.record_every, s.prm.init_complex, s.prm.early_stop_tol,
              s.prm.t_lit, s.prm.t_dark, s.prm.p_per_mask, s.prm.algorithm, s.prm.beta, s.p, s.m,
-             s.p_stride, s.phases, s.levels, s.ustar, s.vstar);
+             s.p_stride, s.phases, s.levels, s.ustar, s.vstar, (int)s.tol_on_device);
     return buf;
 }
 
@@ -1079,6 +1197,7 @@ int enqueue_full_solve(pm_plan* pl) {
         // one cooperative launch: initial iterate, all iterations, final pair
         CK(cudaMemsetAsync(pl->st, 0, s.batch * sizeof(MaskState), pl->stream));
         CK(cudaMemsetAsync(pl->hist, 0, (size_t)s.batch * pl->hist_cap * 4 * sizeof(double), pl->stream));
+        CKR(enqueue_tolerances(pl));
         CKR(enqueue_escale(pl));
         s.it = s.prm.max_iters;
         return solve_launch(pl, 1, 1, s.prm.max_iters + 1, 1);
@@ -1119,7 +1238,7 @@ int enqueue_full_solve(pm_plan* pl) {
 
 // Copy history / state back and fill the host-side result fields.
 int read_records(pm_plan* pl, int first, int last, double* gap, double* lit, double* dark,
-                 int* iters, int* diverged, int* aborted = nullptr) {
+                 int* iters, int* diverged, int* aborted = nullptr, int* zero = nullptr) {
     auto& s = pl->s;
     const int B = s.batch, K = s.prm.max_iters;
     std::vector<MaskState> st(B);
@@ -1131,7 +1250,9 @@ int read_records(pm_plan* pl, int first, int last, double* gap, double* lit, dou
                            pl->stream));
     }
     CK(cudaStreamSynchronize(pl->stream));
+    if (zero) *zero = 0;
     for (int b = 0; b < B; ++b) {
+        if (zero) *zero |= st[b].zero;
         if (iters) iters[b] = st[b].iters_run;
         if (diverged) diverged[b] = st[b].diverged;
         if (aborted) aborted[b] = st[b].aborted;
@@ -1146,6 +1267,14 @@ int read_records(pm_plan* pl, int first, int last, double* gap, double* lit, dou
             }
         }
     }
+    return PM_OK;
+}
+
+// The reference's validation messages (src/solver.py:122-125) for masks the
+// device found identically zero.
+int zero_error(int z) {
+    if (z & 1) return set_err(PM_ERR_ARG, "SLM amplitude is identically zero");
+    if (z & 2) return set_err(PM_ERR_ARG, "target pattern is identically zero (all dark)");
     return PM_OK;
 }
 
@@ -1435,14 +1564,6 @@ int pm_project_fourier(pm_plan* pl, const void* u, const void* m, double zero_to
     return PM_OK;
 }
 
-static int ensure_red(pm_plan* pl, int nb) {
-    if (nb + 1 <= pl->red_cap) return PM_OK;
-    if (pl->red) cudaFree(pl->red);
-    pl->red = nullptr;
-    CK(cudaMalloc((void**)&pl->red, (nb + 1) * sizeof(double)));
-    pl->red_cap = nb + 1;
-    return PM_OK;
-}
 
 static void reduce_grid(long long n, int* nb, long long* chunk) {
     *nb = (int)std::max<long long>(1, std::min<long long>(1024, (n + 4095) / 4096));
@@ -1591,7 +1712,7 @@ int pm_phases(int device, const void* u, long long count, int precision, double 
 static int solve_core(pm_plan* pl, const void* d_p, const void* d_m, const void* d_init, int batch,
                       const pm_params* prm, const double* tol_p, const double* tol_m,
                       const double* energy, pm_result* res, bool host_io) {
-    if (!tol_p || !tol_m) return set_err(PM_ERR_ARG, "null tolerance arrays");
+    if (!tol_p != !tol_m) return set_err(PM_ERR_ARG, "tolerance arrays: pass both or neither");
     CKR(session_setup(pl, d_p, d_m, batch, prm, tol_p, tol_m, energy));
     auto& s = pl->s;
     const size_t N = pl->N;
@@ -1627,14 +1748,16 @@ static int solve_core(pm_plan* pl, const void* d_p, const void* d_m, const void*
             CK(cudaMemcpyAsync(res->v_star, pl->vstar, batch * N * pl->csz, cudaMemcpyDeviceToHost, pl->stream));
     }
     std::vector<int> iters(batch), div(batch);
+    int zero = 0;
     CKR(read_records(pl, 1, prm->max_iters, res ? res->gap : nullptr, res ? res->err_lit : nullptr,
-                     res ? res->err_dark : nullptr, iters.data(), div.data()));
+                     res ? res->err_dark : nullptr, iters.data(), div.data(), nullptr, &zero));
     if (res) {
         if (res->iters_run) std::copy(iters.begin(), iters.end(), res->iters_run);
         if (res->diverged_iter) std::copy(div.begin(), div.end(), res->diverged_iter);
         if (res->device_ms) CK(cudaEventElapsedTime(res->device_ms, pl->ev0, pl->ev1));
     }
     s.active = false;
+    CKR(zero_error(zero));
     if (any_diverged(div)) return set_err(PM_ERR_DIVERGED, "non-finite values during the iteration");
     return PM_OK;
 }
@@ -1666,7 +1789,7 @@ int pm_solve_device(pm_plan* pl, const void* d_p, const void* d_m, const void* d
 int pm_solve_begin(pm_plan* pl, const void* p, const void* m, const void* m_init, int batch,
                    const pm_params* prm, const double* tol_p, const double* tol_m, const double* energy) {
     CKR(check_plan(pl));
-    if (!p || !m || !tol_p || !tol_m) return set_err(PM_ERR_ARG, "null input");
+    if (!p || !m || !tol_p != !tol_m) return set_err(PM_ERR_ARG, "null input");
     CKR(validate_params(prm, batch));
     std::lock_guard<std::mutex> lk(pl->mu);
     CKR(ensure_capacity(pl, batch, prm->max_iters));
@@ -1738,14 +1861,16 @@ int pm_solve_finish(pm_plan* pl, int abort, pm_result* res) {
             CK(cudaMemcpyAsync(res->v_star, pl->vstar, batch * N * pl->csz, cudaMemcpyDeviceToHost, pl->stream));
     }
     std::vector<int> iters(batch), div(batch);
+    int zero = 0;
     CKR(read_records(pl, 1, s.prm.max_iters, res ? res->gap : nullptr, res ? res->err_lit : nullptr,
-                     res ? res->err_dark : nullptr, iters.data(), div.data()));
+                     res ? res->err_dark : nullptr, iters.data(), div.data(), nullptr, &zero));
     if (res) {
         if (res->iters_run) std::copy(iters.begin(), iters.end(), res->iters_run);
         if (res->diverged_iter) std::copy(div.begin(), div.end(), res->diverged_iter);
         if (res->device_ms) CK(cudaEventElapsedTime(res->device_ms, pl->ev0, pl->ev1));
     }
     s.active = false;
+    CKR(zero_error(zero));
     if (any_diverged(div)) return set_err(PM_ERR_DIVERGED, "non-finite values during the iteration");
     return PM_OK;
 }

@@ -55,7 +55,7 @@ struct MaskState {
     int n_records;
     double prev_gap;
     int decided;     // last iteration whose record / stop decision is taken
-    int pad_;
+    int zero;        // device-side validation: 1 = p identically zero, 2 = m all dark
     double pend_lit, pend_dark;   // RAAR, sweep path: physical error of the last column sweep's iterate
 };
 

@@ -308,3 +308,24 @@ def test_mixed_radix_early_stop_callbacks_and_batch():
     np.testing.assert_array_equal(res.phases[0], rn.mask.phases)
     with pytest.raises(NotImplementedError):
         pm.solve(c, mc, pm.SolveConfig(max_iters=3, algorithm="raar"))
+
+
+def test_batch_device_tolerances_match_host_and_reject_zero_inputs():
+    """solve_stack derives the zero tolerances on the device; results equal a
+    solve with host-computed tolerances bitwise, and identically zero inputs
+    raise the reference's messages (src/solver.py:122-125)."""
+    for tag in ("single", "double"):
+        prec = pm.Precision.from_tag(tag)
+        p, m = make_problem(256, 8, 7)
+        spec = pm.GridSpec(256, 256)
+        cfg = pm.SolveConfig(max_iters=15, precision=prec, record_every=5)
+        r = pm.solve(pm.SlmConstraint(pm.RealGrid(spec, p), prec), pm.FourierConstraint(pm.RealGrid(spec, m), prec), cfg)
+        res = solve_stack(p.astype(prec.float_dtype), m[None].astype(prec.float_dtype), cfg)
+        np.testing.assert_array_equal(res.phases[0], r.mask.phases)
+        assert [x.gap for x in r.history] == list(res.gap[0][~np.isnan(res.gap[0])])
+    p, m = make_problem(128, 4, 3)
+    ms = np.stack([m, np.zeros_like(m)])
+    with pytest.raises(ValueError, match="all dark"):
+        solve_stack(p, ms, pm.SolveConfig(max_iters=3))
+    with pytest.raises(ValueError, match="identically zero"):
+        solve_stack(np.zeros_like(p), m[None], pm.SolveConfig(max_iters=3))
