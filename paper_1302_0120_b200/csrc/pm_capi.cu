@@ -4,6 +4,7 @@
 // stand-alone transform / projection / reduction entry points and the
 // measurement helpers used by bench.py.
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <cmath>
@@ -395,6 +396,9 @@ struct pm_plan {
     void* gtwy = nullptr;
     int gtc_r = 1, gtc_c = 1;         // transforms per CTA
     size_t gsm_r = 0, gsm_c = 0;      // their shared memory
+    // TMA maps of the persistent column phase (pm_kernels.cuh col_phase)
+    CUtensorMap tm_field{}, tm_field2{}, tm_m{};
+    bool tm_field_ok = false, tm_field2_ok = false, tm_m_ok = false;
     MaskState* st = nullptr;          // cap
     double* hist = nullptr;           // cap * hist_cap * 4
     double* part = nullptr;           // column partial sums, 2 (parity) * cap * nb * 3
@@ -413,6 +417,7 @@ struct pm_plan {
     GridBar* bar = nullptr;           // grid barrier of the persistent kernel
     unsigned long long* stamps = nullptr;  // optional phase timestamps (pm_debug_phase_stamps)
     int solve_grid = 0;               // CTAs of the persistent kernel (0: not available)
+    int solve_grid_tma = 0;           // CTAs of its TMA variant (0: not available)
     int path = 0;                     // 0 auto, 1 persistent, 2 sweep graph
     RowCfg rc{};
     ColCfg cc{};
@@ -490,6 +495,46 @@ void drop_graphs(pm_plan* pl) {
     pl->graphs.clear();
 }
 
+// ------------------------------------------------------------ TMA maps
+PFN_cuTensorMapEncodeTiled_v12000 tma_encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = []() -> PFN_cuTensorMapEncodeTiled_v12000 {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
+        return (PFN_cuTensorMapEncodeTiled_v12000)f;
+    }();
+    return fn;
+}
+
+// Columns per task of the persistent kernel (its CTA over the column transform).
+int solve_cols(const pm_plan* pl) {
+    const KernelSet& k = kset(pl->prec, pl->lgy);
+    return std::max(1, k.solve_threads / std::max(1, k.col.TG));
+}
+
+// [depth][n_y][width] elements of `esize` bytes, boxes [1][min(256, n_y)][box_w].
+bool tma_encode(CUtensorMap* map, void* base, int single, long long width, int n_y, int depth, int box_w) {
+    auto fn = tma_encode_fn();
+    if (!fn || !base || ((uintptr_t)base & 15)) return false;
+    const size_t esz = single ? 4 : 8;
+    cuuint64_t dims[3] = {(cuuint64_t)width, (cuuint64_t)n_y, (cuuint64_t)std::max(depth, 1)};
+    cuuint64_t strides[2] = {(cuuint64_t)(width * esz), (cuuint64_t)(width * esz * n_y)};
+    cuuint32_t box[3] = {(cuuint32_t)box_w, (cuuint32_t)std::min(256, n_y), 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    if ((box_w * esz) % 16 != 0 || box_w > 256 || strides[0] % 16 != 0) return false;
+    CUresult r = fn(map, single ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims,
+                    strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+// m box width: the columns of a task, at least 16 bytes.
+int tma_m_box(const pm_plan* pl) { return std::max(solve_cols(pl), (int)(16 / pl->rsz)); }
+
 int ensure_capacity(pm_plan* pl, int batch, int max_iters) {
     if (batch <= pl->cap && max_iters <= pl->hist_cap) return PM_OK;
     const int cap = std::max(batch, pl->cap);
@@ -519,6 +564,9 @@ int ensure_capacity(pm_plan* pl, int batch, int max_iters) {
     CK(cudaMemsetAsync(pl->st, 0, cap * sizeof(MaskState), pl->stream));
     pl->cap = cap;
     pl->hist_cap = hcap;
+    pl->tm_field_ok = !pl->generic && tma_encode(&pl->tm_field, pl->field, pl->prec == PM_SINGLE, 2LL * pl->nx,
+                                                 pl->ny, cap, 2 * solve_cols(pl));
+    pl->tm_field2_ok = false;
     return PM_OK;
 }
 
@@ -548,6 +596,8 @@ int ensure_raar(pm_plan* pl) {
     CK(cudaMalloc(&pl->xbuf, n * pl->csz));
     CK(cudaMalloc((void**)&pl->rpart, (size_t)pl->cap * pl->ny * row_wpr(pl) * 2 * sizeof(double)));
     pl->raar_cap = pl->cap;
+    pl->tm_field2_ok = tma_encode(&pl->tm_field2, pl->field2, pl->prec == PM_SINGLE, 2LL * pl->nx, pl->ny, pl->cap,
+                                  2 * solve_cols(pl));
     return PM_OK;
 }
 
@@ -721,11 +771,27 @@ int launch_solve(pm_plan* pl, int do_init, int it_begin, int it_end, int do_fina
     a.init_mode = pl->s.prm.init_complex ? 1 : 0;
     a.do_probe = do_probe;
     a.stamps = pl->stamps;
+    {
+        static const bool off = getenv("PM_NO_TMA") != nullptr;
+        const bool raar = pl->s.prm.algorithm == PM_ALGO_RAAR;
+        const bool in_ok = raar ? pl->tm_field2_ok : pl->tm_field_ok;
+        a.tma = (!off && in_ok && pl->tm_m_ok) ? 1 : 0;
+        a.tm_in = raar ? pl->tm_field2 : pl->tm_field;
+        a.tm_m = pl->tm_m;
+    }
+    // the TMA variant when CTAs get several column tasks per phase (batches):
+    // its tiles stream the next task in while one computes
+    const bool raar = pl->s.prm.algorithm == PM_ALGO_RAAR;
+    const long long col_tasks = (long long)pl->s.batch * (pl->nx / solve_cols(pl));
+    const bool use_tma = a.tma && pl->solve_grid_tma > 0 && col_tasks >= 2LL * pl->solve_grid_tma;
+    a.tma = use_tma ? 1 : 0;
+    const void* fn = use_tma ? (raar ? k.solve_raar_tma : k.solve_tma) : (raar ? k.solve_raar : k.solve);
     void* args[] = {&a};
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(pl->solve_grid);
+    cfg.gridDim = dim3(use_tma ? pl->solve_grid_tma : pl->solve_grid);
     cfg.blockDim = dim3(k.solve_threads);
-    cfg.dynamicSmemBytes = (size_t)(pl->s.prm.algorithm == PM_ALGO_RAAR ? k.solve_smem_raar : k.solve_smem);
+    cfg.dynamicSmemBytes = (size_t)(use_tma ? (raar ? k.solve_smem_raar_tma : k.solve_smem_tma)
+                                            : (raar ? k.solve_smem_raar : k.solve_smem));
     cfg.stream = pl->stream;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeCooperative;
@@ -733,7 +799,7 @@ int launch_solve(pm_plan* pl, int do_init, int it_begin, int it_end, int do_fina
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     CK(cudaMemsetAsync(pl->bar, 0, sizeof(GridBar), pl->stream));
-    CK(cudaLaunchKernelExC(&cfg, pl->s.prm.algorithm == PM_ALGO_RAAR ? k.solve_raar : k.solve, args));
+    CK(cudaLaunchKernelExC(&cfg, fn, args));
     pl->launches++;
     return PM_OK;
 }
@@ -1036,6 +1102,8 @@ int session_setup(pm_plan* pl, const void* d_p, const void* d_m, int batch, cons
     s.p = d_p;
     s.m = d_m;
     s.p_stride = prm->p_per_mask ? (long long)pl->N : 0;
+    pl->tm_m_ok = !pl->generic && tma_encode(&pl->tm_m, const_cast<void*>(d_m), pl->prec == PM_SINGLE, pl->nx, pl->ny,
+                                             batch, tma_m_box(pl));
     // pinned-free small uploads: stage in the session's host vectors, which
     // must outlive the async copies -> keep them in the plan
     s.h_en.resize(batch);
@@ -1394,6 +1462,19 @@ int pm_plan_create(int device, int n_x, int n_y, int precision, int max_batch, p
             per_sm = std::min(per_sm, per_sm_raar);
             if (e4 == cudaSuccess && per_sm > 0) pl->solve_grid = per_sm * nsm;
             cudaGetLastError();
+            if (e4 == cudaSuccess && ks.solve_tma) {
+                int a1 = 0, a2 = 0;
+                cudaError_t e5 = allow_smem(ks.solve_tma, ks.solve_smem_tma);
+                if (e5 == cudaSuccess) e5 = allow_smem(ks.solve_raar_tma, ks.solve_smem_raar_tma);
+                if (e5 == cudaSuccess)
+                    e5 = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a1, ks.solve_tma, ks.solve_threads,
+                                                                       ks.solve_smem_tma);
+                if (e5 == cudaSuccess)
+                    e5 = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a2, ks.solve_raar_tma, ks.solve_threads,
+                                                                       ks.solve_smem_raar_tma);
+                if (e5 == cudaSuccess && std::min(a1, a2) > 0) pl->solve_grid_tma = std::min(a1, a2) * nsm;
+                cudaGetLastError();
+            }
         }
         if (cudaMalloc((void**)&pl->bar, sizeof(GridBar)) != cudaSuccess ||
             cudaMemset(pl->bar, 0, sizeof(GridBar)) != cudaSuccess)

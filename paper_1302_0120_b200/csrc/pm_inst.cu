@@ -38,6 +38,10 @@ KernelSet PM_CAT3(make_set_, PM_TAG, PM_LG)() {
     s.col_fft = (const void*)&col_fft_kernel<PM_T, PM_LG, PM_LGR_COL>;
     s.solve = nullptr;
     s.solve_raar = nullptr;
+    s.solve_tma = nullptr;
+    s.solve_raar_tma = nullptr;
+    s.solve_smem_tma = 0;
+    s.solve_smem_raar_tma = 0;
     s.solve_smem = 0;
     s.solve_smem_raar = 0;
     s.solve_threads = 0;
@@ -45,8 +49,15 @@ KernelSet PM_CAT3(make_set_, PM_TAG, PM_LG)() {
     if constexpr (PM_LG >= 7 && FR::TG <= kSolveThreads && FC::TG <= kSolveThreads) {
         s.solve = (const void*)&solve_kernel<PM_T, PM_LG, PM_LGR_ROW, PM_LGR_COL, 0>;
         s.solve_raar = (const void*)&solve_kernel<PM_T, PM_LG, PM_LGR_ROW, PM_LGR_COL, 1>;
-        s.solve_smem = SolveSmem<PM_T, PM_LG, PM_LGR_ROW, PM_LGR_COL>::BYTES;
-        s.solve_smem_raar = SolveSmem<PM_T, PM_LG, PM_LGR_ROW, PM_LGR_COL>::BYTES_RAAR;
+        using LT = SolveSmem<PM_T, PM_LG, PM_LGR_ROW, PM_LGR_COL, true>;
+        if constexpr (LT::TMA) {
+            s.solve_tma = (const void*)&solve_kernel<PM_T, PM_LG, PM_LGR_ROW, PM_LGR_COL, 0, true>;
+            s.solve_raar_tma = (const void*)&solve_kernel<PM_T, PM_LG, PM_LGR_ROW, PM_LGR_COL, 1, true>;
+            s.solve_smem_tma = LT::BYTES_ALL + 128;
+            s.solve_smem_raar_tma = LT::BYTES_ALL_RAAR + 128;
+        }
+        s.solve_smem = SolveSmem<PM_T, PM_LG, PM_LGR_ROW, PM_LGR_COL>::BYTES_ALL + 128;
+        s.solve_smem_raar = SolveSmem<PM_T, PM_LG, PM_LGR_ROW, PM_LGR_COL>::BYTES_ALL_RAAR + 128;
         s.solve_threads = kSolveThreads;
     }
     s.row = AxisShape{FR::lgR, FR::TG, FR::NP, FR::SM, FR::TW};

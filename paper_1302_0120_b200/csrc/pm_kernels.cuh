@@ -23,6 +23,8 @@
 // non-finite), so a whole solve runs without host round trips; sweeps after
 // the decision exit at their first instruction.
 #pragma once
+#include <cuda.h>   // CUtensorMap (the maps are encoded on the host through the driver entry point)
+
 #include "pm_fft.cuh"
 
 // PM_ROLL=1: one rolled copy of the transform per task (half the code);
@@ -394,6 +396,37 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
+// ---------------------------------------------------------------- TMA
+// Tensor-memory-accelerator copies (cp.async.bulk.tensor) completing on an
+// mbarrier: one elected thread moves a whole column tile into shared memory
+// while the CTA computes, with no load instructions on the LSU path.
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z,
+                                            unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+        ::"r"(smem_u32(dst)), "l"(map), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+        : "memory");
+}
+
 // No prefetch: the sweep kernels and single-task phases.
 struct NoPrefetch {
     __device__ __forceinline__ void operator()() const {}
@@ -633,11 +666,26 @@ __device__ __forceinline__ void final_task(const FinalArgs<T>& a, int b, int row
 // receives this task's [n_y][C] slice of m through cp.async.
 // `tile` / `prefetch()`: cross-task prefetch as in row_task (the tile holds
 // this task's [n_y][C] input, written by the previous task's cp.async).
+// TM (TMA): the input arrived in shared memory through the tensor
+// accelerator: `tma` holds the tiles, their mbarriers and the parity of this
+// task; the task issues the next task's copies (next_f / next_m) as soon as
+// its own tiles are consumed.
+template <typename T>
+struct TmaTask {
+    const cx<T>* ft;              // [n_y][C] input
+    const T* mt;                  // [n_y][MC] m
+    unsigned long long* bars;     // [0] input, [1] m
+    unsigned parity;
+    int MC;
+};
+
 template <typename T, int LG_L, int LG_R, int NX, bool TS = false, bool PS = false, int CC = 0,
-          class Prefetch = NoPrefetch>
+          class Prefetch = NoPrefetch, bool TM = false, class NextF = NoPrefetch, class NextM = NoPrefetch>
 __device__ __forceinline__ void col_task(const ColArgs<T>& a, int b, int col0, int C, cx<T>* smbase,
                                          const twe<T>* tw, T* ms, bool live, double (&acc)[3],
-                                         const cx<T>* tile = nullptr, Prefetch prefetch = Prefetch{}) {
+                                         const cx<T>* tile = nullptr, Prefetch prefetch = Prefetch{},
+                                         TmaTask<T> tma = TmaTask<T>{}, NextF next_f = NextF{},
+                                         NextM next_m = NextM{}) {
     using F = FftShape<LG_L, LG_R>;
     const int c = threadIdx.x % C, j = threadIdx.x / C;
     const size_t nx = NX > 0 ? (size_t)NX : (size_t)a.nx;
@@ -655,6 +703,12 @@ __device__ __forceinline__ void col_task(const ColArgs<T>& a, int b, int col0, i
         // conj(ColIFFT(m)) is ColFFT(m); the row phase finishes u0
 #pragma unroll
         for (int k = 0; k < F::R; ++k) v[k] = mk<T>(m[k * rs], T(0));
+    } else if (TM && a.mode == 2) {
+        mbar_wait(&tma.bars[0], tma.parity);
+#pragma unroll
+        for (int k = 0; k < F::R; ++k) v[k] = tma.ft[(j + F::TG * k) * C + c];
+        __syncthreads();                                                         // tile free
+        if (threadIdx.x == 0) next_f();
     } else if (tile) {
         cp_async_wait<0>();
         __syncthreads();
@@ -678,7 +732,7 @@ __device__ __forceinline__ void col_task(const ColArgs<T>& a, int b, int col0, i
         }
         return;
     }
-    if constexpr (PS) {
+    if constexpr (PS && !TM) {
         // CC: the persistent kernel's compile-time column count (division-free copy loop)
         static_assert(CC > 0, "staged m needs the compile-time column count");
         stage_tile<T, (1 << LG_L), CC, CC * F::TG>(ms, a.m + b * a.m_stride + col0, nx, threadIdx.x);
@@ -707,15 +761,23 @@ __device__ __forceinline__ void col_task(const ColArgs<T>& a, int b, int col0, i
             for (int k = 0; k < F::R; ++k) v[k] = cscale(v[k], a.scale);
         }
         const T thr = T(scaled ? a.thr_m[b] : a.thr_ms[b]);
-        if constexpr (PS) {
-            cp_async_wait<1>();                      // m of this task (the prefetch may stay in flight)
-            __syncthreads();
-        }
         T mm[F::R];
+        if constexpr (TM) {
+            mbar_wait(&tma.bars[1], tma.parity);
 #pragma unroll
-        for (int k = 0; k < F::R; ++k) {
-            if constexpr (PS) mm[k] = ms[(j + F::TG * k) * C + c];
-            else mm[k] = m[k * rs];
+            for (int k = 0; k < F::R; ++k) mm[k] = tma.mt[(j + F::TG * k) * tma.MC + c];
+            __syncthreads();                                                     // m tile free
+            if (threadIdx.x == 0) next_m();
+        } else {
+            if constexpr (PS) {
+                cp_async_wait<1>();                  // m of this task (the prefetch may stay in flight)
+                __syncthreads();
+            }
+#pragma unroll
+            for (int k = 0; k < F::R; ++k) {
+                if constexpr (PS) mm[k] = ms[(j + F::TG * k) * C + c];
+                else mm[k] = m[k * rs];
+            }
         }
         if (rec && act) {
             // reconstructed intensity and physical error (src/metrics.py:74-112);
@@ -941,6 +1003,9 @@ struct SolveArgs {
     int init_mode;             // column init from real m (0) or complex field (1)
     int do_probe;              // RAAR: end with the gap / decision of the last iterate
     unsigned long long* stamps; // optional: globaltimer at every phase boundary (CTA 0)
+    int tma;                   // the column phase's TMA maps below are valid
+    CUtensorMap tm_in;         // column input w' ([batch][n_y][2 n_x] floats or doubles)
+    CUtensorMap tm_m;          // m ([batch][n_y][n_x])
 };
 
 // stamps[cta * kStampsPerCta + i] = %globaltimer at the i-th stamp point.
@@ -968,7 +1033,7 @@ constexpr int kSolveThreads = PM_SOLVE_NT;
 // then, while they fit, the staged real grid of a task (p rows / m columns,
 // PS) and copies of the twiddle tables (TS; L1 does not survive the grid
 // barrier's acquire, so tables read through L1 would miss once per pass).
-template <typename T, int LG, int LGR_R, int LGR_C>
+template <typename T, int LG, int LGR_R, int LGR_C, bool TV = false>
 struct SolveSmem {
     using FR = FftShape<LG, LGR_R>;
     using FC = FftShape<LG, LGR_C>;
@@ -997,18 +1062,48 @@ struct SolveSmem {
 #ifndef PM_PF
 #define PM_PF 0
 #endif
+#ifndef PM_TMA
+#define PM_TMA 1
+#endif
+    // TMA column tiles (column phase): the task's input [n_y][C] and its m
+    // [n_y][MC] (a TMA box row is >= 16 bytes), plus two mbarriers. Placed
+    // after every other region when they fit (A); else the shared twiddles
+    // give way (B); else the tiles overlay the row phase's staging, which is
+    // idle during the column phase (C).
+    static constexpr int MC = C * (int)sizeof(T) >= 16 ? C : 16 / (int)sizeof(T);
+    static constexpr int FTB = up16((int)sizeof(cx<T>) * (C << LG));
+    static constexpr int MTB = up16((int)sizeof(T) * (MC << LG));
+    static constexpr int TMAB = FTB + MTB + 16;
+    static constexpr int XSB = up16((int)sizeof(cx<T>) * (G << LG));   // RAAR: the row's x staged with p
     static constexpr bool PF = PM_PF && EX + ST + TILE + TWB <= LIMIT;
-    static constexpr bool TS = PF ? (EX + ST + TILE + TWB <= LIMIT) : (EX + TWB <= LIMIT);
-    static constexpr bool PS = PF || (EX + (TS ? TWB : 0) + ST <= LIMIT);
+    static constexpr bool TS0 = PF ? (EX + ST + TILE + TWB <= LIMIT) : (EX + TWB <= LIMIT);
+    static constexpr bool PS0 = PF || (EX + (TS0 ? TWB : 0) + ST <= LIMIT);
+    static constexpr int BASE0 = EX + (PS0 ? ST : 0) + (PF ? TILE : 0) + (TS0 ? TWB : 0);
+    // (boxes exactly one task wide: a 16-byte m box over a narrower task
+    // faulted on B200 at 256^2, so narrower tasks keep the cp.async staging)
+    static constexpr bool WANT = TV && PM_TMA && LG >= 8 && !PF && MC == C;
+    static constexpr bool TMA_A = WANT && BASE0 + TMAB <= LIMIT;
+    // (B / C drop the shared twiddles; measured: the hoisted global twiddle
+    // loads then spill at 2048^2 / 4096^2, so only A is enabled)
+    static constexpr bool TMA_B = false && WANT && !TMA_A && EX + ST + TMAB <= LIMIT;
+    static constexpr bool TMA_C = false && WANT && !TMA_A && !TMA_B && EX + TMAB <= LIMIT;
+    static constexpr bool TMA = TMA_A || TMA_B || TMA_C;
+    static constexpr bool TS = (TMA_B || TMA_C) ? false : TS0;
+    static constexpr bool PS = (TMA_B || TMA_C) ? true : PS0;
     static constexpr int OFF_ST = EX;
     static constexpr int OFF_TILE = EX + (PS ? ST : 0);
     static constexpr int OFF_TW = OFF_TILE + (PF ? TILE : 0);
     static constexpr int BYTES = OFF_TW + (TS ? TWB : 0);
-    // RAAR kernel: the row's iterate x staged with p (cp.async) when it fits
-    static constexpr int XSB = up16((int)sizeof(cx<T>) * (G << LG));
-    static constexpr bool XS = PS && BYTES + XSB <= LIMIT;
-    static constexpr int OFF_XS = BYTES;
-    static constexpr int BYTES_RAAR = BYTES + (XS ? XSB : 0);
+    static constexpr int up128(int x) { return (x + 127) / 128 * 128; }
+    static constexpr int OFF_FT = TMA_C ? EX : up128(BYTES);
+    static constexpr int OFF_MT = OFF_FT + FTB;
+    static constexpr int OFF_BAR = OFF_MT + MTB;
+    static constexpr int TMA_END = TMA ? OFF_BAR + 16 : 0;
+    static constexpr int BYTES_T = TMA_END > BYTES ? TMA_END : BYTES;
+    static constexpr bool XS = PS && BYTES_T + XSB <= LIMIT;
+    static constexpr int OFF_XS = BYTES_T;
+    static constexpr int BYTES_ALL = BYTES_T;
+    static constexpr int BYTES_ALL_RAAR = BYTES_T + (XS ? XSB : 0);
     static constexpr int CB = C * (int)sizeof(T);                 // bytes per m run of a column task
     static constexpr int CH = CB >= 16 ? 16 : CB;                 // cp.async size for it
 };
@@ -1020,9 +1115,9 @@ struct Tables {
 };
 
 // The solve's twiddle tables: shared copies (made once per launch) or global.
-template <typename T, int LG, int LGR_R, int LGR_C>
+template <typename T, int LG, int LGR_R, int LGR_C, bool TV = false>
 __device__ __forceinline__ Tables<T> load_tables(const RowArgs<T>& r, const ColArgs<T>& c, unsigned char* smraw) {
-    using L = SolveSmem<T, LG, LGR_R, LGR_C>;
+    using L = SolveSmem<T, LG, LGR_R, LGR_C, TV>;
     if constexpr (!L::TS) {
         return Tables<T>{r.twf, c.twf};
     } else {
@@ -1051,10 +1146,10 @@ __device__ __forceinline__ void row_share(int total, int& start, int& count) {
 // time. The field loads of a task are issued before its mask state is known,
 // so the state's L2 round trip overlaps them. Groups of whole warps with no
 // row left skip the round (their barriers are their own).
-template <typename T, int LG, int LGR_R, int LGR_C, int ALG>
+template <typename T, int LG, int LGR_R, int LGR_C, int ALG, bool TV = false>
 __device__ __forceinline__ void row_phase(const RowArgs<T>& a, int batch, unsigned char* smraw,
                                           const Tables<T>& tw) {
-    using L = SolveSmem<T, LG, LGR_R, LGR_C>;
+    using L = SolveSmem<T, LG, LGR_R, LGR_C, TV>;
     using F = FftShape<LG, LGR_R>;
     cx<T>* smem = reinterpret_cast<cx<T>*>(smraw);
     const int G = blockDim.x / F::TG;
@@ -1086,10 +1181,10 @@ __device__ __forceinline__ void row_phase(const RowArgs<T>& a, int batch, unsign
     }
 }
 
-template <typename T, int LG, int LGR_R, int LGR_C>
+template <typename T, int LG, int LGR_R, int LGR_C, bool TV = false>
 __device__ __forceinline__ void final_phase(const FinalArgs<T>& a, int batch, unsigned char* smraw,
                                             const Tables<T>& tw) {
-    using L = SolveSmem<T, LG, LGR_R, LGR_C>;
+    using L = SolveSmem<T, LG, LGR_R, LGR_C, TV>;
     using F = FftShape<LG, LGR_R>;
     cx<T>* smem = reinterpret_cast<cx<T>*>(smraw);
     const int G = blockDim.x / F::TG;
@@ -1110,10 +1205,18 @@ __device__ __forceinline__ void final_phase(const FinalArgs<T>& a, int batch, un
 // Column phase; with metrics, task t of mask b leaves its block sum in
 // part[b][t] so the per-mask total is combined in task order (independent of
 // which CTA ran which task, hence of batch size and grid size).
-template <typename T, int LG, int LGR_R, int LGR_C>
+// TMA maps of the column phase: its input (w') and m, as [batch][n_y][2 n_x]
+// / [batch][n_y][n_x] tensors with boxes of min(256, n_y) rows (null: no TMA).
+struct ColTma {
+    const CUtensorMap* in;
+    const CUtensorMap* m;
+    unsigned* count;              // tile loads completed by this CTA (mbarrier parity)
+};
+
+template <typename T, int LG, int LGR_R, int LGR_C, bool TV = false>
 __device__ __forceinline__ void col_phase(const ColArgs<T>& a, int batch, unsigned char* smraw,
-                                          const Tables<T>& tw) {
-    using L = SolveSmem<T, LG, LGR_R, LGR_C>;
+                                          const Tables<T>& tw, ColTma ct = ColTma{nullptr, nullptr, nullptr}) {
+    using L = SolveSmem<T, LG, LGR_R, LGR_C, TV>;
     using F = FftShape<LG, LGR_C>;
     cx<T>* smem = reinterpret_cast<cx<T>*>(smraw);
     T* ms = reinterpret_cast<T*>(smraw + L::OFF_ST);
@@ -1131,6 +1234,55 @@ __device__ __forceinline__ void col_phase(const ColArgs<T>& a, int batch, unsign
     // prefetch the next task's columns while this one computes (iterate mode,
     // more than one task for this CTA)
     const bool pf = L::PF && a.mode == 2 && (int)blockIdx.x + (int)gridDim.x < total;
+    if constexpr (L::TMA) {
+        // CTAs with several tasks in this phase (batches, large grids); a
+        // single task is faster with direct loads (measured: 1024^2, 1 mask)
+        if (ct.in && a.mode == 2 && (int)blockIdx.x + (int)gridDim.x < total) {
+            // TMA: tiles for task t are in flight before t starts; each task
+            // issues its successor's copies once its own tiles are consumed
+            constexpr int BOXR = NX < 256 ? NX : 256;
+            cx<T>* ft = reinterpret_cast<cx<T>*>(smraw + L::OFF_FT);
+            T* mt = reinterpret_cast<T*>(smraw + L::OFF_MT);
+            unsigned long long* bars = reinterpret_cast<unsigned long long*>(smraw + L::OFF_BAR);
+            auto issue_f = [&](int t) {
+                const int bt = t / tpm, c0 = (t - bt * tpm) * C;
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // prior reads of the tile
+                mbar_expect_tx(&bars[0], (unsigned)(sizeof(cx<T>) * C * NX));
+                for (int r = 0; r < NX; r += BOXR) tma_load_3d(ft + (size_t)r * C, ct.in, 2 * c0, r, bt, &bars[0]);
+            };
+            auto issue_m = [&](int t) {
+                const int bt = t / tpm, c0 = (t - bt * tpm) * C;
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_expect_tx(&bars[1], (unsigned)(sizeof(T) * L::MC * NX));
+                for (int r = 0; r < NX; r += BOXR) tma_load_3d(mt + (size_t)r * L::MC, ct.m, c0, r, bt, &bars[1]);
+            };
+            if (threadIdx.x == 0 && (int)blockIdx.x < total) {
+                issue_f(blockIdx.x);
+                issue_m(blockIdx.x);
+            }
+            for (int t = blockIdx.x; t < total; t += gridDim.x) {
+                const int b = t / tpm, tt = t - b * tpm;
+                const bool act = mask_live(a.st + b);
+                const int tn = t + gridDim.x;
+                auto next_f = [&]() { if (tn < total) issue_f(tn); };
+                auto next_m = [&]() { if (tn < total) issue_m(tn); };
+                TmaTask<T> tk{ft, mt, bars, *ct.count & 1u, L::MC};
+                double acc[3];
+                col_task<T, LG, LGR_C, NX, L::TS, L::PS, L::C, NoPrefetch, true, decltype(next_f), decltype(next_m)>(
+                    a, b, tt * C, C, smem, tw.cf, ms, act, acc, nullptr, NoPrefetch{}, tk, next_f, next_m);
+                *ct.count += 1;
+                if (metr && act) {
+                    double tot[3];
+                    block_reduce<3>(acc, tot);
+                    if (threadIdx.x == 0) {
+                        double* q = part + ((size_t)b * tpm + tt) * 3;
+                        q[0] = tot[0]; q[1] = tot[1]; q[2] = tot[2];
+                    }
+                }
+            }
+            return;
+        }
+    }
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
         const int b = t / tpm, tt = t - b * tpm;
         const bool act = mask_live(a.st + b);
@@ -1201,26 +1353,45 @@ __device__ __forceinline__ void decide_phase_raar(const RowArgs<T>& r, int batch
     }
 }
 
-template <typename T, int LG, int LGR_R, int LGR_C, int ALG>
-__global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(SolveArgs<T> a) {
-    extern __shared__ __align__(16) unsigned char smraw[];
+template <typename T, int LG, int LGR_R, int LGR_C, int ALG, bool TV = false>
+__global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const __grid_constant__ SolveArgs<T> a) {
+    // dynamic shared memory follows the static variables: realign it to 128
+    // bytes (TMA destinations), for which the launch reserves 128 more bytes
+    extern __shared__ __align__(128) unsigned char smraw_[];
+    unsigned char* smraw = smraw_ + ((128u - (smem_u32(smraw_) & 127u)) & 127u);
+    using L = SolveSmem<T, LG, LGR_R, LGR_C, TV>;
     const int B = a.batch;
     int si = 0;
     unsigned epoch = 0;
     stamp(a.stamps, si);
-    const Tables<T> tw = load_tables<T, LG, LGR_R, LGR_C>(a.row, a.col, smraw);
+    const Tables<T> tw = load_tables<T, LG, LGR_R, LGR_C, TV>(a.row, a.col, smraw);
+    unsigned tma_count = 0;
+    ColTma ct{nullptr, nullptr, &tma_count};
+    if constexpr (L::TMA) {
+        if (a.tma) {
+            ct.in = &a.tm_in;
+            ct.m = &a.tm_m;
+            if (threadIdx.x == 0) {
+                unsigned long long* bars = reinterpret_cast<unsigned long long*>(smraw + L::OFF_BAR);
+                mbar_init(&bars[0], 1);
+                mbar_init(&bars[1], 1);
+                asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            }
+            __syncthreads();
+        }
+    }
     if (a.do_init) {
         ColArgs<T> c = a.col;
         c.mode = a.init_mode;
         c.u_iter = 0;
-        col_phase<T, LG, LGR_R, LGR_C>(c, B, smraw, tw);          // u0 column half
+        col_phase<T, LG, LGR_R, LGR_C, TV>(c, B, smraw, tw);          // u0 column half
         grid_sync(a.bar, epoch);
         RowArgs<T> r = a.row;
         r.mode = kRowInit;
-        row_phase<T, LG, LGR_R, LGR_C, ALG>(r, B, smraw, tw);     // u0 row half, w0 (RAAR: and x_0)
+        row_phase<T, LG, LGR_R, LGR_C, ALG, TV>(r, B, smraw, tw);     // u0 row half, w0 (RAAR: and x_0)
         grid_sync(a.bar, epoch);
         c.mode = 2;
-        col_phase<T, LG, LGR_R, LGR_C>(c, B, smraw, tw);          // z1
+        col_phase<T, LG, LGR_R, LGR_C, TV>(c, B, smraw, tw, ct);      // z1
         grid_sync(a.bar, epoch);
     }
     const bool early = a.col.ctl.early_tol >= 0.0;
@@ -1230,27 +1401,27 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(SolveArgs<T> a)
             RowArgs<T> r = a.row;
             r.mode = kRowRaar;
             r.it = it;
-            row_phase<T, LG, LGR_R, LGR_C, ALG>(r, B, smraw, tw);   // gap of x_{it-1}, x_it, w_it
+            row_phase<T, LG, LGR_R, LGR_C, ALG, TV>(r, B, smraw, tw);   // gap of x_{it-1}, x_it, w_it
             grid_sync(a.bar, epoch);
             decide_phase_raar<T>(r, B, it - 1);
             if (early) grid_sync(a.bar, epoch);
             ColArgs<T> c = a.col;
             c.mode = 2;
             c.u_iter = it;
-            col_phase<T, LG, LGR_R, LGR_C>(c, B, smraw, tw);        // lit/dark of x_it, z_{it+1}
+            col_phase<T, LG, LGR_R, LGR_C, TV>(c, B, smraw, tw, ct);    // lit/dark of x_it, z_{it+1}
             grid_sync(a.bar, epoch);
         }
         if (a.do_probe) {
             RowArgs<T> r = a.row;
             r.mode = kRowProbe;
             r.it = a.it_end;
-            row_phase<T, LG, LGR_R, LGR_C, ALG>(r, B, smraw, tw);   // gap of x_{it_end-1}
+            row_phase<T, LG, LGR_R, LGR_C, ALG, TV>(r, B, smraw, tw);   // gap of x_{it_end-1}
             grid_sync(a.bar, epoch);
             decide_phase_raar<T>(r, B, a.it_end - 1);
             grid_sync(a.bar, epoch);
         }
         if (a.do_final) {
-            final_phase<T, LG, LGR_R, LGR_C>(a.fin, B, smraw, tw);   // pair, mask, gap of x_K
+            final_phase<T, LG, LGR_R, LGR_C, TV>(a.fin, B, smraw, tw);   // pair, mask, gap of x_K
             grid_sync(a.bar, epoch);
             decide_phase_raar<T>(a.row, B, a.fin.ctl.max_iters);
         }
@@ -1259,14 +1430,14 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(SolveArgs<T> a)
             RowArgs<T> r = a.row;
             r.mode = kRowGS;
             r.it = it;
-            row_phase<T, LG, LGR_R, LGR_C, ALG>(r, B, smraw, tw);   // u_it, w_it
+            row_phase<T, LG, LGR_R, LGR_C, ALG, TV>(r, B, smraw, tw);   // u_it, w_it
             stamp(a.stamps, si);
             grid_sync(a.bar, epoch);
             stamp(a.stamps, si);
             ColArgs<T> c = a.col;
             c.mode = 2;
             c.u_iter = it;
-            col_phase<T, LG, LGR_R, LGR_C>(c, B, smraw, tw);        // metrics of u_it, z_{it+1}
+            col_phase<T, LG, LGR_R, LGR_C, TV>(c, B, smraw, tw, ct);    // metrics of u_it, z_{it+1}
             stamp(a.stamps, si);
             grid_sync(a.bar, epoch);
             stamp(a.stamps, si);
@@ -1275,7 +1446,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(SolveArgs<T> a)
             if (gap_needed(c.ctl, it) || it >= c.ctl.max_iters || it == a.it_end - 1) decide_phase<T, LG, LGR_C>(c, B);
             if (early) grid_sync(a.bar, epoch);                        // stop flags must be seen by every CTA
         }
-        if (a.do_final) final_phase<T, LG, LGR_R, LGR_C>(a.fin, B, smraw, tw);
+        if (a.do_final) final_phase<T, LG, LGR_R, LGR_C, TV>(a.fin, B, smraw, tw);
     }
     stamp(a.stamps, si);
 }

@@ -24,6 +24,12 @@ struct KernelSet {
     const void* solve_raar; // the same for RAAR
     int solve_smem;         // its dynamic shared memory (bytes)
     int solve_smem_raar;    // the RAAR kernel's (x staged as well)
+    // variants whose column phase streams tiles through TMA (used when a CTA
+    // has several column tasks per phase: batches), or null
+    const void* solve_tma;
+    const void* solve_raar_tma;
+    int solve_smem_tma;
+    int solve_smem_raar_tma;
     int solve_threads;      // its CTA size
     AxisShape row, col;
 };

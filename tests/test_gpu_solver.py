@@ -329,3 +329,25 @@ def test_batch_device_tolerances_match_host_and_reject_zero_inputs():
         solve_stack(p, ms, pm.SolveConfig(max_iters=3))
     with pytest.raises(ValueError, match="identically zero"):
         solve_stack(np.zeros_like(p), m[None], pm.SolveConfig(max_iters=3))
+
+
+@pytest.mark.parametrize("n,tag,algo,B", [(1024, "single", "gs", 4), (512, "double", "gs", 6),
+                                          (512, "single", "raar", 5)])
+def test_tma_batch_variant_is_bitwise_equal_to_single_solves(n, tag, algo, B):
+    """Batches large enough to give every CTA several column tasks run the
+    persistent kernel's TMA variant (tiles streamed by the tensor memory
+    accelerator); each mask must equal its own single-mask solve bitwise,
+    early stopping included."""
+    prec = pm.Precision.from_tag(tag)
+    p, _ = make_problem(n, 8, 7)
+    ms = np.stack([make_problem(n, 8, s)[1] for s in range(20, 20 + B)])
+    cfg = pm.SolveConfig(max_iters=9, precision=prec, record_every=3, algorithm=algo,
+                         early_stop_tol=1e-9 if algo == "gs" else None)
+    whole = solve_stack(p.astype(prec.float_dtype), ms.astype(prec.float_dtype), cfg)
+    spec = pm.GridSpec(n, n)
+    for i in (0, B - 1):
+        r = pm.solve(pm.SlmConstraint(pm.RealGrid(spec, p), prec),
+                     pm.FourierConstraint(pm.RealGrid(spec, ms[i]), prec), cfg)
+        np.testing.assert_array_equal(r.mask.phases, whole.phases[i])
+        assert r.iters_run == whole.iters_run[i]
+        assert [h.gap for h in r.history] == list(whole.gap[i][~np.isnan(whole.gap[i])])
