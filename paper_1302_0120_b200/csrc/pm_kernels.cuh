@@ -1079,9 +1079,7 @@ struct SolveSmem {
     static constexpr bool TS0 = PF ? (EX + ST + TILE + TWB <= LIMIT) : (EX + TWB <= LIMIT);
     static constexpr bool PS0 = PF || (EX + (TS0 ? TWB : 0) + ST <= LIMIT);
     static constexpr int BASE0 = EX + (PS0 ? ST : 0) + (PF ? TILE : 0) + (TS0 ? TWB : 0);
-    // (boxes exactly one task wide: a 16-byte m box over a narrower task
-    // faulted on B200 at 256^2, so narrower tasks keep the cp.async staging)
-    static constexpr bool WANT = TV && PM_TMA && LG >= 8 && !PF && MC == C;
+    static constexpr bool WANT = TV && PM_TMA && LG >= 8 && !PF;
     static constexpr bool TMA_A = WANT && BASE0 + TMAB <= LIMIT;
     // (B / C drop the shared twiddles; measured: the hoisted global twiddle
     // loads then spill at 2048^2 / 4096^2, so only A is enabled)
@@ -1250,11 +1248,16 @@ __device__ __forceinline__ void col_phase(const ColArgs<T>& a, int batch, unsign
                 mbar_expect_tx(&bars[0], (unsigned)(sizeof(cx<T>) * C * NX));
                 for (int r = 0; r < NX; r += BOXR) tma_load_3d(ft + (size_t)r * C, ct.in, 2 * c0, r, bt, &bars[0]);
             };
+            // a box must start on a 16-byte boundary: when a task is narrower
+            // than 16 bytes of m, the box starts at the aligned column below
+            // and the task reads from its offset inside the tile
+            constexpr int MA = 16 / (int)sizeof(T);
             auto issue_m = [&](int t) {
                 const int bt = t / tpm, c0 = (t - bt * tpm) * C;
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 mbar_expect_tx(&bars[1], (unsigned)(sizeof(T) * L::MC * NX));
-                for (int r = 0; r < NX; r += BOXR) tma_load_3d(mt + (size_t)r * L::MC, ct.m, c0, r, bt, &bars[1]);
+                for (int r = 0; r < NX; r += BOXR)
+                    tma_load_3d(mt + (size_t)r * L::MC, ct.m, c0 & ~(MA - 1), r, bt, &bars[1]);
             };
             if (threadIdx.x == 0 && (int)blockIdx.x < total) {
                 issue_f(blockIdx.x);
@@ -1266,7 +1269,7 @@ __device__ __forceinline__ void col_phase(const ColArgs<T>& a, int batch, unsign
                 const int tn = t + gridDim.x;
                 auto next_f = [&]() { if (tn < total) issue_f(tn); };
                 auto next_m = [&]() { if (tn < total) issue_m(tn); };
-                TmaTask<T> tk{ft, mt, bars, *ct.count & 1u, L::MC};
+                TmaTask<T> tk{ft, mt + ((tt * C) & (MA - 1)), bars, *ct.count & 1u, L::MC};
                 double acc[3];
                 col_task<T, LG, LGR_C, NX, L::TS, L::PS, L::C, NoPrefetch, true, decltype(next_f), decltype(next_m)>(
                     a, b, tt * C, C, smem, tw.cf, ms, act, acc, nullptr, NoPrefetch{}, tk, next_f, next_m);

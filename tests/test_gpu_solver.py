@@ -331,7 +331,7 @@ def test_batch_device_tolerances_match_host_and_reject_zero_inputs():
         solve_stack(np.zeros_like(p), m[None], pm.SolveConfig(max_iters=3))
 
 
-@pytest.mark.parametrize("n,tag,algo,B", [(1024, "single", "gs", 4), (512, "double", "gs", 6),
+@pytest.mark.parametrize("n,tag,algo,B", [(1024, "single", "gs", 4), (512, "double", "gs", 6), (256, "single", "gs", 24),
                                           (512, "single", "raar", 5)])
 def test_tma_batch_variant_is_bitwise_equal_to_single_solves(n, tag, algo, B):
     """Batches large enough to give every CTA several column tasks run the
