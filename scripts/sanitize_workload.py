@@ -40,3 +40,5 @@ run(64, 64, "double", algo="raar")
 run(128, 128, "single", batch=3)
 run(60, 42, "double")
 run(30, 40, "single", batch=2)
+run(256, 256, "single", batch=24, K=2)            # TMA build (column tiles via cp.async.bulk.tensor)
+run(512, 512, "single", algo="raar", batch=5, K=2)
