@@ -908,9 +908,17 @@ int gen_setup(pm_plan* pl) {
     pl->gsm_r = 2 * (size_t)pl->nx * pl->gtc_r * pl->csz;
     pl->gsm_c = 2 * (size_t)pl->ny * pl->gtc_c * pl->csz;
     const size_t mx = std::max(pl->gsm_r, pl->gsm_c);
-    cudaError_t e = pl->prec == PM_SINGLE ? allow_smem((const void*)&gen_fft_kernel<float>, mx)
-                                          : allow_smem((const void*)&gen_fft_kernel<double>, mx);
-    if (e != cudaSuccess) return cuda_err(e, "cudaFuncSetAttribute(gen_fft_kernel)");
+    cudaError_t e;
+    if (pl->prec == PM_SINGLE) {
+        e = allow_smem((const void*)&gen_fft_kernel<float>, mx);
+        if (e == cudaSuccess) e = allow_smem((const void*)&gen_col_sweep_kernel<float>, mx);
+        if (e == cudaSuccess) e = allow_smem((const void*)&gen_row_sweep_kernel<float>, mx);
+    } else {
+        e = allow_smem((const void*)&gen_fft_kernel<double>, mx);
+        if (e == cudaSuccess) e = allow_smem((const void*)&gen_col_sweep_kernel<double>, mx);
+        if (e == cudaSuccess) e = allow_smem((const void*)&gen_row_sweep_kernel<double>, mx);
+    }
+    if (e != cudaSuccess) return cuda_err(e, "cudaFuncSetAttribute(gen kernels)");
     return PM_OK;
 }
 
@@ -991,6 +999,48 @@ int gen_half(pm_plan* pl, int u_iter, int metrics_only, int all_masks) {
     return gen_fft2(pl, pl->tmp, pl->tmp, PM_INVERSE, B, pl->st, all_masks);
 }
 
+// w = RowFFT(u): the iterates (field) into the work buffer.
+int gen_rows_fwd(pm_plan* pl, int all_masks) {
+    return pl->prec == PM_SINGLE ? gen_axis<float>(pl, pl->field, pl->tmp, 0, PM_FORWARD, pl->s.batch, pl->st, all_masks)
+                                 : gen_axis<double>(pl, pl->field, pl->tmp, 0, PM_FORWARD, pl->s.batch, pl->st,
+                                                    all_masks);
+}
+
+int lg_of(int tc) {
+    int l = 0;
+    while ((1 << l) < tc) ++l;
+    return l;
+}
+
+// Fused column sweep on the work buffer (ColFFT, replace_m + metrics of
+// u_{u_iter}, ColIFFT).
+template <typename T>
+int gen_col_sweep(pm_plan* pl, int u_iter, int metrics_only, int all_masks) {
+    const int TC = pl->gtc_c;
+    const dim3 grid((pl->nx + TC - 1) / TC, pl->s.batch);
+    GenSolveArgs g = gen_args(pl);
+    g.nblk = (int)grid.x;
+    gen_col_sweep_kernel<T><<<grid, 256, pl->gsm_c, pl->stream>>>(
+        (cx<T>*)pl->tmp, (const T*)pl->s.m, pl->thrm, pl->escale, (const cx<T>*)pl->gtwy, pl->gy, pl->nx,
+        lg_of(TC), g, u_iter, metrics_only, all_masks);
+    CK(cudaGetLastError());
+    pl->launches++;
+    return PM_OK;
+}
+
+// Fused row sweep (RowIFFT, P_S into the iterate, RowFFT into the work buffer).
+template <typename T>
+int gen_row_sweep(pm_plan* pl, int it) {
+    const int TC = pl->gtc_r;
+    const dim3 grid((pl->ny + TC - 1) / TC, pl->s.batch);
+    gen_row_sweep_kernel<T><<<grid, 256, pl->gsm_r, pl->stream>>>(
+        (cx<T>*)pl->tmp, (cx<T>*)pl->field, (const T*)pl->s.p, pl->s.p_stride, pl->thrx, (const cx<T>*)pl->gtwx,
+        pl->gx, pl->ny, lg_of(TC), pl->st, (long long)pl->N, it);
+    CK(cudaGetLastError());
+    pl->launches++;
+    return PM_OK;
+}
+
 int gen_begin(pm_plan* pl) {
     auto& s = pl->s;
     const long long total = (long long)s.batch * pl->N;
@@ -1004,7 +1054,8 @@ int gen_begin(pm_plan* pl) {
         CK(cudaGetLastError());
         pl->launches++;
     }
-    return gen_fft2(pl, pl->field, pl->field, PM_INVERSE, s.batch, pl->st, 0);   // u0 = F^-1(m e^{i phi})
+    CKR(gen_fft2(pl, pl->field, pl->field, PM_INVERSE, s.batch, pl->st, 0));   // u0 = F^-1(m e^{i phi})
+    return gen_rows_fwd(pl, 0);                                                  // w = RowFFT(u0)
 }
 
 template <typename T>
@@ -1017,16 +1068,21 @@ int gen_slm(pm_plan* pl, int it) {
     return PM_OK;
 }
 
+// Two fused sweeps per iteration over the work buffer, which holds
+// RowFFT(u_{it-1}) on entry and RowFFT(u_it) on exit; the iterate itself is
+// kept in `field` so a mask that stops keeps its last iterate.
 int gen_steps(pm_plan* pl, int n, bool probe) {
     auto& s = pl->s;
+    const bool f32 = pl->prec == PM_SINGLE;
     bool any = false;
     for (int i = 0; i < n && s.it < s.prm.max_iters; ++i) {
         s.it += 1;
         any = true;
-        CKR(gen_half(pl, s.it - 1, 0, 0));                                 // metrics of u_{it-1}
-        CKR(pl->prec == PM_SINGLE ? gen_slm<float>(pl, s.it) : gen_slm<double>(pl, s.it));   // u_it
+        CKR(f32 ? gen_col_sweep<float>(pl, s.it - 1, 0, 0) : gen_col_sweep<double>(pl, s.it - 1, 0, 0));
+        CKR(f32 ? gen_row_sweep<float>(pl, s.it) : gen_row_sweep<double>(pl, s.it));
     }
-    if (any && probe) CKR(gen_half(pl, s.it, 1, 0));                       // gap + decision of u_it now
+    if (any && probe)                                                       // gap + decision of u_it now
+        CKR(f32 ? gen_col_sweep<float>(pl, s.it, 1, 0) : gen_col_sweep<double>(pl, s.it, 1, 0));
     return PM_OK;
 }
 
@@ -1045,8 +1101,12 @@ int gen_final_t(pm_plan* pl) {
 // v* = P_M u (every mask, decision of the last iterate if still pending),
 // then u*, the mask and the levels.
 int gen_finish(pm_plan* pl) {
-    CKR(gen_half(pl, pl->s.it, 0, 1));
-    return pl->prec == PM_SINGLE ? gen_final_t<float>(pl) : gen_final_t<double>(pl);
+    const bool f32 = pl->prec == PM_SINGLE;
+    CKR(gen_rows_fwd(pl, 1));              // every mask from its last iterate (stopped ones included)
+    CKR(f32 ? gen_col_sweep<float>(pl, pl->s.it, 0, 1) : gen_col_sweep<double>(pl, pl->s.it, 0, 1));
+    CKR(f32 ? gen_axis<float>(pl, pl->tmp, pl->tmp, 0, PM_INVERSE, pl->s.batch, pl->st, 1)
+            : gen_axis<double>(pl, pl->tmp, pl->tmp, 0, PM_INVERSE, pl->s.batch, pl->st, 1));
+    return f32 ? gen_final_t<float>(pl) : gen_final_t<double>(pl);
 }
 
 int fft2_dev(pm_plan* pl, const void* in, void* out, int dir, int batch) {

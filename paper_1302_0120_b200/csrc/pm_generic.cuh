@@ -119,6 +119,53 @@ __device__ __forceinline__ void gen_pass(const cx<T>* a, cx<T>* b, const cx<T>* 
     }
 }
 
+// All Stockham passes of one direction over the [L][TC] tile in A (B is the
+// ping-pong buffer); returns the buffer holding the result.
+template <typename T>
+__device__ __forceinline__ cx<T>* gen_passes(cx<T>* A, cx<T>* B, const cx<T>* __restrict__ tw, const GenPlan& gp,
+                                            int lgTC, int dir) {
+    for (int s = 0; s < gp.np; ++s) {
+        switch (gp.radix[s]) {
+            case 2: gen_pass<T, 2>(A, B, tw, gp.L, gp.ns[s], lgTC, dir); break;
+            case 3: gen_pass<T, 3>(A, B, tw, gp.L, gp.ns[s], lgTC, dir); break;
+            case 4: gen_pass<T, 4>(A, B, tw, gp.L, gp.ns[s], lgTC, dir); break;
+            case 5: gen_pass<T, 5>(A, B, tw, gp.L, gp.ns[s], lgTC, dir); break;
+            default: gen_pass<T, 7>(A, B, tw, gp.L, gp.ns[s], lgTC, dir); break;
+        }
+        __syncthreads();
+        cx<T>* tmp = A; A = B; B = tmp;
+    }
+    return A;
+}
+
+// Tile <-> global for TC transforms of length L starting at transform t0
+// (element n of transform t at t*tstride + n*estride).
+template <typename T>
+__device__ __forceinline__ void gen_gather(cx<T>* A, const cx<T>* src, int L, int lgTC, int t0, int tc,
+                                           long long tstride, long long estride) {
+    const int TC = 1 << lgTC;
+    const double inv_l = 1.0 / L;
+    for (int idx = threadIdx.x; idx < L * TC; idx += blockDim.x) {
+        int n, t;
+        if (estride == 1) { t = gen_div(idx, inv_l); n = idx - t * L; }
+        else { n = idx >> lgTC; t = idx & (TC - 1); }
+        A[n * TC + t] = t < tc ? src[(t0 + t) * tstride + n * estride] : mk<T>(T(0), T(0));
+    }
+    __syncthreads();
+}
+template <typename T>
+__device__ __forceinline__ void gen_scatter(const cx<T>* A, cx<T>* dst, int L, int lgTC, int t0, int tc,
+                                            long long tstride, long long estride, T scale) {
+    const int TC = 1 << lgTC;
+    const double inv_l = 1.0 / L;
+    for (int idx = threadIdx.x; idx < L * TC; idx += blockDim.x) {
+        int n, t;
+        if (estride == 1) { t = gen_div(idx, inv_l); n = idx - t * L; }
+        else { n = idx >> lgTC; t = idx & (TC - 1); }
+        if (t < tc) dst[(t0 + t) * tstride + n * estride] = cscale(A[n * TC + t], scale);
+    }
+}
+
 // One axis of the unitary 2-D DFT for `ntrans` transforms of length gp.L per
 // batch slice: element n of transform t at t*tstride + n*estride (+ slice *
 // bstride). Skips masks that are stopped (unless all_masks) or diverged.
@@ -164,6 +211,8 @@ __global__ void gen_fft_kernel(const cx<T>* in, cx<T>* out, const cx<T>* __restr
         if (t < tc) dst[(t0 + t) * tstride + n * estride] = cscale(A[n * TC + t], scale);
     }
 }
+
+struct GenSolveArgs;
 
 struct GenSolveArgs {
     SolveCtl ctl;
@@ -217,6 +266,104 @@ __global__ void gen_replace_kernel(cx<T>* f, const T* m, const double* thr_m, co
     if (reduce_ticket<3>(acc, g.part + (size_t)b * g.nblk * 3, g.ctr + b, g.nblk, blockIdx.x, tot) &&
         threadIdx.x == 0)
         decide(st, g.hist + ((size_t)b * g.hist_stride + (u_iter - 1)) * 4, g.ctl, u_iter, rec, tot);
+}
+
+// Column sweep of the mixed-radix solve, fused: ColFFT -> replace_m (+ the
+// metrics and decision of u_{u_iter}) -> ColIFFT on the work buffer `w`
+// (rows already transformed), in place; metrics_only leaves `w` untouched.
+template <typename T>
+__global__ void gen_col_sweep_kernel(cx<T>* w, const T* m, const double* thr_m, const double* escale,
+                                     const cx<T>* __restrict__ tw, GenPlan gp, int nx, int lgTC, GenSolveArgs g,
+                                     int u_iter, int metrics_only, int all_masks) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    const int b = blockIdx.y;
+    MaskState* st = g.st + b;
+    if (st->done || (!all_masks && st->stop)) return;
+    const bool dec = u_iter >= 1 && st->decided < u_iter && !st->stop;
+    const bool rec = dec && recorded(g.ctl, u_iter);
+    const bool gneed = dec && gap_needed(g.ctl, u_iter);
+    const int TC = 1 << lgTC, L = gp.L;
+    const int t0 = blockIdx.x * TC, tc = min(TC, nx - t0);
+    const T sc = T(1.0 / sqrt((double)L));
+    cx<T>* A = reinterpret_cast<cx<T>*>(smraw);
+    cx<T>* B = A + (size_t)L * TC;
+    cx<T>* wb = w + b * g.n;
+    const T* mb = m + b * g.n;
+    gen_gather<T>(A, wb, L, lgTC, t0, tc, 1, nx);
+    A = gen_passes<T>(A, B, tw, gp, lgTC, -1);
+    B = A == reinterpret_cast<cx<T>*>(smraw) ? A + (size_t)L * TC : reinterpret_cast<cx<T>*>(smraw);
+    const T thr = T(thr_m[b]);
+    const double es = escale[b];
+    double acc[3] = {0.0, 0.0, 0.0};
+    for (int idx = threadIdx.x; idx < L * TC; idx += blockDim.x) {
+        const int n = idx >> lgTC, t = idx & (TC - 1);
+        if (t >= tc) continue;
+        const cx<T> u = cscale(A[idx], sc);                      // u^ = F(u)
+        const T mm = mb[(long long)n * nx + t0 + t];
+        const cx<T> vh = replace_mod(u, mm, thr);
+        if (gneed) acc[0] += norm_sq_d(csub(u, vh));
+        if (rec) {
+            const double inten = norm_sq_d(u) * es;
+            const double m2 = (double)mm * (double)mm;
+            if (m2 > 0.0) {
+                const double dev = fabs(m2 - inten);
+                if (dev > g.ctl.t_lit * m2 && dev / m2 > g.ctl.t_lit)
+                    acc[1] += g.ctl.t_dark * dev / (g.ctl.t_lit * m2) - g.ctl.t_dark;
+            } else if (inten > g.ctl.t_dark) {
+                acc[2] += inten - g.ctl.t_dark;
+            }
+        }
+        A[idx] = vh;
+    }
+    __syncthreads();
+    if (!metrics_only) {
+        A = gen_passes<T>(A, B, tw, gp, lgTC, +1);
+        gen_scatter<T>(A, wb, L, lgTC, t0, tc, 1, nx, sc);
+    }
+    if (!dec) return;
+    double tot[3];
+    if (reduce_ticket<3>(acc, g.part + (size_t)b * g.nblk * 3, g.ctr + b, g.nblk, blockIdx.x, tot) &&
+        threadIdx.x == 0)
+        decide(st, g.hist + ((size_t)b * g.hist_stride + (u_iter - 1)) * 4, g.ctl, u_iter, rec, tot);
+}
+
+// Row sweep of the mixed-radix solve, fused: RowIFFT of the work buffer ->
+// u = P_S v into the iterate (non-finite check) -> RowFFT(u) back into the
+// work buffer for the next column sweep.
+template <typename T>
+__global__ void gen_row_sweep_kernel(cx<T>* w, cx<T>* u, const T* p, long long p_stride, const double* thr_p,
+                                     const cx<T>* __restrict__ tw, GenPlan gp, int ny, int lgTC, MaskState* st,
+                                     long long n, int it) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    const int b = blockIdx.y;
+    if (st[b].done || st[b].stop) return;
+    const int TC = 1 << lgTC, L = gp.L;
+    const int t0 = blockIdx.x * TC, tc = min(TC, ny - t0);
+    const T sc = T(1.0 / sqrt((double)L));
+    cx<T>* A = reinterpret_cast<cx<T>*>(smraw);
+    cx<T>* B = A + (size_t)L * TC;
+    cx<T>* wb = w + b * n;
+    cx<T>* ub = u + b * n;
+    const T* pb = p + b * p_stride;
+    gen_gather<T>(A, wb, L, lgTC, t0, tc, L, 1);
+    A = gen_passes<T>(A, B, tw, gp, lgTC, +1);
+    B = A == reinterpret_cast<cx<T>*>(smraw) ? A + (size_t)L * TC : reinterpret_cast<cx<T>*>(smraw);
+    const T thr = T(thr_p[b]);
+    T chk = T(0);
+    for (int idx = threadIdx.x; idx < L * TC; idx += blockDim.x) {
+        const int k = idx >> lgTC, t = idx & (TC - 1);      // element k of row t0 + t
+        if (t >= tc) continue;
+        const long long x = (long long)(t0 + t) * L + k;
+        T s2;
+        const cx<T> uu = replace_mod(cscale(A[idx], sc), pb[x], thr, s2);
+        chk += s2;
+        ub[x] = uu;
+        A[idx] = uu;
+    }
+    if (!isfinite(chk)) first_bad(&st[b].bad, it);
+    __syncthreads();
+    A = gen_passes<T>(A, B, tw, gp, lgTC, -1);
+    gen_scatter<T>(A, wb, L, lgTC, t0, tc, L, 1, sc);
 }
 
 // u = P_S v from the work buffer back into the iterate, non-finite check.
