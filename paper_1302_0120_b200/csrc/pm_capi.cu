@@ -395,6 +395,7 @@ struct pm_plan {
     void* gtwx = nullptr;             // exp(-2 pi i k / n_x), k < n_x, plan precision
     void* gtwy = nullptr;
     int gtc_r = 1, gtc_c = 1;         // transforms per CTA
+    int gnt_r = 256, gnt_c = 256;     // threads per CTA of the row / column kernels
     size_t gsm_r = 0, gsm_c = 0;      // their shared memory
     // TMA maps of the persistent column phase (pm_kernels.cuh col_phase)
     CUtensorMap tm_field{}, tm_field2{}, tm_m{};
@@ -854,12 +855,14 @@ bool gen_factor(int n, GenPlan* g) {
     g->L = n;
     g->np = 0;
     int rest = n, ns = 1;
-    const int order[] = {4, 2, 3, 5, 7};
+    const int order[] = {8, 4, 2, 3, 5, 7};
     for (int r : order) {
         while (rest % r == 0) {
             if (g->np == kGenMaxPasses) return false;
             g->radix[g->np] = r;
             g->ns[g->np] = ns;
+            g->step[g->np] = n / (ns * r);
+            g->mg[g->np] = ns == 1 ? 0u : 0xFFFFFFFFu / (unsigned)ns + 1u;
             ++g->np;
             ns *= r;
             rest /= r;
@@ -891,7 +894,12 @@ int gen_twiddles(int prec, int n, void** out) {
     return PM_OK;
 }
 
-constexpr size_t kGenSmem = 96 * 1024;   // two [L][TC] buffers per CTA
+constexpr size_t kGenSmem = 100 * 1024;  // preferred tile bytes per CTA (TC is halved down to 1 above it)
+
+int env_int(const char* name, int dflt) {
+    const char* v = std::getenv(name);
+    return v && *v ? std::atoi(v) : dflt;
+}
 
 int gen_setup(pm_plan* pl) {
     CKR(gen_twiddles(pl->prec, pl->nx, &pl->gtwx));
@@ -900,13 +908,15 @@ int gen_setup(pm_plan* pl) {
     // columns wide enough for >= 32-byte segments
     auto tc_for = [&](int L, int ntrans, int want) {
         int tc = want;
-        while (tc > 1 && (2 * (size_t)L * tc * pl->csz > kGenSmem || (ntrans + tc - 1) / tc < 148)) tc >>= 1;
+        while (tc > 1 && (gen_smem_bytes(L, tc, pl->csz) > kGenSmem || (ntrans + tc - 1) / tc < 148)) tc >>= 1;
         return tc;
     };
-    pl->gtc_r = tc_for(pl->nx, pl->ny, 4);
-    pl->gtc_c = tc_for(pl->ny, pl->nx, pl->csz == 8 ? 4 : 2);
-    pl->gsm_r = 2 * (size_t)pl->nx * pl->gtc_r * pl->csz;
-    pl->gsm_c = 2 * (size_t)pl->ny * pl->gtc_c * pl->csz;
+    pl->gtc_r = tc_for(pl->nx, pl->ny, env_int("PM_GEN_TCR", 2));
+    pl->gtc_c = tc_for(pl->ny, pl->nx, env_int("PM_GEN_TCC", 2));
+    pl->gnt_r = env_int("PM_GEN_NTR", 256);
+    pl->gnt_c = env_int("PM_GEN_NTC", 256);
+    pl->gsm_r = gen_smem_bytes(pl->nx, pl->gtc_r, pl->csz);
+    pl->gsm_c = gen_smem_bytes(pl->ny, pl->gtc_c, pl->csz);
     const size_t mx = std::max(pl->gsm_r, pl->gsm_c);
     cudaError_t e;
     if (pl->prec == PM_SINGLE) {
@@ -937,7 +947,7 @@ int gen_axis(pm_plan* pl, const void* in, void* out, int axis, int dir, int batc
     const dim3 grid((ntrans + TC - 1) / TC, batch);
     int lgTC = 0;
     while ((1 << lgTC) < TC) ++lgTC;
-    gen_fft_kernel<T><<<grid, 256, rows ? pl->gsm_r : pl->gsm_c, pl->stream>>>(
+    gen_fft_kernel<T><<<grid, rows ? pl->gnt_r : pl->gnt_c, rows ? pl->gsm_r : pl->gsm_c, pl->stream>>>(
         (const cx<T>*)in, (cx<T>*)out, (const cx<T>*)(rows ? pl->gtwx : pl->gtwy), g, ntrans, tstride, estride,
         (long long)pl->N, dir, scale, lgTC, st, all_masks);
     CK(cudaGetLastError());
@@ -1020,7 +1030,7 @@ int gen_col_sweep(pm_plan* pl, int u_iter, int metrics_only, int all_masks) {
     const dim3 grid((pl->nx + TC - 1) / TC, pl->s.batch);
     GenSolveArgs g = gen_args(pl);
     g.nblk = (int)grid.x;
-    gen_col_sweep_kernel<T><<<grid, 256, pl->gsm_c, pl->stream>>>(
+    gen_col_sweep_kernel<T><<<grid, pl->gnt_c, pl->gsm_c, pl->stream>>>(
         (cx<T>*)pl->tmp, (const T*)pl->s.m, pl->thrm, pl->escale, (const cx<T>*)pl->gtwy, pl->gy, pl->nx,
         lg_of(TC), g, u_iter, metrics_only, all_masks);
     CK(cudaGetLastError());
@@ -1033,7 +1043,7 @@ template <typename T>
 int gen_row_sweep(pm_plan* pl, int it) {
     const int TC = pl->gtc_r;
     const dim3 grid((pl->ny + TC - 1) / TC, pl->s.batch);
-    gen_row_sweep_kernel<T><<<grid, 256, pl->gsm_r, pl->stream>>>(
+    gen_row_sweep_kernel<T><<<grid, pl->gnt_r, pl->gsm_r, pl->stream>>>(
         (cx<T>*)pl->tmp, (cx<T>*)pl->field, (const T*)pl->s.p, pl->s.p_stride, pl->thrx, (const cx<T>*)pl->gtwx,
         pl->gx, pl->ny, lg_of(TC), pl->st, (long long)pl->N, it);
     CK(cudaGetLastError());

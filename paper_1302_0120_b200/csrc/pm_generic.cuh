@@ -1,5 +1,5 @@
-// Mixed-radix path for grids whose sides are not powers of two (radices 2,
-// 3, 4, 5, 7; n <= 4096), e.g. the paper's 800x600 SLM and
+// Mixed-radix path for grids whose sides are not powers of two (radices 8, 4, 2,
+// 3, 5, 7; n <= 4096), e.g. the paper's 800x600 SLM and
 // the reference's acceptance grid (tests/test_acceptance.py:118-128,200-205).
 //
 // The power-of-two path fuses each half iteration into one register-resident
@@ -29,6 +29,8 @@ struct GenPlan {
     int np;                      // passes
     int radix[kGenMaxPasses];    // radix of pass s
     int ns[kGenMaxPasses];       // product of the radices before pass s
+    int step[kGenMaxPasses];     // twiddle index step of pass s: L / (ns * radix)
+    unsigned mg[kGenMaxPasses];  // multiply-high magic of ns (0 for ns = 1)
 };
 
 // cos / sin (2 pi k / r) for the small odd radices, fp64-accurate.
@@ -66,50 +68,84 @@ __device__ __forceinline__ void gen_dft(cx<T>* x) {
         x[2] = mk<T>(s02.x - s13.x, s02.y - s13.y);
         x[1] = mk<T>(d02.x + r13.x, d02.y + r13.y);
         x[3] = mk<T>(d02.x - r13.x, d02.y - r13.y);
+    } else if constexpr (R == 8) {
+        // two radix-4 DFTs (even / odd samples) combined with W8^k
+        cx<T> e[4] = {x[0], x[2], x[4], x[6]}, o[4] = {x[1], x[3], x[5], x[7]};
+        gen_dft<T, 4, DIR>(e);
+        gen_dft<T, 4, DIR>(o);
+        const T h = T(0.70710678118654752440084436210485);
+        const cx<T> o1 = DIR < 0 ? mk<T>(h * (o[1].x + o[1].y), h * (o[1].y - o[1].x))
+                                 : mk<T>(h * (o[1].x - o[1].y), h * (o[1].y + o[1].x));
+        const cx<T> o2 = DIR < 0 ? mk<T>(o[2].y, -o[2].x) : mk<T>(-o[2].y, o[2].x);
+        const cx<T> o3 = DIR < 0 ? mk<T>(h * (o[3].y - o[3].x), -h * (o[3].x + o[3].y))
+                                 : mk<T>(-h * (o[3].x + o[3].y), h * (o[3].x - o[3].y));
+        x[0] = mk<T>(e[0].x + o[0].x, e[0].y + o[0].y);
+        x[4] = mk<T>(e[0].x - o[0].x, e[0].y - o[0].y);
+        x[1] = mk<T>(e[1].x + o1.x, e[1].y + o1.y);
+        x[5] = mk<T>(e[1].x - o1.x, e[1].y - o1.y);
+        x[2] = mk<T>(e[2].x + o2.x, e[2].y + o2.y);
+        x[6] = mk<T>(e[2].x - o2.x, e[2].y - o2.y);
+        x[3] = mk<T>(e[3].x + o3.x, e[3].y + o3.y);
+        x[7] = mk<T>(e[3].x - o3.x, e[3].y - o3.y);
     } else {
-        cx<T> y[R];
+        // odd R: pair the samples n and R - n (a = sum, b = difference), so
+        // y_j / y_{R-j} = x0 + sum_k c(jk) a_k  +/-  i DIR sum_k s(jk) b_k
+        constexpr int H = (R - 1) / 2;
+        cx<T> a[H], b[H];
 #pragma unroll
-        for (int k = 0; k < R; ++k) {
-            T re = x[0].x, im = x[0].y;
-#pragma unroll
-            for (int n = 1; n < R; ++n) {
-                const T c = T(gen_c(R, (n * k) % R)), s = T(DIR) * T(gen_s(R, (n * k) % R));
-                re += x[n].x * c - x[n].y * s;
-                im += x[n].x * s + x[n].y * c;
-            }
-            y[k] = mk<T>(re, im);
+        for (int k = 0; k < H; ++k) {
+            a[k] = mk<T>(x[k + 1].x + x[R - 1 - k].x, x[k + 1].y + x[R - 1 - k].y);
+            b[k] = mk<T>(x[k + 1].x - x[R - 1 - k].x, x[k + 1].y - x[R - 1 - k].y);
         }
+        const cx<T> x0 = x[0];
+        T sx = x0.x, sy = x0.y;
 #pragma unroll
-        for (int k = 0; k < R; ++k) x[k] = y[k];
+        for (int k = 0; k < H; ++k) { sx += a[k].x; sy += a[k].y; }
+        x[0] = mk<T>(sx, sy);
+#pragma unroll
+        for (int j = 1; j <= H; ++j) {
+            T rx = x0.x, ry = x0.y, ix = T(0), iy = T(0);
+#pragma unroll
+            for (int k = 0; k < H; ++k) {
+                const T c = T(gen_c(R, (j * (k + 1)) % R)), sn = T(DIR) * T(gen_s(R, (j * (k + 1)) % R));
+                rx += c * a[k].x;
+                ry += c * a[k].y;
+                ix += sn * b[k].x;
+                iy += sn * b[k].y;
+            }
+            // i * (ix + i iy) = -iy + i ix
+            x[j] = mk<T>(rx - iy, ry + ix);
+            x[R - j] = mk<T>(rx + iy, ry - ix);
+        }
     }
 }
 
-// x / d for 0 <= x, d <= 2^20 without an integer division: the fp64
-// product is within 1e-12 of the quotient, far inside 1/d of the next integer.
-__device__ __forceinline__ int gen_div(int x, double inv_d) { return (int)((double)x * inv_d + 1e-9); }
+// x / d for 0 <= x, d <= 4096 by a multiply-high: mg = ceil(2^32 / d) is
+// exact for x < 2^32 / d (d = 1 handled apart, its magic overflows;
+// computed on the host, GenPlan::mg).
+__device__ __forceinline__ int gen_div(int x, int d, unsigned mg) { return d == 1 ? x : (int)__umulhi((unsigned)x, mg); }
 
 // One Stockham pass of radix R over the TC transforms held in `a`
-// ([L][TC] layout, TC a power of two), into `b`. tw[k] = exp(-2 pi i k / L).
+// ([L][TC] layout, TC a power of two), into `b`. tw[k] = exp(-2 pi i k / L),
+// resident in shared memory.
 template <typename T, int R>
-__device__ __forceinline__ void gen_pass(const cx<T>* a, cx<T>* b, const cx<T>* __restrict__ tw, int L, int Ns,
-                                         int lgTC, int dir) {
+__device__ __forceinline__ void gen_pass(const cx<T>* a, cx<T>* b, const cx<T>* tw, int L, int Ns, int step,
+                                         unsigned mg, int lgTC, int dir) {
     const int TC = 1 << lgTC;
-    const int M = L / R;
-    const int step = L / (Ns * R);              // twiddle index step per (q * k); q * k * step < L
-    const double inv_ns = 1.0 / Ns;
+    const int M = L / R;                        // q * k * step < L
     for (int idx = threadIdx.x; idx < M * TC; idx += blockDim.x) {
         const int t = idx & (TC - 1), jb = idx >> lgTC;
-        const int g = gen_div(jb, inv_ns), k = jb - g * Ns;
+        const int g = gen_div(jb, Ns, mg), k = jb - g * Ns;
         cx<T> x[R];
 #pragma unroll
-        for (int q = 0; q < R; ++q) {
-            cx<T> v = a[(jb + q * M) * TC + t];
-            if (q > 0 && k > 0) {
-                const cx<T> w = __ldg(tw + q * k * step);
+        for (int q = 0; q < R; ++q) x[q] = a[(jb + q * M) * TC + t];
+        if (k > 0) {
+#pragma unroll
+            for (int q = 1; q < R; ++q) {
+                const cx<T> w = tw[q * k * step];
                 const T ws = dir < 0 ? w.y : -w.y;
-                v = mk<T>(v.x * w.x - v.y * ws, v.x * ws + v.y * w.x);
+                x[q] = mk<T>(x[q].x * w.x - x[q].y * ws, x[q].x * ws + x[q].y * w.x);
             }
-            x[q] = v;
         }
         if (dir < 0) gen_dft<T, R, -1>(x);
         else gen_dft<T, R, +1>(x);
@@ -122,15 +158,18 @@ __device__ __forceinline__ void gen_pass(const cx<T>* a, cx<T>* b, const cx<T>* 
 // All Stockham passes of one direction over the [L][TC] tile in A (B is the
 // ping-pong buffer); returns the buffer holding the result.
 template <typename T>
-__device__ __forceinline__ cx<T>* gen_passes(cx<T>* A, cx<T>* B, const cx<T>* __restrict__ tw, const GenPlan& gp,
-                                            int lgTC, int dir) {
+__device__ __forceinline__ cx<T>* gen_passes(cx<T>* A, cx<T>* B, const cx<T>* tw, const GenPlan& gp, int lgTC,
+                                            int dir) {
     for (int s = 0; s < gp.np; ++s) {
+        const int L = gp.L, Ns = gp.ns[s], st = gp.step[s];
+        const unsigned mg = gp.mg[s];
         switch (gp.radix[s]) {
-            case 2: gen_pass<T, 2>(A, B, tw, gp.L, gp.ns[s], lgTC, dir); break;
-            case 3: gen_pass<T, 3>(A, B, tw, gp.L, gp.ns[s], lgTC, dir); break;
-            case 4: gen_pass<T, 4>(A, B, tw, gp.L, gp.ns[s], lgTC, dir); break;
-            case 5: gen_pass<T, 5>(A, B, tw, gp.L, gp.ns[s], lgTC, dir); break;
-            default: gen_pass<T, 7>(A, B, tw, gp.L, gp.ns[s], lgTC, dir); break;
+            case 2: gen_pass<T, 2>(A, B, tw, L, Ns, st, mg, lgTC, dir); break;
+            case 3: gen_pass<T, 3>(A, B, tw, L, Ns, st, mg, lgTC, dir); break;
+            case 4: gen_pass<T, 4>(A, B, tw, L, Ns, st, mg, lgTC, dir); break;
+            case 5: gen_pass<T, 5>(A, B, tw, L, Ns, st, mg, lgTC, dir); break;
+            case 7: gen_pass<T, 7>(A, B, tw, L, Ns, st, mg, lgTC, dir); break;
+            default: gen_pass<T, 8>(A, B, tw, L, Ns, st, mg, lgTC, dir); break;
         }
         __syncthreads();
         cx<T>* tmp = A; A = B; B = tmp;
@@ -138,31 +177,63 @@ __device__ __forceinline__ cx<T>* gen_passes(cx<T>* A, cx<T>* B, const cx<T>* __
     return A;
 }
 
-// Tile <-> global for TC transforms of length L starting at transform t0
-// (element n of transform t at t*tstride + n*estride).
+// Shared-memory layout of the mixed-radix kernels: two [L][TC] complex
+// tiles, the length-L twiddle table and a [L][TC] real tile (p or m).
 template <typename T>
-__device__ __forceinline__ void gen_gather(cx<T>* A, const cx<T>* src, int L, int lgTC, int t0, int tc,
-                                           long long tstride, long long estride) {
-    const int TC = 1 << lgTC;
-    const double inv_l = 1.0 / L;
-    for (int idx = threadIdx.x; idx < L * TC; idx += blockDim.x) {
-        int n, t;
-        if (estride == 1) { t = gen_div(idx, inv_l); n = idx - t * L; }
-        else { n = idx >> lgTC; t = idx & (TC - 1); }
-        A[n * TC + t] = t < tc ? src[(t0 + t) * tstride + n * estride] : mk<T>(T(0), T(0));
+struct GenSmem {
+    cx<T>* A;
+    cx<T>* B;
+    cx<T>* tw;
+    T* g;
+    __device__ GenSmem(unsigned char* raw, int L, int TC) {
+        A = reinterpret_cast<cx<T>*>(raw);
+        B = A + (size_t)L * TC;
+        tw = B + (size_t)L * TC;
+        g = reinterpret_cast<T*>(tw + L);
     }
-    __syncthreads();
+};
+__host__ __device__ constexpr size_t gen_smem_bytes(int L, int TC, int csz) {
+    return (2 * (size_t)L * TC + L) * csz + (size_t)L * TC * (csz / 2);
+}
+
+// Asynchronous copies into the tiles (cp.async; the caller commits / waits):
+// the twiddle table, and TC transforms of length L starting at transform t0
+// (element n of transform t at t*tstride + n*estride), complex or real.
+template <typename T>
+__device__ __forceinline__ void gen_load_tw(cx<T>* tw, const cx<T>* src, int L) {
+    for (int i = threadIdx.x; i < L; i += blockDim.x) cp_async<sizeof(cx<T>)>(tw + i, src + i);
+}
+template <typename E>
+__device__ __forceinline__ void gen_gather(E* A, const E* src, int L, int lgTC, int t0, int tc, long long tstride,
+                                           long long estride, E zero) {
+    const int TC = 1 << lgTC;
+    if (estride == 1) {                           // rows: walk along n for coalescing
+        for (int t = 0; t < TC; ++t)
+            for (int n = threadIdx.x; n < L; n += blockDim.x) {
+                if (t < tc) cp_async<sizeof(E)>(A + n * TC + t, src + (t0 + t) * tstride + n);
+                else A[n * TC + t] = zero;
+            }
+    } else {                                      // columns: walk along t
+        for (int idx = threadIdx.x; idx < L * TC; idx += blockDim.x) {
+            const int n = idx >> lgTC, t = idx & (TC - 1);
+            if (t < tc) cp_async<sizeof(E)>(A + idx, src + (t0 + t) * tstride + n * estride);
+            else A[idx] = zero;
+        }
+    }
 }
 template <typename T>
 __device__ __forceinline__ void gen_scatter(const cx<T>* A, cx<T>* dst, int L, int lgTC, int t0, int tc,
                                             long long tstride, long long estride, T scale) {
     const int TC = 1 << lgTC;
-    const double inv_l = 1.0 / L;
-    for (int idx = threadIdx.x; idx < L * TC; idx += blockDim.x) {
-        int n, t;
-        if (estride == 1) { t = gen_div(idx, inv_l); n = idx - t * L; }
-        else { n = idx >> lgTC; t = idx & (TC - 1); }
-        if (t < tc) dst[(t0 + t) * tstride + n * estride] = cscale(A[n * TC + t], scale);
+    if (estride == 1) {
+        for (int t = 0; t < tc; ++t)
+            for (int n = threadIdx.x; n < L; n += blockDim.x)
+                dst[(t0 + t) * tstride + n] = cscale(A[n * TC + t], scale);
+    } else {
+        for (int idx = threadIdx.x; idx < L * TC; idx += blockDim.x) {
+            const int n = idx >> lgTC, t = idx & (TC - 1);
+            if (t < tc) dst[(t0 + t) * tstride + n * estride] = cscale(A[idx], scale);
+        }
     }
 }
 
@@ -173,43 +244,19 @@ template <typename T>
 __global__ void gen_fft_kernel(const cx<T>* in, cx<T>* out, const cx<T>* __restrict__ tw, GenPlan gp, int ntrans,
                                long long tstride, long long estride, long long bstride, int dir, T scale, int lgTC,
                                const MaskState* st, int all_masks) {
-    const int TC = 1 << lgTC;
     extern __shared__ __align__(16) unsigned char smraw[];
     const int b = blockIdx.y;
     if (st && (st[b].done || (!all_masks && st[b].stop))) return;
-    const int L = gp.L;
-    const int t0 = blockIdx.x * TC;
-    const int tc = min(TC, ntrans - t0);
-    cx<T>* A = reinterpret_cast<cx<T>*>(smraw);
-    cx<T>* B = A + (size_t)L * TC;
-    const cx<T>* src = in + b * bstride;
-    cx<T>* dst = out + b * bstride;
-    const bool contig_e = estride == 1;          // rows: walk along n; columns: walk along t
-    const double inv_l = 1.0 / L;
-    for (int idx = threadIdx.x; idx < L * TC; idx += blockDim.x) {
-        int n, t;
-        if (contig_e) { t = gen_div(idx, inv_l); n = idx - t * L; }
-        else { n = idx >> lgTC; t = idx & (TC - 1); }
-        A[n * TC + t] = t < tc ? src[(t0 + t) * tstride + n * estride] : mk<T>(T(0), T(0));
-    }
+    const int TC = 1 << lgTC, L = gp.L;
+    const int t0 = blockIdx.x * TC, tc = min(TC, ntrans - t0);
+    GenSmem<T> sm(smraw, L, TC);
+    gen_load_tw<T>(sm.tw, tw, L);
+    gen_gather<cx<T>>(sm.A, in + b * bstride, L, lgTC, t0, tc, tstride, estride, mk<T>(T(0), T(0)));
+    cp_async_commit();
+    cp_async_wait_all();
     __syncthreads();
-    for (int s = 0; s < gp.np; ++s) {
-        switch (gp.radix[s]) {
-            case 2: gen_pass<T, 2>(A, B, tw, L, gp.ns[s], lgTC, dir); break;
-            case 3: gen_pass<T, 3>(A, B, tw, L, gp.ns[s], lgTC, dir); break;
-            case 4: gen_pass<T, 4>(A, B, tw, L, gp.ns[s], lgTC, dir); break;
-            case 5: gen_pass<T, 5>(A, B, tw, L, gp.ns[s], lgTC, dir); break;
-            default: gen_pass<T, 7>(A, B, tw, L, gp.ns[s], lgTC, dir); break;
-        }
-        __syncthreads();
-        cx<T>* tmp = A; A = B; B = tmp;
-    }
-    for (int idx = threadIdx.x; idx < L * TC; idx += blockDim.x) {
-        int n, t;
-        if (contig_e) { t = gen_div(idx, inv_l); n = idx - t * L; }
-        else { n = idx >> lgTC; t = idx & (TC - 1); }
-        if (t < tc) dst[(t0 + t) * tstride + n * estride] = cscale(A[n * TC + t], scale);
-    }
+    const cx<T>* R = gen_passes<T>(sm.A, sm.B, sm.tw, gp, lgTC, dir);
+    gen_scatter<T>(R, out + b * bstride, L, lgTC, t0, tc, tstride, estride, scale);
 }
 
 struct GenSolveArgs;
@@ -285,21 +332,27 @@ __global__ void gen_col_sweep_kernel(cx<T>* w, const T* m, const double* thr_m, 
     const int TC = 1 << lgTC, L = gp.L;
     const int t0 = blockIdx.x * TC, tc = min(TC, nx - t0);
     const T sc = T(1.0 / sqrt((double)L));
-    cx<T>* A = reinterpret_cast<cx<T>*>(smraw);
-    cx<T>* B = A + (size_t)L * TC;
+    GenSmem<T> sm(smraw, L, TC);
     cx<T>* wb = w + b * g.n;
-    const T* mb = m + b * g.n;
-    gen_gather<T>(A, wb, L, lgTC, t0, tc, 1, nx);
-    A = gen_passes<T>(A, B, tw, gp, lgTC, -1);
-    B = A == reinterpret_cast<cx<T>*>(smraw) ? A + (size_t)L * TC : reinterpret_cast<cx<T>*>(smraw);
+    gen_load_tw<T>(sm.tw, tw, L);
+    gen_gather<cx<T>>(sm.A, wb, L, lgTC, t0, tc, 1, nx, mk<T>(T(0), T(0)));
+    cp_async_commit();
+    gen_gather<T>(sm.g, m + b * g.n, L, lgTC, t0, tc, 1, nx, T(0));    // m, in flight during the passes
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    cx<T>* A = gen_passes<T>(sm.A, sm.B, sm.tw, gp, lgTC, -1);
+    cx<T>* B = A == sm.A ? sm.B : sm.A;
+    cp_async_wait<0>();
+    __syncthreads();
     const T thr = T(thr_m[b]);
     const double es = escale[b];
     double acc[3] = {0.0, 0.0, 0.0};
     for (int idx = threadIdx.x; idx < L * TC; idx += blockDim.x) {
-        const int n = idx >> lgTC, t = idx & (TC - 1);
+        const int t = idx & (TC - 1);
         if (t >= tc) continue;
         const cx<T> u = cscale(A[idx], sc);                      // u^ = F(u)
-        const T mm = mb[(long long)n * nx + t0 + t];
+        const T mm = sm.g[idx];
         const cx<T> vh = replace_mod(u, mm, thr);
         if (gneed) acc[0] += norm_sq_d(csub(u, vh));
         if (rec) {
@@ -317,7 +370,7 @@ __global__ void gen_col_sweep_kernel(cx<T>* w, const T* m, const double* thr_m, 
     }
     __syncthreads();
     if (!metrics_only) {
-        A = gen_passes<T>(A, B, tw, gp, lgTC, +1);
+        A = gen_passes<T>(A, B, sm.tw, gp, lgTC, +1);
         gen_scatter<T>(A, wb, L, lgTC, t0, tc, 1, nx, sc);
     }
     if (!dec) return;
@@ -340,29 +393,34 @@ __global__ void gen_row_sweep_kernel(cx<T>* w, cx<T>* u, const T* p, long long p
     const int TC = 1 << lgTC, L = gp.L;
     const int t0 = blockIdx.x * TC, tc = min(TC, ny - t0);
     const T sc = T(1.0 / sqrt((double)L));
-    cx<T>* A = reinterpret_cast<cx<T>*>(smraw);
-    cx<T>* B = A + (size_t)L * TC;
+    GenSmem<T> sm(smraw, L, TC);
     cx<T>* wb = w + b * n;
     cx<T>* ub = u + b * n;
-    const T* pb = p + b * p_stride;
-    gen_gather<T>(A, wb, L, lgTC, t0, tc, L, 1);
-    A = gen_passes<T>(A, B, tw, gp, lgTC, +1);
-    B = A == reinterpret_cast<cx<T>*>(smraw) ? A + (size_t)L * TC : reinterpret_cast<cx<T>*>(smraw);
+    gen_load_tw<T>(sm.tw, tw, L);
+    gen_gather<cx<T>>(sm.A, wb, L, lgTC, t0, tc, L, 1, mk<T>(T(0), T(0)));
+    cp_async_commit();
+    gen_gather<T>(sm.g, p + b * p_stride, L, lgTC, t0, tc, L, 1, T(0));  // p, in flight during the passes
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    cx<T>* A = gen_passes<T>(sm.A, sm.B, sm.tw, gp, lgTC, +1);
+    cx<T>* B = A == sm.A ? sm.B : sm.A;
+    cp_async_wait<0>();
+    __syncthreads();
     const T thr = T(thr_p[b]);
     T chk = T(0);
     for (int idx = threadIdx.x; idx < L * TC; idx += blockDim.x) {
         const int k = idx >> lgTC, t = idx & (TC - 1);      // element k of row t0 + t
         if (t >= tc) continue;
-        const long long x = (long long)(t0 + t) * L + k;
         T s2;
-        const cx<T> uu = replace_mod(cscale(A[idx], sc), pb[x], thr, s2);
+        const cx<T> uu = replace_mod(cscale(A[idx], sc), sm.g[idx], thr, s2);
         chk += s2;
-        ub[x] = uu;
         A[idx] = uu;
     }
     if (!isfinite(chk)) first_bad(&st[b].bad, it);
     __syncthreads();
-    A = gen_passes<T>(A, B, tw, gp, lgTC, -1);
+    gen_scatter<T>(A, ub, L, lgTC, t0, tc, L, 1, T(1));     // the iterate, coalesced along the row
+    A = gen_passes<T>(A, B, sm.tw, gp, lgTC, -1);
     gen_scatter<T>(A, wb, L, lgTC, t0, tc, L, 1, sc);
 }
 

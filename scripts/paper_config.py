@@ -17,6 +17,8 @@ mm = torch.from_numpy(m[None].astype(np.float32)).pin_memory().numpy()
 out = torch.empty((1, 600, 800), dtype=torch.float64).pin_memory().numpy()
 for _ in range(3):
     r = solve_stack(pp, mm, cfg, out_phases=out)
+if '--once' in sys.argv:        # for ncu: warm-up solves only
+    sys.exit(0)
 e2e, dev = [], []
 for _ in range(20):
     torch.cuda.synchronize()
