@@ -158,6 +158,16 @@ int pm_sum(int device, const double *data, long long count, double *out);
 int pm_phases(int device, const void *u, long long count, int precision,
               double zero_tol, double *out);
 
+/*
+ * Seeded random-phase start: out[b] = m[b] e^{i phi}, phi = numpy's
+ * default_rng(seed).uniform(0, 2pi, count) draws from the PCG64 state
+ * rng = {state hi, lo, inc hi, lo}, generated on the device (one draw per
+ * pixel, shared by the `batch` masks). Host buffers; replaces the host side
+ * of initial_iterate's random branch (src/solver.py:100-103).
+ */
+int pm_random_start(int device, const void *m, long long count, int batch, int precision,
+                    const unsigned long long rng[4], void *out);
+
 /* --------------------------------------------------------------- solve */
 
 typedef struct pm_params {
@@ -169,6 +179,12 @@ typedef struct pm_params {
     double t_lit, t_dark;    /* ErrorTolerances (src/metrics.py:30-39)          */
     int    p_per_mask;       /* p has `batch` grids (1) or one shared grid (0)  */
     int    init_complex;     /* 1: `m_init` holds complex Fourier-plane starts  */
+    int    init_random;      /* 1: start from m e^{i phi}, phi drawn on the
+                                device from the PCG64 state below exactly as
+                                np.random.default_rng(seed).uniform(0, 2pi)
+                                (SolveConfig.random_phase_init, :100-103)      */
+    unsigned long long rng[4]; /* PCG64 state hi, lo, inc hi, lo after seeding
+                                  (bit_generator.state)                        */
 } pm_params;
 
 typedef struct pm_result {

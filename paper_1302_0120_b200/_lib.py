@@ -42,6 +42,8 @@ class pm_params(C.Structure):
         ("t_dark", C.c_double),
         ("p_per_mask", C.c_int),
         ("init_complex", C.c_int),
+        ("init_random", C.c_int),
+        ("rng", C.c_ulonglong * 4),
     ]
 
 
@@ -83,6 +85,7 @@ SIGNATURES = {
     "pm_norm2": (_I, [_I, _VP, _LL, _I, C.POINTER(_D)]),
     "pm_sum": (_I, [_I, _VP, _LL, C.POINTER(_D)]),
     "pm_phases": (_I, [_I, _VP, _LL, _I, _D, _VP]),
+    "pm_random_start": (_I, [_I, _VP, _LL, _I, _I, _VP, _VP]),
     "pm_solve": (_I, [_VP, _VP, _VP, _VP, _I, C.POINTER(pm_params), _VP, _VP, _VP,
                       C.POINTER(pm_result)]),
     "pm_solve_device": (_I, [_VP, _VP, _VP, _VP, _I, C.POINTER(pm_params), _VP, _VP, _VP,
@@ -291,6 +294,30 @@ def phases(u: np.ndarray, zero_tol: float = 0.0, device: int = 0) -> np.ndarray:
     prec = 0 if a.dtype == np.complex64 else 1
     out = np.empty(a.shape, dtype=np.float64)
     check(load().pm_phases(device, ptr(a), a.size, prec, float(zero_tol), ptr(out)), "pm_phases")
+    return out
+
+
+def pcg64_state(seed: int) -> np.ndarray:
+    """The PCG64 state {state hi, lo, inc hi, lo} of np.random.default_rng(seed)
+    right after seeding (SeedSequence hashing stays on the host)."""
+    st = np.random.default_rng(seed).bit_generator.state["state"]
+    m64 = (1 << 64) - 1
+    return np.array([st["state"] >> 64, st["state"] & m64, st["inc"] >> 64, st["inc"] & m64],
+                    dtype=np.uint64)
+
+
+def random_start(m: np.ndarray, complex_dtype, seed: int, device: int = 0) -> np.ndarray:
+    """m e^{i phi} with phi = default_rng(seed).uniform(0, 2 pi, m.shape[-2:])
+    drawn on the device (pm_random_start); m is (n_y, n_x) or a (B, n_y, n_x)
+    stack sharing the draws."""
+    prec = 0 if np.dtype(complex_dtype) == np.complex64 else 1
+    a = np.ascontiguousarray(m, dtype=np.float32 if prec == 0 else np.float64)
+    count = a.shape[-1] * a.shape[-2]
+    batch = a.size // count
+    out = np.empty(a.shape, dtype=complex_dtype)
+    rng = pcg64_state(seed)
+    check(load().pm_random_start(device, ptr(a), count, batch, prec, ptr(rng), ptr(out)),
+          "pm_random_start")
     return out
 
 

@@ -80,8 +80,10 @@ def solve_stack(p: np.ndarray, m_stack: np.ndarray, cfg: SolveConfig, device: in
     full-speed transfers); ``out_phases`` (B, n_y, n_x) float64 may be a
     caller-owned (e.g. pinned) buffer for the mask; ``levels=True`` also
     returns the 8-bit SLM levels computed on the device; ``init`` (B, n_y, n_x)
-    complex are Fourier-plane starts m e^{i phi} (random-phase init,
-    src/solver.py:100-103) instead of m. The per-mask energy
+    complex are caller-chosen Fourier-plane starts instead of m; without it,
+    ``cfg.random_phase_init`` draws the seeded phases on the device
+    (src/solver.py:100-103, the same draws for every mask, as a reference
+    solve per image re-seeds). The per-mask energy
     sum(m^2) and the zero tolerances are reduced on the device.
     """
     m_stack = np.asarray(m_stack)

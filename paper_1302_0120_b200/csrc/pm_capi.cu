@@ -19,6 +19,7 @@
 
 #include "phasemask_b200.h"
 #include "pm_generic.cuh"
+#include "pm_rng.cuh"
 #include "pm_kernels.cuh"
 #include "pm_table.h"
 
@@ -911,7 +912,7 @@ int gen_setup(pm_plan* pl) {
         while (tc > 1 && (gen_smem_bytes(L, tc, pl->csz) > kGenSmem || (ntrans + tc - 1) / tc < 148)) tc >>= 1;
         return tc;
     };
-    pl->gtc_r = tc_for(pl->nx, pl->ny, env_int("PM_GEN_TCR", 2));
+    pl->gtc_r = tc_for(pl->nx, pl->ny, env_int("PM_GEN_TCR", 1));
     pl->gtc_c = tc_for(pl->ny, pl->nx, env_int("PM_GEN_TCC", 2));
     pl->gnt_r = env_int("PM_GEN_NTR", 256);
     pl->gnt_c = env_int("PM_GEN_NTC", 256);
@@ -1132,6 +1133,27 @@ int check_plan(pm_plan* pl) {
 }
 
 // -------------------------------------------------------------- solve
+// m e^{i phi} starts for `batch` masks of n pixels from the PCG64 state.
+int enqueue_random_start(int prec, const void* d_m, void* d_out, long long n, int batch,
+                         const unsigned long long rng[4], cudaStream_t stream) {
+    const int threads = 256;
+    const int blocks = (int)std::max<long long>(1, std::min<long long>((n + threads - 1) / threads, 148 * 8));
+    const u128 inc = u128_of(rng[2], rng[3]);
+    const PcgJump j = pcg_jump(inc, (unsigned long long)blocks * threads);
+    const auto hi = [](u128 v) { return (unsigned long long)(v >> 64); };
+    const auto lo = [](u128 v) { return (unsigned long long)v; };
+    if (prec == PM_SINGLE)
+        random_start_kernel<float><<<blocks, threads, 0, stream>>>(
+            (const float*)d_m, (float2*)d_out, n, batch, rng[0], rng[1], rng[2], rng[3], hi(j.mult), lo(j.mult),
+            hi(j.plus), lo(j.plus));
+    else
+        random_start_kernel<double><<<blocks, threads, 0, stream>>>(
+            (const double*)d_m, (double2*)d_out, n, batch, rng[0], rng[1], rng[2], rng[3], hi(j.mult), lo(j.mult),
+            hi(j.plus), lo(j.plus));
+    CK(cudaGetLastError());
+    return PM_OK;
+}
+
 int validate_params(const pm_params* prm, int batch) {
     if (!prm) return set_err(PM_ERR_ARG, "null params");
     if (batch < 1) return set_err(PM_ERR_ARG, "batch must be >= 1");
@@ -1141,6 +1163,25 @@ int validate_params(const pm_params* prm, int batch) {
         return set_err(PM_ERR_ARG, "algorithm must be 0 (GS) or 1 (RAAR)");
     if (prm->algorithm == PM_ALGO_RAAR && !std::isfinite(prm->beta))
         return set_err(PM_ERR_ARG, "RAAR beta must be finite");
+    if (prm->init_complex && prm->init_random)
+        return set_err(PM_ERR_ARG, "init_complex and init_random are exclusive");
+    return PM_OK;
+}
+
+// The Fourier-plane start of the session's masks into the field: the
+// caller's complex starts (init_complex) or the seeded random phases
+// generated on the device (init_random); the solve then runs its complex
+// start path for both.
+int stage_start(pm_plan* pl, const void* init, cudaMemcpyKind kind) {
+    auto& s = pl->s;
+    if (s.prm.init_complex) {
+        if (!init) return set_err(PM_ERR_ARG, "init_complex set but m_init is NULL");
+        CK(cudaMemcpyAsync(pl->field, init, (size_t)s.batch * pl->N * pl->csz, kind, pl->stream));
+    } else if (s.prm.init_random) {
+        CKR(enqueue_random_start(pl->prec, s.m, pl->field, (long long)pl->N, s.batch, s.prm.rng, pl->stream));
+        pl->launches++;
+        s.prm.init_complex = 1;
+    }
     return PM_OK;
 }
 
@@ -1826,6 +1867,37 @@ int pm_sum(int device, const double* data, long long count, double* out) {
     return PM_OK;
 }
 
+int pm_random_start(int device, const void* m, long long count, int batch, int precision,
+                    const unsigned long long rng[4], void* out) {
+    if (!m || !out || !rng || count < 1 || batch < 1) return set_err(PM_ERR_ARG, "empty input");
+    if (precision != PM_SINGLE && precision != PM_DOUBLE) return set_err(PM_ERR_ARG, "bad precision");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return set_err(PM_ERR_CUDA, "no CUDA device available (phasemask_b200 has no CPU fallback)");
+    }
+    CK(cudaSetDevice(device));
+    const size_t rsz = precision == PM_SINGLE ? 4 : 8, total = (size_t)count * batch;
+    void *dm = nullptr, *dout = nullptr;
+    CK(cudaMalloc(&dm, total * rsz));
+    cudaError_t e = cudaMalloc(&dout, total * 2 * rsz);
+    if (e != cudaSuccess) {
+        cudaFree(dm);
+        return cuda_err(e, "cudaMalloc");
+    }
+    int rc = PM_OK;
+    e = cudaMemcpy(dm, m, total * rsz, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) {
+        rc = enqueue_random_start(precision, dm, dout, count, batch, rng, 0);
+        if (rc == PM_OK) e = cudaMemcpy(out, dout, total * 2 * rsz, cudaMemcpyDeviceToHost);
+    }
+    cudaFree(dm);
+    cudaFree(dout);
+    if (rc != PM_OK) return rc;
+    if (e != cudaSuccess) return cuda_err(e, "pm_random_start");
+    return PM_OK;
+}
+
 int pm_phases(int device, const void* u, long long count, int precision, double zero_tol, double* out) {
     if (!u || !out || count < 1) return set_err(PM_ERR_ARG, "empty input");
     int ndev = 0;
@@ -1867,11 +1939,7 @@ static int solve_core(pm_plan* pl, const void* d_p, const void* d_m, const void*
     CKR(session_setup(pl, d_p, d_m, batch, prm, tol_p, tol_m, energy));
     auto& s = pl->s;
     const size_t N = pl->N;
-    if (prm->init_complex) {
-        if (!d_init) return set_err(PM_ERR_ARG, "init_complex set but m_init is NULL");
-        CK(cudaMemcpyAsync(pl->field, d_init, batch * N * pl->csz,
-                           host_io ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, pl->stream));
-    }
+    CKR(stage_start(pl, d_init, host_io ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice));
     if (host_io) {
         CKR(ensure_outputs(pl, res && res->phases, res && res->levels, res && res->u_star, res && res->v_star));
         s.phases = (res && res->phases) ? pl->phases : nullptr;
@@ -1949,10 +2017,7 @@ int pm_solve_begin(pm_plan* pl, const void* p, const void* m, const void* m_init
                        pl->stream));
     CK(cudaMemcpyAsync(pl->mbuf, m, batch * N * pl->rsz, cudaMemcpyHostToDevice, pl->stream));
     CKR(session_setup(pl, pl->pbuf, pl->mbuf, batch, prm, tol_p, tol_m, energy));
-    if (prm->init_complex) {
-        if (!m_init) return set_err(PM_ERR_ARG, "init_complex set but m_init is NULL");
-        CK(cudaMemcpyAsync(pl->field, m_init, batch * N * pl->csz, cudaMemcpyHostToDevice, pl->stream));
-    }
+    CKR(stage_start(pl, m_init, cudaMemcpyHostToDevice));
     CK(cudaEventRecord(pl->ev0, pl->stream));
     CKR(enqueue_begin(pl));
     CK(cudaStreamSynchronize(pl->stream));

@@ -120,18 +120,20 @@ def default_amplitude(m: RealGrid, precision: Precision = DOUBLE) -> RealGrid:
     return RealGrid(m.spec, np.full(m.spec.shape, level))
 
 
-def _initial_fourier(m_data: np.ndarray, precision: Precision, random_phases: bool, seed: int):
+def _initial_fourier(m_data: np.ndarray, precision: Precision, random_phases: bool, seed: int,
+                     device: int = 0):
+    """Fourier-plane start m e^{i phi} for the seeded random branch
+    (src/solver.py:100-103), drawn on the device with numpy's PCG64 stream."""
     if random_phases:
-        rng = np.random.default_rng(seed)
-        phi = rng.uniform(0.0, 2 * np.pi, m_data.shape)
-        return (m_data * np.exp(1j * phi)).astype(precision.complex_dtype)
+        return _lib.random_start(m_data, precision.complex_dtype, seed, device)
     return None
 
 
 def initial_iterate(m: FourierConstraint, provider: FftProvider,
                     random_phases: bool = False, seed: int = 0) -> Field:
     """u0 = F^-1(m e^{i phi}), phi = 0 unless seeded random (src/solver.py:93-108)."""
-    data = _initial_fourier(m.m.data, provider.precision, random_phases, seed)
+    data = _initial_fourier(m.m.data, provider.precision, random_phases, seed,
+                            getattr(provider, "device", 0))
     if data is None:
         data = m.m.data.astype(np.complex128).astype(provider.precision.complex_dtype)
     return provider.inverse(Field(m.m.spec, data, FOURIER_PLANE))
@@ -148,6 +150,10 @@ def _params(cfg: SolveConfig, p_per_mask: bool, init_complex: bool) -> _lib.pm_p
     prm.t_dark = float(cfg.tolerances.t_dark)
     prm.p_per_mask = int(p_per_mask)
     prm.init_complex = int(init_complex)
+    if cfg.random_phase_init and not init_complex:
+        # phi drawn on the device from the seeded PCG64 stream (src/solver.py:100-103)
+        prm.init_random = 1
+        prm.rng[:] = [int(v) for v in _lib.pcg64_state(cfg.seed)]
     return prm
 
 
@@ -199,8 +205,8 @@ def solve(c: SlmConstraint, m: FourierConstraint, cfg: SolveConfig,
     tol_p = np.array([c.zero_tol])
     tol_m = np.array([m.zero_tol])
     energy = np.array([float((m.m.data.astype(np.float64) ** 2).sum())])
-    init = _initial_fourier(m.m.data, prec, cfg.random_phase_init, cfg.seed)
-    prm = _params(cfg, False, init is not None)
+    init = None                      # random-phase starts are drawn on the device
+    prm = _params(cfg, False, False)
 
     K = cfg.max_iters
     N = spec.n
