@@ -168,6 +168,20 @@ int pm_phases(int device, const void *u, long long count, int precision,
 int pm_random_start(int device, const void *m, long long count, int batch, int precision,
                     const unsigned long long rng[4], void *out);
 
+/*
+ * Reconstructed intensity and its display image for `batch` fields u
+ * (host, complex, plan precision): I = |F u|^2 in fp64, scaled by
+ * target_energy[b] / sum(I) when target_energy is non-NULL
+ * (metrics.reconstructed_intensity, src/metrics.py:74-87; a zero sum fails
+ * with PM_ERR_ARG "reconstruction carries no energy"); intensity (nullable)
+ * receives I in DFT order, log_image (nullable) the 8-bit log-scale image in
+ * centred order, round(255 (log10(max(I/max I, floor)) - log10 floor) /
+ * -log10 floor) (service._log_scale_u8 after to_centered_order,
+ * src/service.py:91-95,189-194).
+ */
+int pm_recon_image(pm_plan *plan, const void *u, int batch, const double *target_energy,
+                   double log_floor, uint8_t *log_image, double *intensity);
+
 /* --------------------------------------------------------------- solve */
 
 typedef struct pm_params {

@@ -86,6 +86,7 @@ SIGNATURES = {
     "pm_sum": (_I, [_I, _VP, _LL, C.POINTER(_D)]),
     "pm_phases": (_I, [_I, _VP, _LL, _I, _D, _VP]),
     "pm_random_start": (_I, [_I, _VP, _LL, _I, _I, _VP, _VP]),
+    "pm_recon_image": (_I, [_VP, _VP, _I, _VP, _D, _VP, _VP]),
     "pm_solve": (_I, [_VP, _VP, _VP, _VP, _I, C.POINTER(pm_params), _VP, _VP, _VP,
                       C.POINTER(pm_result)]),
     "pm_solve_device": (_I, [_VP, _VP, _VP, _VP, _I, C.POINTER(pm_params), _VP, _VP, _VP,
@@ -257,6 +258,23 @@ class Plan:
             check(self.lib.pm_gap(self.handle, ptr(x), ptr(pp), ptr(mm), float(tol_p), float(tol_m),
                                   C.byref(g)), "pm_gap")
         return g.value
+
+    def recon_image(self, u, target_energy=None, log_floor=None, intensity=True):
+        """(intensity or None, log image or None) of pm_recon_image for a
+        (n_y, n_x) field or a (B, n_y, n_x) stack; target_energy: scalar or
+        per-field array (None: unscaled)."""
+        x = np.ascontiguousarray(u, dtype=self.complex_dtype)
+        shape = x.shape
+        batch = x.size // (shape[-1] * shape[-2])
+        en = None if target_energy is None else np.ascontiguousarray(
+            np.broadcast_to(np.asarray(target_energy, dtype=np.float64), (batch,)))
+        inten = np.empty(shape, dtype=np.float64) if intensity else None
+        img = np.empty(shape, dtype=np.uint8) if log_floor is not None else None
+        with self.lock:
+            check(self.lib.pm_recon_image(self.handle, ptr(x), batch, ptr(en),
+                                          float(log_floor or 0.0), ptr(img), ptr(inten)),
+                  "pm_recon_image")
+        return inten, img
 
     def time_sweep(self, which: int, batch: int, reps: int) -> float:
         ms = C.c_float(0)

@@ -80,6 +80,19 @@ __device__ __forceinline__ double block_sum(double x) {
     return s;
 }
 
+__device__ __forceinline__ double block_max(double x) {
+    __shared__ double wm[32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) x = fmax(x, __shfl_xor_sync(0xffffffffu, x, o));
+    if (lane == 0) wm[warp] = x;
+    __syncthreads();
+    double m = 0.0;
+    if (threadIdx.x == 0)
+        for (int w = 0; w < (int)((blockDim.x + 31) >> 5); ++w) m = fmax(m, wm[w]);
+    return m;
+}
+
 template <typename TIn>
 __device__ __forceinline__ double sq_mag(const TIn* d, long long i);
 template <> __device__ __forceinline__ double sq_mag<float>(const float* d, long long i) {
@@ -151,6 +164,78 @@ __global__ void phases_kernel(const cx<T>* u, long long n, T tol, double* out) {
         const T mag = sqrt(v.x * v.x + v.y * v.y);
         if (tol > T(0) && mag < tol) th = 0.0;
         out[i] = th;
+    }
+}
+
+// Reconstructed intensity |F u|^2 (src/metrics.py:74-87): per mask (blockIdx.y)
+// fixed-partition partial sums and maxima of (double)|F u|^2, |.| taken in
+// the field precision and squared in fp64 as the reference does.
+template <typename T>
+__device__ __forceinline__ double recon_i(cx<T> f) {
+    const double a = (double)sqrt(f.x * f.x + f.y * f.y);
+    return a * a;
+}
+template <typename T>
+__global__ void recon_partial_kernel(const cx<T>* F, long long n, long long chunk, double* part, int nb) {
+    const cx<T>* f = F + blockIdx.y * n;
+    const long long lo = blockIdx.x * chunk, hi = min(n, lo + chunk);
+    double acc = 0.0, mx = 0.0;
+    for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+        const double v = recon_i<T>(f[i]);
+        acc += v;
+        mx = fmax(mx, v);
+    }
+    const double s = block_sum(acc);
+    __syncthreads();
+    const double m = block_max(mx);
+    if (threadIdx.x == 0) {
+        part[(size_t)blockIdx.y * 2 * nb + blockIdx.x] = s;
+        part[(size_t)blockIdx.y * 2 * nb + nb + blockIdx.x] = m;
+    }
+}
+// scale = E / sum (1 without E) and the peak of the scaled intensity, per mask
+// (max commutes with the monotone rounded scaling: max(I s) = max(I) s).
+__global__ void recon_final_kernel(const double* part, int nb, const double* energy, double* out) {
+    const int b = blockIdx.x;
+    const double* q = part + (size_t)b * 2 * nb;
+    double x = 0.0, m = 0.0;
+    for (int i = threadIdx.x; i < nb; i += 32) {
+        x += q[i];
+        m = fmax(m, q[nb + i]);
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+        x += __shfl_xor_sync(0xffffffffu, x, o);
+        m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    }
+    if (threadIdx.x == 0) {
+        const double sc = energy ? (x == 0.0 ? 0.0 : energy[b] / x) : 1.0;
+        out[2 * b] = sc;
+        out[2 * b + 1] = m * sc;
+    }
+}
+// The scaled intensity in DFT order and its log-scale 8-bit image in
+// centred order (to_centered_order + service._log_scale_u8,
+// src/service.py:91-95): v = I / peak (0 if peak == 0),
+// round(255 (log10(max(v, floor)) - lf) / -lf), lf = log10(floor).
+template <typename T>
+__global__ void recon_image_kernel(const cx<T>* F, int nx, int ny, const double* sp, double floor_, double lf,
+                                   double* inten, uint8_t* img) {
+    const long long n = (long long)nx * ny;
+    const int b = blockIdx.y;
+    const double sc = sp[2 * b], peak = sp[2 * b + 1];
+    const cx<T>* f = F + b * n;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const double v = recon_i<T>(f[i]) * sc;
+        if (inten) inten[b * n + i] = v;
+        if (img) {
+            const double d = peak > 0.0 ? v / peak : 0.0;
+            const double l = (log10(fmax(d, floor_)) - lf) / (-lf);
+            const int y = (int)(i / nx), x = (int)(i - (long long)y * nx);
+            const int yc = (y + ny / 2) % ny, xc = (x + nx / 2) % nx;     // fftshift
+            img[b * n + (long long)yc * nx + xc] = (uint8_t)rint(l * 255.0);
+        }
     }
 }
 
@@ -1796,6 +1881,70 @@ int pm_gap(pm_plan* pl, const void* u, const void* p, const void* m, double zero
 }
 
 // ----------------------------------------------------------- reductions
+int pm_recon_image(pm_plan* pl, const void* u, int batch, const double* target_energy, double log_floor,
+                   uint8_t* log_image, double* intensity) {
+    CKR(check_plan(pl));
+    if (!u || batch < 1) return set_err(PM_ERR_ARG, "null buffer or batch < 1");
+    if (log_image && !(log_floor > 0.0)) return set_err(PM_ERR_ARG, "log_floor must be > 0");
+    std::lock_guard<std::mutex> lk(pl->mu);
+    CKR(ensure_capacity(pl, batch, 1));
+    const long long n = (long long)pl->N;
+    int nb;
+    long long chunk;
+    reduce_grid(n, &nb, &chunk);
+    CKR(ensure_red(pl, batch * (2 * nb + 2) + batch));
+    double* part = pl->red;
+    double* sp = pl->red + (size_t)batch * 2 * nb;
+    double* en = sp + 2 * batch;
+    if (target_energy)
+        CK(cudaMemcpyAsync(en, target_energy, batch * sizeof(double), cudaMemcpyHostToDevice, pl->stream));
+    CK(cudaMemcpyAsync(pl->field, u, (size_t)batch * n * pl->csz, cudaMemcpyHostToDevice, pl->stream));
+    CKR(fft2_dev(pl, pl->field, pl->field, PM_FORWARD, batch));
+    uint8_t* dimg = nullptr;
+    double* dint = nullptr;
+    if (log_image) CK(cudaMalloc((void**)&dimg, (size_t)batch * n));
+    if (intensity) {
+        cudaError_t e = cudaMalloc((void**)&dint, (size_t)batch * n * sizeof(double));
+        if (e != cudaSuccess) {
+            cudaFree(dimg);
+            return cuda_err(e, "cudaMalloc");
+        }
+    }
+    const int blocks = (int)std::min<long long>((n + 255) / 256, 1184);
+    const double lf = std::log10(log_floor > 0.0 ? log_floor : 1.0);
+    if (pl->prec == PM_SINGLE) {
+        recon_partial_kernel<float><<<dim3(nb, batch), 256, 0, pl->stream>>>((const float2*)pl->field, n, chunk,
+                                                                              part, nb);
+        recon_final_kernel<<<batch, 32, 0, pl->stream>>>(part, nb, target_energy ? en : nullptr, sp);
+        recon_image_kernel<float><<<dim3(blocks, batch), 256, 0, pl->stream>>>(
+            (const float2*)pl->field, pl->nx, pl->ny, sp, log_floor, lf, dint, dimg);
+    } else {
+        recon_partial_kernel<double><<<dim3(nb, batch), 256, 0, pl->stream>>>((const double2*)pl->field, n,
+                                                                               chunk, part, nb);
+        recon_final_kernel<<<batch, 32, 0, pl->stream>>>(part, nb, target_energy ? en : nullptr, sp);
+        recon_image_kernel<double><<<dim3(blocks, batch), 256, 0, pl->stream>>>(
+            (const double2*)pl->field, pl->nx, pl->ny, sp, log_floor, lf, dint, dimg);
+    }
+    cudaError_t e = cudaGetLastError();
+    pl->launches += 3;
+    std::vector<double> h(2 * batch);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h.data(), sp, 2 * batch * sizeof(double), cudaMemcpyDeviceToHost,
+                                              pl->stream);
+    if (e == cudaSuccess && log_image)
+        e = cudaMemcpyAsync(log_image, dimg, (size_t)batch * n, cudaMemcpyDeviceToHost, pl->stream);
+    if (e == cudaSuccess && intensity)
+        e = cudaMemcpyAsync(intensity, dint, (size_t)batch * n * sizeof(double), cudaMemcpyDeviceToHost,
+                            pl->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(pl->stream);
+    cudaFree(dimg);
+    cudaFree(dint);
+    if (e != cudaSuccess) return cuda_err(e, "pm_recon_image");
+    if (target_energy)
+        for (int b = 0; b < batch; ++b)
+            if (h[2 * b] == 0.0) return set_err(PM_ERR_ARG, "reconstruction carries no energy");
+    return PM_OK;
+}
+
 int pm_norm2(int device, const void* data, long long count, int dtype, double* out) {
     if (!data || !out || count < 1) return set_err(PM_ERR_ARG, "cannot reduce an empty grid");
     if (dtype < 0 || dtype > 3) return set_err(PM_ERR_ARG, "dtype must be 0..3");

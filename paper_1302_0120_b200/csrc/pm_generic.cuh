@@ -410,7 +410,7 @@ __global__ void gen_row_sweep_kernel(cx<T>* w, cx<T>* u, const T* p, long long p
     const T thr = T(thr_p[b]);
     T chk = T(0);
     for (int idx = threadIdx.x; idx < L * TC; idx += blockDim.x) {
-        const int k = idx >> lgTC, t = idx & (TC - 1);      // element k of row t0 + t
+        const int t = idx & (TC - 1);                        // element idx >> lgTC of row t0 + t
         if (t >= tc) continue;
         T s2;
         const cx<T> uu = replace_mod(cscale(A[idx], sc), sm.g[idx], thr, s2);

@@ -24,6 +24,8 @@ import numpy as np
 
 from .grid import GridSpec, RealGrid
 
+LOG_FLOOR = 1e-6        # display floor of the log-scale images (src/patterns.py:22)
+
 
 def spot_grid_centers(spec: GridSpec, cols: int = 3, rows: int = 3):
     """Evenly spaced spot lattice (reference ``src/bench.py:78-82``)."""

@@ -236,3 +236,45 @@ def test_norm2_and_phases_on_gpu(rng):
     from paper_1302_0120_b200.backends import deterministic_sum
     v = rng.standard_normal(100000)
     assert deterministic_sum(v) == pytest.approx(orc.deterministic_sum(v), rel=1e-12, abs=1e-12)
+
+
+# ---------------------------------------------------------------- §8f-2
+def _ref_log_u8(intensity, floor=1e-6):
+    """service._log_scale_u8 (src/service.py:91-95), restated."""
+    import math
+    peak = intensity.max()
+    data = intensity / peak if peak > 0 else np.zeros_like(intensity)
+    data = (np.log10(np.maximum(data, floor)) - math.log10(floor)) / (-math.log10(floor))
+    return np.round(data * 255.0).astype(np.uint8)
+
+
+@pytest.mark.parametrize("prec", [pm.DOUBLE, pm.SINGLE])
+@pytest.mark.parametrize("shape", [(64, 64), (48, 80), (600, 800)])
+def test_reconstruction_intensity_and_log_image(prec, shape):
+    from paper_1302_0120_b200.metrics import reconstruction_log_image, reconstructed_intensity
+    from paper_1302_0120_b200.patterns import to_centered_order
+    ny, nx = shape
+    spec = pm.GridSpec(nx, ny)
+    rng = np.random.default_rng(5)
+    u = (rng.standard_normal(shape) + 1j * rng.standard_normal(shape)).astype(prec.complex_dtype)
+    f = pm.Field(spec, u)
+    prov = pm.FftProvider(spec, prec)
+    E = 17.0
+    F = np.fft.fft2(u.astype(np.complex128), norm="ortho").astype(prec.complex_dtype)
+    amps = np.abs(F).astype(np.float64)
+    ref = amps * amps
+    ref = ref * (E / ref.sum())
+    got = reconstructed_intensity(f, prov, E).data
+    # fp32: the two fp32 FFTs differ by ~eps |u|, relative to the peak for small bins
+    np.testing.assert_allclose(got, ref, rtol=1e-12 if prec is pm.DOUBLE else 2e-5,
+                               atol=0 if prec is pm.DOUBLE else 1e-6 * ref.max())
+    img = reconstruction_log_image(f, prov, E)
+    want = _ref_log_u8(to_centered_order(pm.RealGrid(spec, got)).data)
+    # same intensities: only log10 ulps may move a value across a .5 boundary
+    assert np.abs(img.astype(int) - want.astype(int)).max() <= 1
+    assert np.mean(img == want) > 0.999
+    # unscaled intensity; zero energy is rejected with the reference's message
+    raw = reconstructed_intensity(f, prov).data
+    np.testing.assert_allclose(raw * (E / raw.sum()), got, rtol=1e-12 if prec is pm.DOUBLE else 1e-6)
+    with pytest.raises(ValueError, match="reconstruction carries no energy"):
+        reconstructed_intensity(pm.Field(spec, np.zeros(shape, prec.complex_dtype)), prov, E)
