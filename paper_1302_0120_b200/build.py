@@ -82,9 +82,11 @@ def _units(build_dir):
             row, col, nt = _config(tag, lg)
             roll = int(os.environ.get("PM_ROLL", "0"))
             pf = int(os.environ.get("PM_PF", "0"))
-            units.append((CSRC / "pm_inst.cu", build_dir / f"pm_inst_{tag}_{lg}_{row}{col}_{nt}_r{roll}_p{pf}.o",
+            xd = os.environ.get("PM_XDEFS", "").split()        # experiment macros (-DNAME=V ...)
+            xs = "".join("_" + d.lstrip("-D").replace("=", "") for d in xd)
+            units.append((CSRC / "pm_inst.cu", build_dir / f"pm_inst_{tag}_{lg}_{row}{col}_{nt}_r{roll}_p{pf}{xs}.o",
                           [f"-DPM_F64={f64}", f"-DPM_LG={lg}", f"-DPM_LGR_ROW={row}", f"-DPM_LGR_COL={col}",
-                           f"-DPM_SOLVE_NT={nt}", f"-DPM_ROLL={roll}", f"-DPM_PF={pf}"]))
+                           f"-DPM_SOLVE_NT={nt}", f"-DPM_ROLL={roll}", f"-DPM_PF={pf}", *xd]))
     units.append((CSRC / "pm_table.cu", build_dir / "pm_table.o", []))
     units.append((CSRC / "pm_capi.cu", build_dir / "pm_capi.o", []))
     return units

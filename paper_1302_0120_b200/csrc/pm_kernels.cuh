@@ -978,6 +978,9 @@ __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
 // Grid barrier: every CTA releases one arrival (no returned atomic) and
 // polls the monotonic arrival count until the whole grid has arrived at this
 // epoch; `epoch` counts this launch's barriers (identical in all CTAs).
+#ifndef PM_BAR_NS
+#define PM_BAR_NS 32         // poll back-off (ns) of the grid barrier
+#endif
 __device__ __forceinline__ void grid_sync(GridBar* bar, unsigned& epoch) {
     __syncthreads();
     ++epoch;
@@ -985,6 +988,7 @@ __device__ __forceinline__ void grid_sync(GridBar* bar, unsigned& epoch) {
         red_release_add(&bar->count, 1u);
         const unsigned target = epoch * gridDim.x;
         while (ld_acquire(&bar->count) < target) {
+            if constexpr (PM_BAR_NS > 0) __nanosleep(PM_BAR_NS);
         }
     }
     __syncthreads();

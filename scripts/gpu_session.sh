@@ -2,7 +2,7 @@
 # One gpurun call's worth of evidence: GPU tests, smoke, per-size timings,
 # the bench line, the ncu launch list and one full ncu capture of the
 # persistent solve kernel. Usage (from the repo root, under gpurun):
-#   bash scripts/gpu_session.sh [tag] [what...]   what: tests smoke perf bench launches full
+#   bash scripts/gpu_session.sh [tag] [what...]   what: tests smoke perf bench launches benchfull ref paper full
 set -u
 TAG=${1:-r01}
 shift || true
@@ -25,6 +25,15 @@ for w in $WHAT; do
       timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
         --log-file "$OUT/launches.csv" python bench.py --steps 3 --warmup 3 --no-cpu-baseline > "$OUT/launches.log" 2>&1
       echo "launches rc=$?" ;;
+    benchfull)
+      timeout 900 ncu --set full --clock-control none --import-source on -k regex:solve_kernel -s 5 -c 1 \
+        -o "$OUT/bench_solve" -f python bench.py --steps 3 --warmup 3 --no-cpu-baseline > "$OUT/benchfull.log" 2>&1
+      echo "benchfull rc=$?" ;;
+    ref)
+      timeout 900 python bench.py --impl reference > "$OUT/bench_reference.json" 2> "$OUT/bench_reference.err"
+      echo "ref rc=$?"; tail -c 1500 "$OUT/bench_reference.json" ;;
+    paper)
+      timeout 300 python scripts/paper_config.py > "$OUT/paper.log" 2>&1; echo "paper rc=$?"; cat "$OUT/paper.log" ;;
     full)
       timeout 1200 ncu --set full --clock-control none --import-source on -k regex:solve_kernel -s 2 -c 1 \
         -o "$OUT/solve_full" -f python scripts/prof_solve.py > "$OUT/full.log" 2>&1

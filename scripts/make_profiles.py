@@ -91,6 +91,8 @@ def main(src, tag):
                            "so DRAM traffic is the cold first touch plus write-back, far below the algorithmic bytes"},
                   (prof / f"{tag}_ncu_traffic.json").open("w"), indent=1)
     sf = src / "solve.ncu-rep"
+    if not sf.exists():
+        sf = src / "solve_full.ncu-rep"
     if sf.exists():
         from ncu_lines import main as lines_main
         import contextlib

@@ -2,7 +2,7 @@
 neighbours): ms per mask, us per iteration per mask, and the stand-alone
 row / column sweep times of the same plan.
 
-    python scripts/sweep_perf.py [n_cases]
+    python scripts/sweep_perf.py [n_cases | i,j,...]
 """
 import os, sys
 sys.path.insert(0, '/root/repo')
@@ -45,7 +45,9 @@ cases = [(1024, 'single', 1, 'gs', 100), (1024, 'single', 8, 'gs', 100), (256, '
          (2048, 'single', 1, 'gs', 100), (4096, 'single', 1, 'gs', 100), (512, 'single', 1, 'gs', 100),
          (1024, 'double', 1, 'gs', 100), (512, 'double', 1, 'gs', 100), (256, 'single', 1, 'gs', 100),
          (16, 'single', 1, 'gs', 100)]
-if len(sys.argv) > 1: cases = cases[:int(sys.argv[1])]
+if len(sys.argv) > 1:   # n_cases, or a comma list of case indices
+    a = sys.argv[1]
+    cases = [cases[int(i)] for i in a.split(",") if i] if "," in a else cases[:int(a)]
 for n, tag, b, algo, K in cases:
     try:
         run(n, tag, b, algo, K)
