@@ -45,15 +45,16 @@ def nvcc() -> str:
 # kernel's CTA size, per precision and size (DESIGN.md "Kernel
 # configuration"); override every size at once for experiments with
 # PM_LGR="f32row,f32col,f64row,f64col" and PM_SOLVE_NT="f32,f64".
-# Measured on B200 (profiles/): radix-4 / radix-8 with small CTAs
-# for 256^2 / 512^2 (latency-bound: spread rows and columns over all SMs),
+# Measured on B200 (profiles/): radix-4 / radix-8 with 256-thread CTAs
+# for 256^2 / 512^2 (latency-bound: short chains),
 # radix-32 rows and columns with a 256-thread persistent CTA at 1024^2 fp32,
 # radix-16 and 512 threads for the HBM-resident 2048^2 / 4096^2 grids and
 # for fp64.
 def default_config(tag: str, lg: int) -> tuple[int, int, int]:
     """(log2 points per thread of rows, of columns, persistent CTA size)."""
     if lg <= 8:
-        return (2, 2, 128)          # short dependency chains, rows/columns spread over all SMs
+        return (2, 2, 256)          # short dependency chains (256^2: 6.4 / 8.5 us per iteration f32 / f64,
+                                    # vs 8.4 / 9.9 with 128-thread CTAs; scripts/variants_small.sh)
     if lg == 9:
         return (3, 3, 256)
     if tag == "f32":
