@@ -936,25 +936,61 @@ int launch_fft2(pm_plan* pl, const void* in, void* out, int dir, int batch) {
 
 // ------------------------------------------------------- mixed-radix path
 // Factor n into passes of radix 4, 2, 3, 5, 7 (fails for other primes).
-bool gen_factor(int n, GenPlan* g) {
+int env_int(const char* name, int dflt) {
+    const char* v = std::getenv(name);
+    return v && *v ? std::atoi(v) : dflt;
+}
+
+// Pass plan of a length-n transform: the fewest passes over the radices
+// the kernels instantiate (base 2, 3, 4, 5, 7, 8 and the register
+// composites 9, 10, 12, 16 of pm_generic.cuh, up to rmax), ties broken
+// towards the larger smallest radix.
+bool gen_factor(int n, GenPlan* g, int rmax) {
     if (n < 1 || n > (1 << kMaxLg)) return false;
+    static const int radices[] = {16, 12, 10, 9, 8, 7, 5, 4, 3, 2};
+    // best[k] for every divisor k of n: (passes, -smallest radix, first radix)
+    std::map<int, std::pair<std::pair<int, int>, int>> best;
+    std::vector<int> divs;
+    for (int d = 1; d <= n; ++d)
+        if (n % d == 0) divs.push_back(d);
+    best[1] = {{0, -1000}, 0};
+    for (int k : divs) {
+        if (k == 1) continue;
+        std::pair<std::pair<int, int>, int> b{{1 << 20, 0}, 0};
+        for (int r : radices) {
+            if (r > rmax || k % r != 0) continue;
+            auto it = best.find(k / r);
+            if (it == best.end() || it->second.first.first >= (1 << 20)) continue;
+            const std::pair<int, int> cand{it->second.first.first + 1, std::max(it->second.first.second, -r)};
+            if (cand < b.first) b = {cand, r};
+        }
+        best[k] = b;
+    }
+    if (best[n].first.first >= (1 << 20) || best[n].first.first > kGenMaxPasses) return false;
+    std::vector<int> rs;
+    for (int rest = n; rest > 1; rest /= best[rest].second) rs.push_back(best[rest].second);
+    // pass order: 1 = descending radix (default; 800x600 fp32: 0.82 vs
+    // 0.87 ms with 0 = powers of two first, then the rest ascending); 2 = ascending
+    const int order = env_int("PM_GEN_ORDER", 1);
+    auto pow2 = [](int r) { return (r & (r - 1)) == 0; };
+    std::sort(rs.begin(), rs.end(), [&](int a, int b) {
+        if (order == 1) return a > b;
+        if (order == 2) return a < b;
+        if (pow2(a) != pow2(b)) return pow2(a);
+        return pow2(a) ? a > b : a < b;
+    });
     g->L = n;
     g->np = 0;
-    int rest = n, ns = 1;
-    const int order[] = {8, 4, 2, 3, 5, 7};
-    for (int r : order) {
-        while (rest % r == 0) {
-            if (g->np == kGenMaxPasses) return false;
-            g->radix[g->np] = r;
-            g->ns[g->np] = ns;
-            g->step[g->np] = n / (ns * r);
-            g->mg[g->np] = ns == 1 ? 0u : 0xFFFFFFFFu / (unsigned)ns + 1u;
-            ++g->np;
-            ns *= r;
-            rest /= r;
-        }
+    int ns = 1;
+    for (int r : rs) {
+        g->radix[g->np] = r;
+        g->ns[g->np] = ns;
+        g->step[g->np] = n / (ns * r);
+        g->mg[g->np] = ns == 1 ? 0u : 0xFFFFFFFFu / (unsigned)ns + 1u;
+        ++g->np;
+        ns *= r;
     }
-    return rest == 1;
+    return true;
 }
 
 // exp(-2 pi i k / n) in the plan precision, long-double accurate.
@@ -982,25 +1018,34 @@ int gen_twiddles(int prec, int n, void** out) {
 
 constexpr size_t kGenSmem = 100 * 1024;  // preferred tile bytes per CTA (TC is halved down to 1 above it)
 
-int env_int(const char* name, int dflt) {
-    const char* v = std::getenv(name);
-    return v && *v ? std::atoi(v) : dflt;
-}
 
 int gen_setup(pm_plan* pl) {
     CKR(gen_twiddles(pl->prec, pl->nx, &pl->gtwx));
     CKR(gen_twiddles(pl->prec, pl->ny, &pl->gtwy));
     // transforms per CTA: a power of two, enough CTAs to cover the SMs,
     // columns wide enough for >= 32-byte segments
-    auto tc_for = [&](int L, int ntrans, int want) {
-        int tc = want;
-        while (tc > 1 && (gen_smem_bytes(L, tc, pl->csz) > kGenSmem || (ntrans + tc - 1) / tc < 148)) tc >>= 1;
-        return tc;
+    // transforms per CTA (TC): 2, halved while the grid would not cover the
+    // SMs or the tiles would not fit; 256 threads (measured on the paper's
+    // 800x600 fp32: TC 1-8 x 64-256 threads, scripts/gen_tune_rmax.sh)
+    auto shape_for = [&](const GenPlan& g, int ntrans, const char* etc, const char* ent, int& tc, int& nt) {
+        tc = env_int(etc, 2);
+        while (tc > 1 && (gen_smem_bytes(g.L, tc, pl->csz) > kGenSmem || (ntrans + tc - 1) / tc < 148)) tc >>= 1;
+        nt = env_int(ent, 256);
     };
-    pl->gtc_r = tc_for(pl->nx, pl->ny, env_int("PM_GEN_TCR", 1));
-    pl->gtc_c = tc_for(pl->ny, pl->nx, env_int("PM_GEN_TCC", 2));
-    pl->gnt_r = env_int("PM_GEN_NTR", 256);
-    pl->gnt_c = env_int("PM_GEN_NTC", 256);
+    shape_for(pl->gx, pl->ny, "PM_GEN_TCR", "PM_GEN_NTR", pl->gtc_r, pl->gnt_r);
+    shape_for(pl->gy, pl->nx, "PM_GEN_TCC", "PM_GEN_NTC", pl->gtc_c, pl->gnt_c);
+    {   // the register budget bounds the CTA size
+        cudaFuncAttributes fa[3];
+        const bool f32 = pl->prec == PM_SINGLE;
+        CK(cudaFuncGetAttributes(&fa[0], f32 ? (const void*)&gen_fft_kernel<float> : (const void*)&gen_fft_kernel<double>));
+        CK(cudaFuncGetAttributes(&fa[1], f32 ? (const void*)&gen_col_sweep_kernel<float>
+                                             : (const void*)&gen_col_sweep_kernel<double>));
+        CK(cudaFuncGetAttributes(&fa[2], f32 ? (const void*)&gen_row_sweep_kernel<float>
+                                             : (const void*)&gen_row_sweep_kernel<double>));
+        const int cap = std::min({fa[0].maxThreadsPerBlock, fa[1].maxThreadsPerBlock, fa[2].maxThreadsPerBlock}) / 32 * 32;
+        pl->gnt_r = std::min(pl->gnt_r, cap);
+        pl->gnt_c = std::min(pl->gnt_c, cap);
+    }
     pl->gsm_r = gen_smem_bytes(pl->nx, pl->gtc_r, pl->csz);
     pl->gsm_c = gen_smem_bytes(pl->ny, pl->gtc_c, pl->csz);
     const size_t mx = std::max(pl->gsm_r, pl->gsm_c);
@@ -1073,28 +1118,6 @@ GenSolveArgs gen_args(pm_plan* pl) {
     return g;
 }
 
-template <typename T>
-int gen_replace(pm_plan* pl, int u_iter, int metrics_only, int all_masks) {
-    const dim3 grid(gen_elem_blocks(pl), pl->s.batch);
-    gen_replace_kernel<T><<<grid, 256, 0, pl->stream>>>((cx<T>*)pl->tmp, (const T*)pl->s.m, pl->thrm, pl->escale,
-                                                        gen_args(pl), u_iter, metrics_only, all_masks);
-    CK(cudaGetLastError());
-    pl->launches++;
-    return PM_OK;
-}
-
-// F^-1 replace_m F of the iterates (field -> tmp), with the metrics and
-// decision of iterate u_iter (0: none).
-int gen_half(pm_plan* pl, int u_iter, int metrics_only, int all_masks) {
-    const int B = pl->s.batch;
-    CKR(gen_fft2(pl, pl->field, pl->tmp, PM_FORWARD, B, pl->st, all_masks));
-    CKR(pl->prec == PM_SINGLE ? gen_replace<float>(pl, u_iter, metrics_only, all_masks)
-                              : gen_replace<double>(pl, u_iter, metrics_only, all_masks));
-    if (metrics_only) return PM_OK;
-    // inverse: columns then rows (any order gives the 2-D inverse)
-    return gen_fft2(pl, pl->tmp, pl->tmp, PM_INVERSE, B, pl->st, all_masks);
-}
-
 // w = RowFFT(u): the iterates (field) into the work buffer.
 int gen_rows_fwd(pm_plan* pl, int all_masks) {
     return pl->prec == PM_SINGLE ? gen_axis<float>(pl, pl->field, pl->tmp, 0, PM_FORWARD, pl->s.batch, pl->st, all_masks)
@@ -1152,16 +1175,6 @@ int gen_begin(pm_plan* pl) {
     }
     CKR(gen_fft2(pl, pl->field, pl->field, PM_INVERSE, s.batch, pl->st, 0));   // u0 = F^-1(m e^{i phi})
     return gen_rows_fwd(pl, 0);                                                  // w = RowFFT(u0)
-}
-
-template <typename T>
-int gen_slm(pm_plan* pl, int it) {
-    const dim3 grid(gen_elem_blocks(pl), pl->s.batch);
-    gen_slm_kernel<T><<<grid, 256, 0, pl->stream>>>((const cx<T>*)pl->tmp, (cx<T>*)pl->field, (const T*)pl->s.p,
-                                                    pl->s.p_stride, pl->thrx, pl->st, (long long)pl->N, it);
-    CK(cudaGetLastError());
-    pl->launches++;
-    return PM_OK;
 }
 
 // Two fused sweeps per iteration over the work buffer, which holds
@@ -1578,7 +1591,8 @@ int pm_plan_create(int device, int n_x, int n_y, int precision, int max_batch, p
     bool generic = false;
     if (lgx < 0 || lgy < 0 || lgx > kMaxLg || lgy > kMaxLg) {
         // mixed-radix path: every side a product of 2, 3, 5, 7, at most 4096
-        if (!gen_factor(n_x, &gx) || !gen_factor(n_y, &gy))
+        const int rmax = env_int("PM_GEN_RMAX", 16);
+        if (!gen_factor(n_x, &gx, rmax) || !gen_factor(n_y, &gy, rmax))
             return set_err(PM_ERR_UNSUPPORTED, "grid " + std::to_string(n_x) + "x" + std::to_string(n_y) +
                                                    ": n_x and n_y must be at most 4096 with prime factors 2, 3, 5, 7");
         generic = true;

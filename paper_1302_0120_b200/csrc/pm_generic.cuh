@@ -1,23 +1,31 @@
-// Mixed-radix path for grids whose sides are not powers of two (radices 8, 4, 2,
-// 3, 5, 7; n <= 4096), e.g. the paper's 800x600 SLM and
+// Mixed-radix path for grids whose sides are not powers of two (prime factors
+// 2, 3, 5, 7; n <= 4096), e.g. the paper's 800x600 SLM and
 // the reference's acceptance grid (tests/test_acceptance.py:118-128,200-205).
 //
-// The power-of-two path fuses each half iteration into one register-resident
-// sweep; this path is a plain sequence of kernels over a work buffer, which
-// is enough for the sizes it serves:
-//   gen_fft_kernel      one axis of a unitary 2-D DFT: a CTA gathers TC
-//                       transforms into shared memory (coalesced along
-//                       whichever axis is contiguous), runs the Stockham
-//                       passes there and scatters the result;
-//   gen_replace_kernel  replace_m in the Fourier plane + the metrics of the
-//                       iterate (gap by Parseval, E_lit / E_dark) reduced
-//                       per block in a fixed order; the last block decides
-//                       (record / early stop / max_iters / divergence);
-//   gen_slm_kernel      P_S back into the iterate + non-finite detection;
-//   gen_final_kernel    u* = P_S v*, the float64 mask and uint8 levels.
+// The power-of-two path runs a whole solve in one persistent launch; this
+// path is two fused sweep kernels per iteration over a work buffer that
+// holds RowFFT(u):
+//   gen_col_sweep_kernel  a CTA stages TC columns, the twiddle table and its
+//                         slice of m in shared memory (cp.async), runs the
+//                         Stockham passes, replace_m with the metrics of the
+//                         previous iterate (fixed-order fp64 partials; the
+//                         last CTA of a mask decides record / early stop /
+//                         max_iters / divergence), and the inverse passes;
+//   gen_row_sweep_kernel  inverse row passes, P_S into the iterate
+//                         (non-finite check), forward row passes;
+//   gen_fft_kernel        one axis of a unitary 2-D DFT (start, finish and
+//                         the stand-alone transform);
+//   gen_final_kernel      u* = P_S v*, the float64 mask and uint8 levels.
+// A pass is one radix of the plan: base radices 2, 3, 4, 5, 7, 8 and the
+// register composites 9, 10, 12, 16 (internal twiddles as compile-time
+// constants), so 800 = 16 x 10 x 5 and 600 = 12 x 10 x 5 take three passes.
+// (Composites up to 32 ran slower: one long register DFT per thread leaves
+// too few warps per SM, and every extra radix grows the kernels' code.)
 // Semantics (threshold decisions, fixed-order fp64 sums, stop logic) are the
 // fused path's: see pm_kernels.cuh.
 #pragma once
+#include <type_traits>
+
 #include "pm_kernels.cuh"
 
 namespace pm {
@@ -52,10 +60,113 @@ __host__ __device__ constexpr double gen_s(int r, int k) {
            : k == 5 ? -0.97492791218182360701813168299393 : -0.78183148246802980870844452667406);
 }
 
+// cos / sin (2 pi m / R) as compile-time constants: the angle is reduced
+// exactly on the integer numerator to [0, pi/4] (quadrant + reflection) and
+// the Taylor series there is summed far below one fp64 ulp.
+__host__ __device__ constexpr double gen_tsin(double x) {
+    double t = x, s = x;
+    for (int k = 1; k < 14; ++k) {
+        t *= -x * x / ((2.0 * k) * (2.0 * k + 1.0));
+        s += t;
+    }
+    return s;
+}
+__host__ __device__ constexpr double gen_tcos(double x) {
+    double t = 1.0, s = 1.0;
+    for (int k = 1; k < 14; ++k) {
+        t *= -x * x / ((2.0 * k - 1.0) * (2.0 * k));
+        s += t;
+    }
+    return s;
+}
+__host__ __device__ constexpr double gen_kc(int R, int m, bool want_sin) {
+    const int mm = ((m % R) + R) % R;
+    const int u = 4 * mm, q = u / R, r = u - q * R;              // angle = (q + r / R) pi / 2
+    const double half_pi = 1.57079632679489661923132169163975;
+    double c0 = 0.0, s0 = 0.0;
+    if (2 * r <= R) {
+        const double a = half_pi * r / R;
+        c0 = gen_tcos(a);
+        s0 = gen_tsin(a);
+    } else {
+        const double a = half_pi * (R - r) / R;
+        c0 = gen_tsin(a);
+        s0 = gen_tcos(a);
+    }
+    double c = c0, s = s0;
+    if (q == 1) { c = -s0; s = c0; }
+    else if (q == 2) { c = -c0; s = -s0; }
+    else if (q == 3) { c = s0; s = -c0; }
+    return want_sin ? s : c;
+}
+
+// Composite radices R = A * B, run in registers (Cooley-Tukey with
+// n = b + B a, k = ka + A kb); A = 0 marks a base radix (2, 3, 4, 5, 7, 8).
+// More splits (e.g. 25 = 5 x 5, 32 = 8 x 4) only need a line here, a case in
+// gen_passes and an entry in gen_factor's list.
+template <int R> struct GenSplit { static constexpr int A = 0, B = 0; };
+#define PM_GEN_SPLIT(R_, A_, B_) \
+    template <> struct GenSplit<R_> { static constexpr int A = A_, B = B_; };
+PM_GEN_SPLIT(9, 3, 3)
+PM_GEN_SPLIT(10, 5, 2)
+PM_GEN_SPLIT(12, 4, 3)
+PM_GEN_SPLIT(16, 4, 4)
+#undef PM_GEN_SPLIT
+
+// Compile-time loop: f(integral_constant<int, i>) for i in [I, N).
+template <int I, int N>
+struct GenFor {
+    template <class F>
+    __device__ __forceinline__ static void run(F&& f) {
+        if constexpr (I < N) {
+            f(std::integral_constant<int, I>{});
+            GenFor<I + 1, N>::run(f);
+        }
+    }
+};
+
+template <typename T, int R, int DIR>
+__device__ __forceinline__ void gen_dft(cx<T>* x);
+
+template <typename T, int R, int DIR>
+__device__ __forceinline__ void gen_dft_split(cx<T>* x) {
+    constexpr int A = GenSplit<R>::A, B = GenSplit<R>::B;
+    cx<T> y[R];
+    GenFor<0, B>::run([&](auto bc) {
+        constexpr int b = decltype(bc)::value;
+        cx<T> s[A];
+#pragma unroll
+        for (int a = 0; a < A; ++a) s[a] = x[b + B * a];
+        gen_dft<T, A, DIR>(s);
+        GenFor<0, A>::run([&](auto kc) {
+            constexpr int ka = decltype(kc)::value;
+            if constexpr (b * ka == 0) {
+                y[b * A + ka] = s[ka];
+            } else {
+                // W_R^{b ka} = exp(DIR 2 pi i b ka / R)
+                constexpr double c = gen_kc(R, b * ka, false), sn = DIR * gen_kc(R, b * ka, true);
+                const cx<T> v = s[ka];
+                y[b * A + ka] = mk<T>(v.x * T(c) - v.y * T(sn), v.x * T(sn) + v.y * T(c));
+            }
+        });
+    });
+#pragma unroll
+    for (int ka = 0; ka < A; ++ka) {
+        cx<T> s[B];
+#pragma unroll
+        for (int b = 0; b < B; ++b) s[b] = y[b * A + ka];
+        gen_dft<T, B, DIR>(s);
+#pragma unroll
+        for (int kb = 0; kb < B; ++kb) x[ka + A * kb] = s[kb];
+    }
+}
+
 // In-place DFT of R points, sign DIR (-1 forward), natural order.
 template <typename T, int R, int DIR>
 __device__ __forceinline__ void gen_dft(cx<T>* x) {
-    if constexpr (R == 2) {
+    if constexpr (GenSplit<R>::A > 0) {
+        gen_dft_split<T, R, DIR>(x);
+    } else if constexpr (R == 2) {
         const cx<T> a = x[0], b = x[1];
         x[0] = mk<T>(a.x + b.x, a.y + b.y);
         x[1] = mk<T>(a.x - b.x, a.y - b.y);
@@ -163,14 +274,14 @@ __device__ __forceinline__ cx<T>* gen_passes(cx<T>* A, cx<T>* B, const cx<T>* tw
     for (int s = 0; s < gp.np; ++s) {
         const int L = gp.L, Ns = gp.ns[s], st = gp.step[s];
         const unsigned mg = gp.mg[s];
-        switch (gp.radix[s]) {
-            case 2: gen_pass<T, 2>(A, B, tw, L, Ns, st, mg, lgTC, dir); break;
-            case 3: gen_pass<T, 3>(A, B, tw, L, Ns, st, mg, lgTC, dir); break;
-            case 4: gen_pass<T, 4>(A, B, tw, L, Ns, st, mg, lgTC, dir); break;
-            case 5: gen_pass<T, 5>(A, B, tw, L, Ns, st, mg, lgTC, dir); break;
-            case 7: gen_pass<T, 7>(A, B, tw, L, Ns, st, mg, lgTC, dir); break;
-            default: gen_pass<T, 8>(A, B, tw, L, Ns, st, mg, lgTC, dir); break;
+#define PM_GEN_CASE(R_) \
+    case R_: gen_pass<T, R_>(A, B, tw, L, Ns, st, mg, lgTC, dir); break;
+        switch (gp.radix[s]) {   // the radices gen_factor plans with (pm_capi.cu)
+            PM_GEN_CASE(2) PM_GEN_CASE(3) PM_GEN_CASE(4) PM_GEN_CASE(5) PM_GEN_CASE(7) PM_GEN_CASE(8)
+            PM_GEN_CASE(9) PM_GEN_CASE(10) PM_GEN_CASE(12) PM_GEN_CASE(16)
+            default: __trap();
         }
+#undef PM_GEN_CASE
         __syncthreads();
         cx<T>* tmp = A; A = B; B = tmp;
     }
@@ -271,49 +382,6 @@ struct GenSolveArgs {
     int nblk;
     long long n;          // pixels per mask
 };
-
-// v^ = replace_m(u^) in place (unless metrics_only), with the metrics of the
-// iterate u_{u_iter} when it is decided here: gap^2 = sum |u^ - v^|^2
-// (Parseval, GS), E_lit / E_dark of the reconstruction (src/metrics.py:67-112).
-template <typename T>
-__global__ void gen_replace_kernel(cx<T>* f, const T* m, const double* thr_m, const double* escale, GenSolveArgs g,
-                                   int u_iter, int metrics_only, int all_masks) {
-    const int b = blockIdx.y;
-    MaskState* st = g.st + b;
-    if (st->done || (!all_masks && st->stop)) return;
-    const bool dec = u_iter >= 1 && st->decided < u_iter && !st->stop;
-    const bool rec = dec && recorded(g.ctl, u_iter);
-    const bool gneed = dec && gap_needed(g.ctl, u_iter);
-    const T thr = T(thr_m[b]);
-    const double sc = escale[b];
-    cx<T>* fb = f + b * g.n;
-    const T* mb = m + b * g.n;
-    double acc[3] = {0.0, 0.0, 0.0};
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < g.n;
-         i += (long long)gridDim.x * blockDim.x) {
-        const cx<T> u = fb[i];
-        const T mm = mb[i];
-        const cx<T> vh = replace_mod(u, mm, thr);
-        if (gneed) acc[0] += norm_sq_d(csub(u, vh));
-        if (rec) {
-            const double inten = norm_sq_d(u) * sc;
-            const double m2 = (double)mm * (double)mm;
-            if (m2 > 0.0) {
-                const double dev = fabs(m2 - inten);
-                if (dev > g.ctl.t_lit * m2 && dev / m2 > g.ctl.t_lit)
-                    acc[1] += g.ctl.t_dark * dev / (g.ctl.t_lit * m2) - g.ctl.t_dark;
-            } else if (inten > g.ctl.t_dark) {
-                acc[2] += inten - g.ctl.t_dark;
-            }
-        }
-        if (!metrics_only) fb[i] = vh;
-    }
-    if (!dec) return;
-    double tot[3];
-    if (reduce_ticket<3>(acc, g.part + (size_t)b * g.nblk * 3, g.ctr + b, g.nblk, blockIdx.x, tot) &&
-        threadIdx.x == 0)
-        decide(st, g.hist + ((size_t)b * g.hist_stride + (u_iter - 1)) * 4, g.ctl, u_iter, rec, tot);
-}
 
 // Column sweep of the mixed-radix solve, fused: ColFFT -> replace_m (+ the
 // metrics and decision of u_{u_iter}) -> ColIFFT on the work buffer `w`
@@ -422,26 +490,6 @@ __global__ void gen_row_sweep_kernel(cx<T>* w, cx<T>* u, const T* p, long long p
     gen_scatter<T>(A, ub, L, lgTC, t0, tc, L, 1, T(1));     // the iterate, coalesced along the row
     A = gen_passes<T>(A, B, sm.tw, gp, lgTC, -1);
     gen_scatter<T>(A, wb, L, lgTC, t0, tc, L, 1, sc);
-}
-
-// u = P_S v from the work buffer back into the iterate, non-finite check.
-template <typename T>
-__global__ void gen_slm_kernel(const cx<T>* v, cx<T>* u, const T* p, long long p_stride, const double* thr_p,
-                               MaskState* st, long long n, int it) {
-    const int b = blockIdx.y;
-    if (st[b].done || st[b].stop) return;
-    const T thr = T(thr_p[b]);
-    const cx<T>* vb = v + b * n;
-    cx<T>* ub = u + b * n;
-    const T* pb = p + b * p_stride;
-    T chk = T(0);
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-         i += (long long)gridDim.x * blockDim.x) {
-        T s2;
-        ub[i] = replace_mod(vb[i], pb[i], thr, s2);
-        chk += s2;
-    }
-    if (!isfinite(chk)) first_bad(&st[b].bad, it);
 }
 
 // Best-approximation pair and mask from v* (src/solver.py:201-206).

@@ -132,7 +132,10 @@ def test_unsupported_prime_factor_is_not_implemented(rng):
         pm.FftProvider(pm.GridSpec(22, 13)).forward(pm.Field(pm.GridSpec(22, 13), np.zeros((13, 22))))
 
 
-@pytest.mark.parametrize("nx,ny", [(800, 600), (6, 10), (15, 8), (49, 12), (1000, 90), (3, 1)])
+@pytest.mark.parametrize("nx,ny", [(800, 600), (6, 10), (15, 8), (49, 12), (1000, 90), (3, 1),
+                                   # every register composite (6 ... 32) and long chains
+                                   (9, 14), (20, 21), (27, 28), (24, 25), (96, 160), (243, 7),
+                                   (343, 5), (625, 48), (4050, 3), (3, 3969), (2187, 2)])
 @pytest.mark.parametrize("tag", ["double", "single"])
 def test_mixed_radix_transform_matches_scipy(nx, ny, tag, rng):
     """Sides with prime factors 2, 3, 5, 7 (the paper's 800x600 SLM) run the
