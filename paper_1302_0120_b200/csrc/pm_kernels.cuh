@@ -145,6 +145,8 @@ struct ColArgs {
     long long part_alt;       // persistent RAAR: offset of the odd-iteration partial buffer
     const T* m;
     long long m_stride;
+    const T* mT;              // persistent column phase: m transposed per mask ([batch][nx][ny], same
+                              // stride), so a task's m is one contiguous run (null: stage from m)
     const twe<T>* twf;
     const twe<T>* twi;
     int nx, ny;
@@ -473,6 +475,33 @@ __device__ __forceinline__ void stage_tile(E* dst, const E* src, size_t gstride,
     }
 }
 
+// stage_tile into rows of DSTR elements (DSTR >= RUN; DSTR * sizeof(E) a
+// multiple of the copy size).
+template <typename E, int ROWS, int RUN, int DSTR, int NTHR>
+__device__ __forceinline__ void stage_tile_s(E* dst, const E* src, size_t gstride, int t) {
+    constexpr int CH = RUN * (int)sizeof(E) >= 16 ? 16 : RUN * (int)sizeof(E);
+    constexpr int EPC = CH / (int)sizeof(E);
+    constexpr int CPR = RUN / EPC;
+    constexpr int TOT = ROWS * CPR;
+    static_assert(CPR * EPC == RUN && (CPR & (CPR - 1)) == 0 && (DSTR * (int)sizeof(E)) % CH == 0,
+                  "runs must split into power-of-two aligned copies");
+#pragma unroll 4
+    for (int i = t; i < TOT; i += NTHR) {
+        const int r = i / CPR, q = i % CPR;
+        cp_async<CH>(dst + (size_t)r * DSTR + q * EPC, src + r * gstride + q * EPC);
+    }
+}
+
+// Row stride of the transposed m tile of a column task: ny plus a pad that
+// spreads the C columns of a warp over distinct banks (and keeps 16-byte rows).
+template <typename T, int NY, int CC>
+struct MtStride {
+    static constexpr int PAD0 = CC > 0 ? 32 / CC : 1;
+    static constexpr int Q = 16 / (int)sizeof(T);
+    static constexpr int PAD = (PAD0 + Q - 1) / Q * Q;
+    static constexpr int V = NY + PAD;
+};
+
 // A row task: the TG threads of group g transform one row. `inb` == false
 // (row beyond the batch) runs the same instruction stream on zeros without
 // touching memory, so group barriers stay aligned when a CTA has fewer rows
@@ -735,7 +764,11 @@ __device__ __forceinline__ void col_task(const ColArgs<T>& a, int b, int col0, i
     if constexpr (PS && !TM) {
         // CC: the persistent kernel's compile-time column count (division-free copy loop)
         static_assert(CC > 0, "staged m needs the compile-time column count");
-        stage_tile<T, (1 << LG_L), CC, CC * F::TG>(ms, a.m + b * a.m_stride + col0, nx, threadIdx.x);
+        if (a.mT)     // transposed m: the task's CC columns are one contiguous run
+            stage_tile_s<T, CC, (1 << LG_L), MtStride<T, (1 << LG_L), CC>::V, CC * F::TG>(
+                ms, a.mT + b * a.m_stride + (size_t)col0 * (1 << LG_L), (size_t)(1 << LG_L), threadIdx.x);
+        else
+            stage_tile<T, (1 << LG_L), CC, CC * F::TG>(ms, a.m + b * a.m_stride + col0, nx, threadIdx.x);
         cp_async_commit();
     }
     prefetch();
@@ -773,10 +806,17 @@ __device__ __forceinline__ void col_task(const ColArgs<T>& a, int b, int col0, i
                 cp_async_wait<1>();                  // m of this task (the prefetch may stay in flight)
                 __syncthreads();
             }
+            if constexpr (PS) {
+                if (a.mT) {
 #pragma unroll
-            for (int k = 0; k < F::R; ++k) {
-                if constexpr (PS) mm[k] = ms[(j + F::TG * k) * C + c];
-                else mm[k] = m[k * rs];
+                    for (int k = 0; k < F::R; ++k) mm[k] = ms[c * MtStride<T, (1 << LG_L), CC>::V + j + F::TG * k];
+                } else {
+#pragma unroll
+                    for (int k = 0; k < F::R; ++k) mm[k] = ms[(j + F::TG * k) * C + c];
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < F::R; ++k) mm[k] = m[k * rs];
             }
         }
         if (rec && act) {
@@ -1048,7 +1088,8 @@ struct SolveSmem {
     static constexpr int cols = FC::SM ? C * (FC::SM + pad) : 0;
     static constexpr int up16(int x) { return (x + 15) / 16 * 16; }
     static constexpr int EX = up16((int)sizeof(cx<T>) * (rows > cols ? rows : cols));
-    static constexpr int ST = up16((int)sizeof(T) * ((G > C ? G : C) << LG));
+    static constexpr int ST = up16((int)sizeof(T) * ((G > C ? G : C) << LG) +
+                                   (int)sizeof(T) * C * MtStride<T, (1 << LG), C>::PAD);   // + transposed-m pad
     static constexpr bool F32 = sizeof(T) == 4;
     static constexpr bool SAME = LGR_R == LGR_C;
     static constexpr int NTAB = 1;                                // forward transforms only (conjugate storage)

@@ -128,6 +128,24 @@ def test_identical_runs_bitwise(path):
     assert [r.gap for r in a.history] == [r.gap for r in b.history]
 
 
+def test_transposed_m_column_staging_matches_sweep_path():
+    """2048^2 fp32: the persistent kernel stages m from a transposed copy
+    (one contiguous run per column task); the sweep path reads m row-major.
+    Same iterates to fp32 tolerance, same gap history."""
+    spec, c, m = problem(2048, "single", spots=50)
+    plan = pm.transform.get_plan(spec, pm.SINGLE)
+    cfg = pm.SolveConfig(max_iters=8, precision=pm.SINGLE)
+    a = pm.solve(c, m, cfg)
+    plan.set_path(2)
+    try:
+        b = pm.solve(c, m, cfg)
+    finally:
+        plan.set_path(0)
+    assert orc.relative_l2(a.u_star.data, b.u_star.data) <= 1e-5
+    np.testing.assert_allclose([r.gap for r in a.history], [r.gap for r in b.history], rtol=1e-6)
+    np.testing.assert_allclose([r.err_lit for r in a.history], [r.err_lit for r in b.history], rtol=1e-5)
+
+
 def test_backend_selector_does_not_change_results():
     spec, c, m, _ = spot_problem(64)
     a = pm.solve(c, m, pm.SolveConfig(max_iters=10, backend=pm.BackendSelector("serial")))
