@@ -145,8 +145,7 @@ __device__ __forceinline__ void gen_dft_split(cx<T>* x) {
             } else {
                 // W_R^{b ka} = exp(DIR 2 pi i b ka / R)
                 constexpr double c = gen_kc(R, b * ka, false), sn = DIR * gen_kc(R, b * ka, true);
-                const cx<T> v = s[ka];
-                y[b * A + ka] = mk<T>(v.x * T(c) - v.y * T(sn), v.x * T(sn) + v.y * T(c));
+                y[b * A + ka] = cmul_cs(s[ka], T(c), T(sn));
             }
         });
     });
@@ -161,43 +160,45 @@ __device__ __forceinline__ void gen_dft_split(cx<T>* x) {
     }
 }
 
-// In-place DFT of R points, sign DIR (-1 forward), natural order.
+// r + c a with a real broadcast (one FFMA2 in fp32).
+__device__ __forceinline__ float2 cfmas(float2 a, float c, float2 r) { return fma2(a, make_float2(c, c), r); }
+__device__ __forceinline__ double2 cfmas(double2 a, double c, double2 r) {
+    return make_double2(r.x + c * a.x, r.y + c * a.y);
+}
+
+// In-place DFT of R points, sign DIR (-1 forward), natural order; fp32 in
+// packed f32x2 arithmetic (pm_fft.cuh helpers).
 template <typename T, int R, int DIR>
 __device__ __forceinline__ void gen_dft(cx<T>* x) {
     if constexpr (GenSplit<R>::A > 0) {
         gen_dft_split<T, R, DIR>(x);
     } else if constexpr (R == 2) {
         const cx<T> a = x[0], b = x[1];
-        x[0] = mk<T>(a.x + b.x, a.y + b.y);
-        x[1] = mk<T>(a.x - b.x, a.y - b.y);
+        x[0] = cadd(a, b);
+        x[1] = csub(a, b);
     } else if constexpr (R == 4) {
-        const cx<T> s02 = mk<T>(x[0].x + x[2].x, x[0].y + x[2].y), d02 = mk<T>(x[0].x - x[2].x, x[0].y - x[2].y);
-        const cx<T> s13 = mk<T>(x[1].x + x[3].x, x[1].y + x[3].y), d13 = mk<T>(x[1].x - x[3].x, x[1].y - x[3].y);
-        // DIR * i * d13
-        const cx<T> r13 = DIR < 0 ? mk<T>(d13.y, -d13.x) : mk<T>(-d13.y, d13.x);
-        x[0] = mk<T>(s02.x + s13.x, s02.y + s13.y);
-        x[2] = mk<T>(s02.x - s13.x, s02.y - s13.y);
-        x[1] = mk<T>(d02.x + r13.x, d02.y + r13.y);
-        x[3] = mk<T>(d02.x - r13.x, d02.y - r13.y);
+        const cx<T> s02 = cadd(x[0], x[2]), d02 = csub(x[0], x[2]);
+        const cx<T> s13 = cadd(x[1], x[3]), d13 = csub(x[1], x[3]);
+        x[0] = cadd(s02, s13);
+        x[2] = csub(s02, s13);
+        x[1] = add_rot<DIR>(d02, d13);          // d02 + DIR i d13
+        x[3] = add_rot<-DIR>(d02, d13);
     } else if constexpr (R == 8) {
         // two radix-4 DFTs (even / odd samples) combined with W8^k
         cx<T> e[4] = {x[0], x[2], x[4], x[6]}, o[4] = {x[1], x[3], x[5], x[7]};
         gen_dft<T, 4, DIR>(e);
         gen_dft<T, 4, DIR>(o);
         const T h = T(0.70710678118654752440084436210485);
-        const cx<T> o1 = DIR < 0 ? mk<T>(h * (o[1].x + o[1].y), h * (o[1].y - o[1].x))
-                                 : mk<T>(h * (o[1].x - o[1].y), h * (o[1].y + o[1].x));
-        const cx<T> o2 = DIR < 0 ? mk<T>(o[2].y, -o[2].x) : mk<T>(-o[2].y, o[2].x);
-        const cx<T> o3 = DIR < 0 ? mk<T>(h * (o[3].y - o[3].x), -h * (o[3].x + o[3].y))
-                                 : mk<T>(-h * (o[3].x + o[3].y), h * (o[3].x - o[3].y));
-        x[0] = mk<T>(e[0].x + o[0].x, e[0].y + o[0].y);
-        x[4] = mk<T>(e[0].x - o[0].x, e[0].y - o[0].y);
-        x[1] = mk<T>(e[1].x + o1.x, e[1].y + o1.y);
-        x[5] = mk<T>(e[1].x - o1.x, e[1].y - o1.y);
-        x[2] = mk<T>(e[2].x + o2.x, e[2].y + o2.y);
-        x[6] = mk<T>(e[2].x - o2.x, e[2].y - o2.y);
-        x[3] = mk<T>(e[3].x + o3.x, e[3].y + o3.y);
-        x[7] = mk<T>(e[3].x - o3.x, e[3].y - o3.y);
+        const cx<T> o1 = cmul_cs(o[1], h, T(DIR) * h);       // W8^1 = h (1 + DIR i)
+        const cx<T> o3 = cmul_cs(o[3], -h, T(DIR) * h);      // W8^3 = h (-1 + DIR i)
+        x[0] = cadd(e[0], o[0]);
+        x[4] = csub(e[0], o[0]);
+        x[1] = cadd(e[1], o1);
+        x[5] = csub(e[1], o1);
+        x[2] = add_rot<DIR>(e[2], o[2]);                     // W8^2 = DIR i
+        x[6] = add_rot<-DIR>(e[2], o[2]);
+        x[3] = cadd(e[3], o3);
+        x[7] = csub(e[3], o3);
     } else {
         // odd R: pair the samples n and R - n (a = sum, b = difference), so
         // y_j / y_{R-j} = x0 + sum_k c(jk) a_k  +/-  i DIR sum_k s(jk) b_k
@@ -205,28 +206,24 @@ __device__ __forceinline__ void gen_dft(cx<T>* x) {
         cx<T> a[H], b[H];
 #pragma unroll
         for (int k = 0; k < H; ++k) {
-            a[k] = mk<T>(x[k + 1].x + x[R - 1 - k].x, x[k + 1].y + x[R - 1 - k].y);
-            b[k] = mk<T>(x[k + 1].x - x[R - 1 - k].x, x[k + 1].y - x[R - 1 - k].y);
+            a[k] = cadd(x[k + 1], x[R - 1 - k]);
+            b[k] = csub(x[k + 1], x[R - 1 - k]);
         }
         const cx<T> x0 = x[0];
-        T sx = x0.x, sy = x0.y;
+        cx<T> s0 = x0;
 #pragma unroll
-        for (int k = 0; k < H; ++k) { sx += a[k].x; sy += a[k].y; }
-        x[0] = mk<T>(sx, sy);
+        for (int k = 0; k < H; ++k) s0 = cadd(s0, a[k]);
+        x[0] = s0;
 #pragma unroll
         for (int j = 1; j <= H; ++j) {
-            T rx = x0.x, ry = x0.y, ix = T(0), iy = T(0);
+            cx<T> re = x0, im = mk<T>(T(0), T(0));
 #pragma unroll
             for (int k = 0; k < H; ++k) {
-                const T c = T(gen_c(R, (j * (k + 1)) % R)), sn = T(DIR) * T(gen_s(R, (j * (k + 1)) % R));
-                rx += c * a[k].x;
-                ry += c * a[k].y;
-                ix += sn * b[k].x;
-                iy += sn * b[k].y;
+                re = cfmas(a[k], T(gen_c(R, (j * (k + 1)) % R)), re);
+                im = cfmas(b[k], T(DIR) * T(gen_s(R, (j * (k + 1)) % R)), im);
             }
-            // i * (ix + i iy) = -iy + i ix
-            x[j] = mk<T>(rx - iy, ry + ix);
-            x[R - j] = mk<T>(rx + iy, ry - ix);
+            x[j] = add_rot<1>(re, im);          // re + i im
+            x[R - j] = add_rot<-1>(re, im);
         }
     }
 }
@@ -254,8 +251,7 @@ __device__ __forceinline__ void gen_pass(const cx<T>* a, cx<T>* b, const cx<T>* 
 #pragma unroll
             for (int q = 1; q < R; ++q) {
                 const cx<T> w = tw[q * k * step];
-                const T ws = dir < 0 ? w.y : -w.y;
-                x[q] = mk<T>(x[q].x * w.x - x[q].y * ws, x[q].x * ws + x[q].y * w.x);
+                x[q] = cmul_cs(x[q], w.x, dir < 0 ? w.y : -w.y);
             }
         }
         if (dir < 0) gen_dft<T, R, -1>(x);
