@@ -1151,6 +1151,30 @@ int gen_rows_fwd(pm_plan* pl, int all_masks) {
                                                     all_masks);
 }
 
+// Launch configuration with programmatic dependent launch: the sweep kernel
+// may be scheduled while its predecessor drains; it prefetches its twiddles
+// and then waits (griddepcontrol.wait) before touching the predecessor's data.
+struct PdlConfig {
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute attr[1];
+    const cudaLaunchConfig_t* get() {
+        cfg.attrs = attr;
+        return &cfg;
+    }
+};
+PdlConfig pdl_config(dim3 grid, int threads, size_t smem, cudaStream_t stream) {
+    static const bool off = getenv("PM_NO_PDL") != nullptr;
+    PdlConfig c;
+    c.cfg.gridDim = grid;
+    c.cfg.blockDim = dim3(threads);
+    c.cfg.dynamicSmemBytes = smem;
+    c.cfg.stream = stream;
+    c.attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    c.attr[0].val.programmaticStreamSerializationAllowed = off ? 0 : 1;
+    c.cfg.numAttrs = 1;
+    return c;
+}
+
 int lg_of(int tc) {
     int l = 0;
     while ((1 << l) < tc) ++l;
@@ -1165,10 +1189,9 @@ int gen_col_sweep(pm_plan* pl, int u_iter, int metrics_only, int all_masks) {
     const dim3 grid((pl->nx + TC - 1) / TC, pl->s.batch);
     GenSolveArgs g = gen_args(pl);
     g.nblk = (int)grid.x;
-    gen_col_sweep_kernel<T><<<grid, pl->gnt_c, pl->gsm_c, pl->stream>>>(
-        (cx<T>*)pl->tmp, (const T*)pl->s.m, pl->thrm, pl->escale, (const cx<T>*)pl->gtwy, pl->gy, pl->nx,
-        lg_of(TC), g, u_iter, metrics_only, all_masks);
-    CK(cudaGetLastError());
+    CK(cudaLaunchKernelEx(pdl_config(grid, pl->gnt_c, pl->gsm_c, pl->stream).get(), gen_col_sweep_kernel<T>,
+                          (cx<T>*)pl->tmp, (const T*)pl->s.m, (const double*)pl->thrm, (const double*)pl->escale,
+                          (const cx<T>*)pl->gtwy, pl->gy, pl->nx, lg_of(TC), g, u_iter, metrics_only, all_masks));
     pl->launches++;
     return PM_OK;
 }
@@ -1178,10 +1201,10 @@ template <typename T>
 int gen_row_sweep(pm_plan* pl, int it) {
     const int TC = pl->gtc_r;
     const dim3 grid((pl->ny + TC - 1) / TC, pl->s.batch);
-    gen_row_sweep_kernel<T><<<grid, pl->gnt_r, pl->gsm_r, pl->stream>>>(
-        (cx<T>*)pl->tmp, (cx<T>*)pl->field, (const T*)pl->s.p, pl->s.p_stride, pl->thrx, (const cx<T>*)pl->gtwx,
-        pl->gx, pl->ny, lg_of(TC), pl->st, (long long)pl->N, it);
-    CK(cudaGetLastError());
+    CK(cudaLaunchKernelEx(pdl_config(grid, pl->gnt_r, pl->gsm_r, pl->stream).get(), gen_row_sweep_kernel<T>,
+                          (cx<T>*)pl->tmp, (cx<T>*)pl->field, (const T*)pl->s.p, (long long)pl->s.p_stride,
+                          (const double*)pl->thrx, (const cx<T>*)pl->gtwx, pl->gx, pl->ny, lg_of(TC), pl->st,
+                          (long long)pl->N, it));
     pl->launches++;
     return PM_OK;
 }

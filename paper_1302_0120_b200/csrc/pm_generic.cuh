@@ -310,6 +310,19 @@ template <typename T>
 __device__ __forceinline__ void gen_load_tw(cx<T>* tw, const cx<T>* src, int L) {
     for (int i = threadIdx.x; i < L; i += blockDim.x) cp_async<sizeof(cx<T>)>(tw + i, src + i);
 }
+// Programmatic dependent launch: wait until this kernel's predecessor has
+// completed and its writes are visible (a no-op without the launch
+// attribute); the successor is released as this grid's CTAs exit.
+#ifndef PM_PDL_EARLY
+#define PM_PDL_EARLY 0   // trigger the successor at kernel start (measured slower: its waiting CTAs hold slots)
+#endif
+__device__ __forceinline__ void gen_pdl_wait() {
+#if PM_PDL_EARLY
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 template <typename E>
 __device__ __forceinline__ void gen_gather(E* A, const E* src, int L, int lgTC, int t0, int tc, long long tstride,
                                            long long estride, E zero) {
@@ -387,18 +400,19 @@ __global__ void gen_col_sweep_kernel(cx<T>* w, const T* m, const double* thr_m, 
                                      const cx<T>* __restrict__ tw, GenPlan gp, int nx, int lgTC, GenSolveArgs g,
                                      int u_iter, int metrics_only, int all_masks) {
     extern __shared__ __align__(16) unsigned char smraw[];
+    const int TC = 1 << lgTC, L = gp.L;
+    GenSmem<T> sm(smraw, L, TC);
+    gen_load_tw<T>(sm.tw, tw, L);                 // constant: before the predecessor completes
+    gen_pdl_wait();
     const int b = blockIdx.y;
     MaskState* st = g.st + b;
     if (st->done || (!all_masks && st->stop)) return;
     const bool dec = u_iter >= 1 && st->decided < u_iter && !st->stop;
     const bool rec = dec && recorded(g.ctl, u_iter);
     const bool gneed = dec && gap_needed(g.ctl, u_iter);
-    const int TC = 1 << lgTC, L = gp.L;
     const int t0 = blockIdx.x * TC, tc = min(TC, nx - t0);
     const T sc = T(1.0 / sqrt((double)L));
-    GenSmem<T> sm(smraw, L, TC);
     cx<T>* wb = w + b * g.n;
-    gen_load_tw<T>(sm.tw, tw, L);
     gen_gather<cx<T>>(sm.A, wb, L, lgTC, t0, tc, 1, nx, mk<T>(T(0), T(0)));
     cp_async_commit();
     gen_gather<T>(sm.g, m + b * g.n, L, lgTC, t0, tc, 1, nx, T(0));    // m, in flight during the passes
@@ -452,15 +466,16 @@ __global__ void gen_row_sweep_kernel(cx<T>* w, cx<T>* u, const T* p, long long p
                                      const cx<T>* __restrict__ tw, GenPlan gp, int ny, int lgTC, MaskState* st,
                                      long long n, int it) {
     extern __shared__ __align__(16) unsigned char smraw[];
+    const int TC = 1 << lgTC, L = gp.L;
+    GenSmem<T> sm(smraw, L, TC);
+    gen_load_tw<T>(sm.tw, tw, L);                 // constant: before the predecessor completes
+    gen_pdl_wait();
     const int b = blockIdx.y;
     if (st[b].done || st[b].stop) return;
-    const int TC = 1 << lgTC, L = gp.L;
     const int t0 = blockIdx.x * TC, tc = min(TC, ny - t0);
     const T sc = T(1.0 / sqrt((double)L));
-    GenSmem<T> sm(smraw, L, TC);
     cx<T>* wb = w + b * n;
     cx<T>* ub = u + b * n;
-    gen_load_tw<T>(sm.tw, tw, L);
     gen_gather<cx<T>>(sm.A, wb, L, lgTC, t0, tc, L, 1, mk<T>(T(0), T(0)));
     cp_async_commit();
     gen_gather<T>(sm.g, p + b * p_stride, L, lgTC, t0, tc, L, 1, T(0));  // p, in flight during the passes
