@@ -18,7 +18,7 @@
  *    unshifted frequency order (src/transform.py:1-7).
  *  - n_x and n_y are at most 4096 with prime factors 2, 3, 5, 7; powers of
  *    two run the fused register-resident kernels, other sides the
- *    mixed-radix path (GS only).
+ *    mixed-radix path (GS and RAAR).
  *  - Every function returns 0 on success or a negative PM_ERR_* code;
  *    pm_last_error() returns the calling thread's last message.
  *  - "_device" variants take device pointers on the plan's device and run

@@ -701,6 +701,10 @@ int ensure_raar(pm_plan* pl) {
     pl->raar_cap = 0;
     const size_t n = (size_t)pl->cap * pl->N;
     CK(cudaMalloc(&pl->field2, n * pl->csz));
+    if (pl->generic) {                     // mixed radix: the second iterate buffer only
+        pl->raar_cap = pl->cap;
+        return PM_OK;
+    }
     CK(cudaMalloc(&pl->xbuf, n * pl->csz));
     CK(cudaMalloc((void**)&pl->rpart, (size_t)pl->cap * pl->ny * row_wpr(pl) * 2 * sizeof(double)));
     pl->raar_cap = pl->cap;
@@ -1061,14 +1065,17 @@ int gen_setup(pm_plan* pl) {
     shape_for(pl->gx, pl->ny, "PM_GEN_TCR", "PM_GEN_NTR", pl->gtc_r, pl->gnt_r);
     shape_for(pl->gy, pl->nx, "PM_GEN_TCC", "PM_GEN_NTC", pl->gtc_c, pl->gnt_c);
     {   // the register budget bounds the CTA size
-        cudaFuncAttributes fa[3];
+        cudaFuncAttributes fa[4];
         const bool f32 = pl->prec == PM_SINGLE;
         CK(cudaFuncGetAttributes(&fa[0], f32 ? (const void*)&gen_fft_kernel<float> : (const void*)&gen_fft_kernel<double>));
         CK(cudaFuncGetAttributes(&fa[1], f32 ? (const void*)&gen_col_sweep_kernel<float>
                                              : (const void*)&gen_col_sweep_kernel<double>));
         CK(cudaFuncGetAttributes(&fa[2], f32 ? (const void*)&gen_row_sweep_kernel<float>
                                              : (const void*)&gen_row_sweep_kernel<double>));
-        const int cap = std::min({fa[0].maxThreadsPerBlock, fa[1].maxThreadsPerBlock, fa[2].maxThreadsPerBlock}) / 32 * 32;
+        CK(cudaFuncGetAttributes(&fa[3], f32 ? (const void*)&gen_row_raar_kernel<float>
+                                             : (const void*)&gen_row_raar_kernel<double>));
+        const int cap = std::min({fa[0].maxThreadsPerBlock, fa[1].maxThreadsPerBlock, fa[2].maxThreadsPerBlock,
+                                  fa[3].maxThreadsPerBlock}) / 32 * 32;
         pl->gnt_r = std::min(pl->gnt_r, cap);
         pl->gnt_c = std::min(pl->gnt_c, cap);
     }
@@ -1080,10 +1087,12 @@ int gen_setup(pm_plan* pl) {
         e = allow_smem((const void*)&gen_fft_kernel<float>, mx);
         if (e == cudaSuccess) e = allow_smem((const void*)&gen_col_sweep_kernel<float>, mx);
         if (e == cudaSuccess) e = allow_smem((const void*)&gen_row_sweep_kernel<float>, mx);
+        if (e == cudaSuccess) e = allow_smem((const void*)&gen_row_raar_kernel<float>, mx);
     } else {
         e = allow_smem((const void*)&gen_fft_kernel<double>, mx);
         if (e == cudaSuccess) e = allow_smem((const void*)&gen_col_sweep_kernel<double>, mx);
         if (e == cudaSuccess) e = allow_smem((const void*)&gen_row_sweep_kernel<double>, mx);
+        if (e == cudaSuccess) e = allow_smem((const void*)&gen_row_raar_kernel<double>, mx);
     }
     if (e != cudaSuccess) return cuda_err(e, "cudaFuncSetAttribute(gen kernels)");
     return PM_OK;
@@ -1191,7 +1200,8 @@ int gen_col_sweep(pm_plan* pl, int u_iter, int metrics_only, int all_masks) {
     g.nblk = (int)grid.x;
     CK(cudaLaunchKernelEx(pdl_config(grid, pl->gnt_c, pl->gsm_c, pl->stream).get(), gen_col_sweep_kernel<T>,
                           (cx<T>*)pl->tmp, (const T*)pl->s.m, (const double*)pl->thrm, (const double*)pl->escale,
-                          (const cx<T>*)pl->gtwy, pl->gy, pl->nx, lg_of(TC), g, u_iter, metrics_only, all_masks));
+                          (const cx<T>*)pl->gtwy, pl->gy, pl->nx, lg_of(TC), g, u_iter, metrics_only, all_masks,
+                          pl->s.prm.algorithm == PM_ALGO_RAAR ? 1 : 0));
     pl->launches++;
     return PM_OK;
 }
@@ -1229,10 +1239,55 @@ int gen_begin(pm_plan* pl) {
 // Two fused sweeps per iteration over the work buffer, which holds
 // RowFFT(u_{it-1}) on entry and RowFFT(u_it) on exit; the iterate itself is
 // kept in `field` so a mask that stops keeps its last iterate.
+// RAAR row sweep of iteration `it` (x_{it-1} from the buffer of its parity,
+// x_it into the other; upd = 0: gap + decision of x_{it-1} only).
+template <typename T>
+int gen_row_raar(pm_plan* pl, int it, int upd) {
+    const int TC = pl->gtc_r;
+    const dim3 grid((pl->ny + TC - 1) / TC, pl->s.batch);
+    GenSolveArgs g = gen_args(pl);
+    g.nblk = (int)grid.x;
+    cx<T>* xs[2] = {(cx<T>*)pl->field, (cx<T>*)pl->field2};
+    const auto& prm = pl->s.prm;
+    CK(cudaLaunchKernelEx(pdl_config(grid, pl->gnt_r, pl->gsm_r, pl->stream).get(), gen_row_raar_kernel<T>,
+                          (cx<T>*)pl->tmp, (const cx<T>*)xs[(it - 1) & 1], xs[it & 1], (const T*)pl->s.p,
+                          (long long)pl->s.p_stride, (const double*)pl->thrx, (const cx<T>*)pl->gtwx, pl->gx, pl->ny,
+                          lg_of(TC), g, (T)prm.beta, (T)(1.0 - 2.0 * prm.beta), (const double*)pl->energy,
+                          pl->escale, it, upd));
+    pl->launches++;
+    return PM_OK;
+}
+
+// RAAR: gap + decision of the current iterate x_{s.it} now (the stepping
+// API's probe, and the last iterate before the pair). The column sweep
+// leaves RowFFT(P_M x) in the work buffer for the row probe; `restore`
+// puts RowFFT(x) back for further steps.
+int gen_raar_probe(pm_plan* pl, bool restore) {
+    const bool f32 = pl->prec == PM_SINGLE;
+    const int it = pl->s.it;
+    CKR(f32 ? gen_col_sweep<float>(pl, it, 0, 0) : gen_col_sweep<double>(pl, it, 0, 0));   // lit / dark, P_M
+    CKR(f32 ? gen_row_raar<float>(pl, it + 1, 0) : gen_row_raar<double>(pl, it + 1, 0));   // gap, decision
+    if (!restore) return PM_OK;
+    const void* x = (it & 1) ? pl->field2 : pl->field;
+    return f32 ? gen_axis<float>(pl, x, pl->tmp, 0, PM_FORWARD, pl->s.batch, pl->st, 0)
+               : gen_axis<double>(pl, x, pl->tmp, 0, PM_FORWARD, pl->s.batch, pl->st, 0);
+}
+
 int gen_steps(pm_plan* pl, int n, bool probe) {
     auto& s = pl->s;
     const bool f32 = pl->prec == PM_SINGLE;
     bool any = false;
+    if (s.prm.algorithm == PM_ALGO_RAAR) {
+        for (int i = 0; i < n && s.it < s.prm.max_iters; ++i) {
+            s.it += 1;
+            any = true;
+            // lit / dark of x_{it-1}; then its gap + decision and x_it
+            CKR(f32 ? gen_col_sweep<float>(pl, s.it - 1, 0, 0) : gen_col_sweep<double>(pl, s.it - 1, 0, 0));
+            CKR(f32 ? gen_row_raar<float>(pl, s.it, 1) : gen_row_raar<double>(pl, s.it, 1));
+        }
+        if (any && probe) CKR(gen_raar_probe(pl, true));
+        return PM_OK;
+    }
     for (int i = 0; i < n && s.it < s.prm.max_iters; ++i) {
         s.it += 1;
         any = true;
@@ -1260,8 +1315,22 @@ int gen_final_t(pm_plan* pl) {
 // then u*, the mask and the levels.
 int gen_finish(pm_plan* pl) {
     const bool f32 = pl->prec == PM_SINGLE;
+    int u_iter = pl->s.it;
+    if (pl->s.prm.algorithm == PM_ALGO_RAAR) {
+        CKR(gen_raar_probe(pl, false));    // the last iterate's gap and decision (no-op where taken)
+        const dim3 grid(gen_elem_blocks(pl), pl->s.batch);
+        if (f32)
+            gen_pick_kernel<float><<<grid, 256, 0, pl->stream>>>((float2*)pl->field, (const float2*)pl->field2, pl->st,
+                                                                 (long long)pl->N, pl->s.it);
+        else
+            gen_pick_kernel<double><<<grid, 256, 0, pl->stream>>>((double2*)pl->field, (const double2*)pl->field2,
+                                                                  pl->st, (long long)pl->N, pl->s.it);
+        CK(cudaGetLastError());
+        pl->launches++;
+        u_iter = 0;                        // every decision is taken
+    }
     CKR(gen_rows_fwd(pl, 1));              // every mask from its last iterate (stopped ones included)
-    CKR(f32 ? gen_col_sweep<float>(pl, pl->s.it, 0, 1) : gen_col_sweep<double>(pl, pl->s.it, 0, 1));
+    CKR(f32 ? gen_col_sweep<float>(pl, u_iter, 0, 1) : gen_col_sweep<double>(pl, u_iter, 0, 1));
     CKR(f32 ? gen_axis<float>(pl, pl->tmp, pl->tmp, 0, PM_INVERSE, pl->s.batch, pl->st, 1)
             : gen_axis<double>(pl, pl->tmp, pl->tmp, 0, PM_INVERSE, pl->s.batch, pl->st, 1));
     return f32 ? gen_final_t<float>(pl) : gen_final_t<double>(pl);
@@ -1348,8 +1417,6 @@ constexpr int kTolBlocks = 64;
 int session_setup(pm_plan* pl, const void* d_p, const void* d_m, int batch, const pm_params* prm,
                   const double* tol_p, const double* tol_m, const double* energy) {
     CKR(validate_params(prm, batch));
-    if (pl->generic && prm->algorithm == PM_ALGO_RAAR)
-        return set_err(PM_ERR_UNSUPPORTED, "RAAR needs power-of-two grid sides (the mixed-radix path runs GS)");
     CKR(ensure_capacity(pl, batch, prm->max_iters));
     if (prm->algorithm == PM_ALGO_RAAR) CKR(ensure_raar(pl));
     auto& s = pl->s;

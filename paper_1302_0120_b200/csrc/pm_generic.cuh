@@ -398,7 +398,7 @@ struct GenSolveArgs {
 template <typename T>
 __global__ void gen_col_sweep_kernel(cx<T>* w, const T* m, const double* thr_m, const double* escale,
                                      const cx<T>* __restrict__ tw, GenPlan gp, int nx, int lgTC, GenSolveArgs g,
-                                     int u_iter, int metrics_only, int all_masks) {
+                                     int u_iter, int metrics_only, int all_masks, int raar) {
     extern __shared__ __align__(16) unsigned char smraw[];
     const int TC = 1 << lgTC, L = gp.L;
     GenSmem<T> sm(smraw, L, TC);
@@ -409,7 +409,9 @@ __global__ void gen_col_sweep_kernel(cx<T>* w, const T* m, const double* thr_m, 
     if (st->done || (!all_masks && st->stop)) return;
     const bool dec = u_iter >= 1 && st->decided < u_iter && !st->stop;
     const bool rec = dec && recorded(g.ctl, u_iter);
-    const bool gneed = dec && gap_needed(g.ctl, u_iter);
+    // RAAR: only lit / dark here (kept in the mask state); the gap and the
+    // decision come from the next row sweep, where x and P_M x meet
+    const bool gneed = dec && !raar && gap_needed(g.ctl, u_iter);
     const int t0 = blockIdx.x * TC, tc = min(TC, nx - t0);
     const T sc = T(1.0 / sqrt((double)L));
     cx<T>* wb = w + b * g.n;
@@ -454,8 +456,14 @@ __global__ void gen_col_sweep_kernel(cx<T>* w, const T* m, const double* thr_m, 
     if (!dec) return;
     double tot[3];
     if (reduce_ticket<3>(acc, g.part + (size_t)b * g.nblk * 3, g.ctr + b, g.nblk, blockIdx.x, tot) &&
-        threadIdx.x == 0)
-        decide(st, g.hist + ((size_t)b * g.hist_stride + (u_iter - 1)) * 4, g.ctl, u_iter, rec, tot);
+        threadIdx.x == 0) {
+        if (raar) {
+            st->pend_lit = tot[1];
+            st->pend_dark = tot[2];
+        } else {
+            decide(st, g.hist + ((size_t)b * g.hist_stride + (u_iter - 1)) * 4, g.ctl, u_iter, rec, tot);
+        }
+    }
 }
 
 // Row sweep of the mixed-radix solve, fused: RowIFFT of the work buffer ->
@@ -501,6 +509,97 @@ __global__ void gen_row_sweep_kernel(cx<T>* w, cx<T>* u, const T* p, long long p
     gen_scatter<T>(A, ub, L, lgTC, t0, tc, L, 1, T(1));     // the iterate, coalesced along the row
     A = gen_passes<T>(A, B, sm.tw, gp, lgTC, -1);
     gen_scatter<T>(A, wb, L, lgTC, t0, tc, L, 1, sc);
+}
+
+// RAAR row sweep of iteration `it`: RowIFFT of the work
+// buffer gives v = P_M x_{it-1}; with x_{it-1} from `x_in`:
+//   gap of x_{it-1} = ||P_S x_{it-1} - v|| (src/metrics.py:67-71), when needed;
+//   x_it = beta x + beta P_S(2v - x) + (1 - 2 beta) v into `x_out` (upd), in
+//   numpy's operation order, then RowFFT(x_it) back into the work buffer.
+// The iterates alternate between two buffers so a mask that stops at
+// x_{it-1} (decided here, after x_it is written) keeps it. The last CTA of a
+// mask (ticket) sums the gap and |x_it|^2 partials in a fixed order, takes
+// the record / early-stop decision of x_{it-1} with the column sweep's
+// lit / dark, and leaves E / sum |x_it|^2 (the reconstructed-intensity scale of
+// x_it) in `xsc` for the next column sweep. upd = 0: measure and decide only
+// (the last iterate, the stepping API's probe).
+template <typename T>
+__global__ void gen_row_raar_kernel(cx<T>* w, const cx<T>* x_in, cx<T>* x_out, const T* p, long long p_stride,
+                                    const double* thr_p, const cx<T>* __restrict__ tw, GenPlan gp, int ny, int lgTC,
+                                    GenSolveArgs g, T beta, T c1, const double* energy, double* xsc, int it,
+                                    int upd) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    const int TC = 1 << lgTC, L = gp.L;
+    GenSmem<T> sm(smraw, L, TC);
+    gen_load_tw<T>(sm.tw, tw, L);
+    gen_pdl_wait();
+    const int b = blockIdx.y;
+    MaskState* st = g.st + b;
+    if (st->done || st->stop) return;
+    const int i = it - 1;                                     // the iterate measured here
+    const bool dec = i >= 1 && st->decided < i;
+    const bool rec = dec && recorded(g.ctl, i);
+    const bool gneed = dec && gap_needed(g.ctl, i);
+    const int t0 = blockIdx.x * TC, tc = min(TC, ny - t0);
+    const T sc = T(1.0 / sqrt((double)L));
+    cx<T>* wb = w + b * g.n;
+    gen_gather<cx<T>>(sm.A, wb, L, lgTC, t0, tc, L, 1, mk<T>(T(0), T(0)));
+    cp_async_commit();
+    gen_gather<T>(sm.g, p + b * p_stride, L, lgTC, t0, tc, L, 1, T(0));
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    cx<T>* A = gen_passes<T>(sm.A, sm.B, sm.tw, gp, lgTC, +1);
+    cx<T>* B = A == sm.A ? sm.B : sm.A;
+    cp_async_wait<0>();
+    __syncthreads();
+    const T thr = T(thr_p[b]);
+    const cx<T>* xb = x_in + b * g.n;
+    cx<T>* xo = x_out + b * g.n;
+    double g2 = 0.0, e2 = 0.0;
+    for (int idx = threadIdx.x; idx < L * TC; idx += blockDim.x) {
+        const int k = idx >> lgTC, t = idx & (TC - 1);
+        if (t >= tc) continue;
+        const long long e = (long long)(t0 + t) * L + k;
+        const cx<T> vv = cscale(A[idx], sc);                  // v = P_M x_{it-1}
+        const cx<T> xx = xb[e];
+        const T pk = sm.g[idx];
+        if (gneed) g2 += norm_sq_d(csub_rn(replace_mod(xx, pk, thr), vv));
+        if (upd) {
+            const cx<T> py = replace_mod(csub_rn(cscale(vv, T(2)), xx), pk, thr);
+            const cx<T> xn = cadd_rn(cadd_rn(cmul_rn(xx, beta), cmul_rn(py, beta)), cmul_rn(vv, c1));
+            xo[e] = xn;
+            e2 += norm_sq_d(xn);
+            A[idx] = xn;
+        }
+    }
+    if (upd && !isfinite(e2)) first_bad(&st->bad, it);
+    double acc[2] = {g2, e2}, tot[2];
+    const bool last = reduce_ticket<2>(acc, g.part + (size_t)b * g.nblk * 2, g.ctr + b, g.nblk, blockIdx.x, tot);
+    if (last && threadIdx.x == 0) {
+        if (upd) xsc[b] = energy[b] / tot[1];
+        if (dec) {
+            const double t3[3] = {tot[0], st->pend_lit, st->pend_dark};
+            decide(st, g.hist + ((size_t)b * g.hist_stride + (i - 1)) * 4, g.ctl, i, rec, t3);
+        }
+    }
+    if (!upd) return;
+    __syncthreads();
+    A = gen_passes<T>(A, B, sm.tw, gp, lgTC, -1);
+    gen_scatter<T>(A, wb, L, lgTC, t0, tc, L, 1, sc);
+}
+
+// RAAR finish: the final iterate of mask b is x_j, j = iters_run (stopped)
+// or `it` (aborted); odd j lives in the second buffer and is copied into the
+// first, which the best-approximation pair then reads.
+template <typename T>
+__global__ void gen_pick_kernel(cx<T>* x0, const cx<T>* x1, const MaskState* st, long long n, int it) {
+    const int b = blockIdx.y;
+    if (st[b].done) return;
+    const int j = st[b].stop ? st[b].iters_run : it;
+    if (!(j & 1)) return;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        x0[b * n + i] = x1[b * n + i];
 }
 
 // Best-approximation pair and mask from v* (src/solver.py:201-206).

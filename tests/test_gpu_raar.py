@@ -159,3 +159,54 @@ def test_raar_is_deterministic():
     b = gpu(p, m, "single", max_iters=30, beta=0.9)
     np.testing.assert_array_equal(a.mask.phases, b.mask.phases)
     assert [x.gap for x in a.history] == [x.gap for x in b.history]
+
+
+# --- mixed-radix grids (pm_generic.cuh: alternating iterate buffers) --------
+
+@pytest.mark.parametrize("nx,ny", [(60, 42), (100, 64), (120, 90)])
+def test_raar_mixed_radix_fp64_matches_oracle(nx, ny):
+    p, m = make_problem(nx, 6, 5, n_y=ny)
+    o = orc.solve(p, m, 20, "double", algorithm="raar", beta=0.9, record_every=3)
+    check_vs(gpu(p, m, "double", max_iters=20, beta=0.9, record_every=3), o, "double", 1e-10)
+
+
+def test_raar_mixed_radix_fp32_paper_grid():
+    p, m = make_problem(800, 12, 7, n_y=600)
+    o = orc.solve(p, m, 5, "single", algorithm="raar", beta=0.9)
+    check_vs(gpu(p, m, "single", max_iters=5, beta=0.9), o, "single", 1e-5)
+
+
+def test_raar_mixed_radix_early_stop_callbacks_abort_and_batch():
+    p, m = make_problem(120, 6, 3, n_y=90)
+    spec = pm.GridSpec(120, 90)
+    c, mc = pm.SlmConstraint(pm.RealGrid(spec, p)), pm.FourierConstraint(pm.RealGrid(spec, m))
+    # early stop on an odd and an even iterate (the two iterate buffers)
+    for tol in (1e-3, 3e-3):
+        o = orc.solve(p, m, 200, "double", algorithm="raar", beta=0.6, early_stop_tol=tol)
+        r = pm.solve(c, mc, pm.SolveConfig(max_iters=200, algorithm="raar", beta=0.6, early_stop_tol=tol))
+        assert o["iters_run"] < 200
+        check_vs(r, o, "double", 1e-9, field=o["iters_run"] <= 20)
+    # stepped solve (callbacks) == one-shot solve
+    seen = []
+    cfg = pm.SolveConfig(max_iters=11, algorithm="raar", beta=0.8, record_every=2)
+    rc = pm.solve(c, mc, cfg, on_record=seen.append)
+    rn = pm.solve(c, mc, cfg)
+    assert [x.iter for x in seen] == [1, 3, 5, 7, 9, 11]
+    assert [x.gap for x in seen] == [x.gap for x in rn.history]
+    np.testing.assert_array_equal(rc.u_star.data, rn.u_star.data)
+    # abort after three polls: the pair comes from x_3 (odd: second buffer)
+    polls = []
+
+    def abort():
+        polls.append(1)
+        return len(polls) >= 3
+
+    ra = pm.solve(c, mc, pm.SolveConfig(max_iters=50, algorithm="raar", beta=0.9), should_abort=abort)
+    o = orc.solve(p, m, 3, "double", algorithm="raar", beta=0.9)
+    assert ra.aborted and ra.iters_run == 3
+    check_vs(ra, o, "double", 1e-10)
+    # a batch equals its single solves bitwise
+    ms = np.stack([make_problem(120, 6, s, n_y=90)[1] for s in (3, 4)])
+    res = solve_stack(p, ms, cfg)
+    np.testing.assert_array_equal(res.phases[0], rn.mask.phases)
+

@@ -324,8 +324,6 @@ def test_mixed_radix_early_stop_callbacks_and_batch():
     ms = np.stack([make_problem(120, 6, s, n_y=90)[1] for s in (3, 4)])
     res = solve_stack(p, ms, pm.SolveConfig(max_iters=9, record_every=4))
     np.testing.assert_array_equal(res.phases[0], rn.mask.phases)
-    with pytest.raises(NotImplementedError):
-        pm.solve(c, mc, pm.SolveConfig(max_iters=3, algorithm="raar"))
 
 
 def test_batch_device_tolerances_match_host_and_reject_zero_inputs():
