@@ -47,5 +47,6 @@ run(60, 42, "double")
 run(30, 40, "single", batch=2)
 run(256, 256, "single", batch=24, K=2)            # TMA build (column tiles via cp.async.bulk.tensor)
 run(512, 512, "single", algo="raar", batch=5, K=2)
+run(60, 42, "double", algo="raar", K=4)          # mixed-radix RAAR (alternating iterate buffers)
 run(800, 600, "single", K=2, rand=True)            # mixed radix 16 x 10 x 5 / 12 x 10 x 5, device random start
 run(2048, 2048, "single", K=1)                     # persistent column phase staging m from its transposed copy
