@@ -137,6 +137,112 @@ def solve_stack(p: np.ndarray, m_stack: np.ndarray, cfg: SolveConfig, device: in
     return out
 
 
+def solve_stream(items, cfg: SolveConfig, device: int = 0, out_phases: list | None = None):
+    """A real-time sequence of masks on one device (the paper's interactive
+    use: a new target pattern per frame), pipelined.
+
+    ``items`` yields ``(p, m)`` pairs of (n_y, n_x) host arrays (pinned for
+    full-speed copies), one mask per item. While mask i is solved, the
+    upload of item i+1 and the download of mask i-1 run on their own CUDA
+    streams, so a frame costs about max(solve, transfers) instead of their
+    sum. Yields one :class:`BatchResult` (batch 1) per item, in order, one
+    item behind the solve. ``out_phases``: optional two (1, n_y, n_x) float64
+    (pinned) host buffers, used alternately for the masks (a yielded mask
+    stays valid until two more have been produced); otherwise fresh arrays.
+    Every solve is :func:`solve_stack`'s (device tolerances and energy),
+    bitwise.
+    """
+    import torch                                        # streams and events only (plumbing)
+
+    dev = torch.device("cuda", device)
+    it = iter(items)
+    first = next(it, None)
+    if first is None:
+        return
+    p0 = np.asarray(first[0])
+    ny, nx = p0.shape
+    prec = cfg.precision
+    fdt = prec.float_dtype
+    tdt = torch.float32 if fdt == np.float32 else torch.float64
+    plan = get_plan(GridSpec(nx, ny), prec, device)
+    K = cfg.max_iters
+    prm = _params(cfg, False, False)
+    # the solve runs on the plan's own stream; uploads and downloads on two more
+    h = _lib.C.c_void_p(0)
+    _lib.check(plan.lib.pm_plan_get_stream(plan.handle, _lib.C.byref(h)), "pm_plan_get_stream")
+    compute = torch.cuda.ExternalStream(h.value or 0, device=dev)
+    up, down = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    d_p = [torch.empty((ny, nx), dtype=tdt, device=dev) for _ in range(2)]
+    d_m = [torch.empty((ny, nx), dtype=tdt, device=dev) for _ in range(2)]
+    d_ph = [torch.empty((ny, nx), dtype=torch.float64, device=dev) for _ in range(2)]
+    ev_up = [torch.cuda.Event() for _ in range(2)]
+    ev_done = [torch.cuda.Event() for _ in range(2)]
+    ev_down = [torch.cuda.Event() for _ in range(2)]
+    outs = out_phases or [None, None]
+
+    def upload(slot, item):
+        pp = np.ascontiguousarray(item[0], dtype=fdt)
+        mm = np.ascontiguousarray(item[1], dtype=fdt)
+        if pp.shape != (ny, nx) or mm.shape != (ny, nx):
+            raise ValueError("amplitude and target constraints live on different grids")
+        with torch.cuda.stream(up):
+            up.wait_event(ev_done[slot])               # the solve two frames back read this slot
+            d_p[slot].copy_(torch.from_numpy(pp), non_blocking=True)
+            d_m[slot].copy_(torch.from_numpy(mm), non_blocking=True)
+            ev_up[slot].record(up)
+        return pp, mm                                  # keep the host arrays alive until copied
+
+    pending = None                                     # (slot, BatchResult, host phases) of the last frame
+    keep = [upload(0, first), None]
+    item, i = first, 0
+    try:
+        while item is not None:
+            s = i & 1
+            nxt = next(it, None)
+            if nxt is not None:
+                keep[s ^ 1] = upload(s ^ 1, nxt)
+            compute.wait_event(ev_up[s])
+            compute.wait_event(ev_down[s])        # d_ph[s] downloaded (frame i-2)
+            res_py = BatchResult(None, np.full((1, K), np.nan), np.full((1, K), np.nan),
+                                 np.full((1, K), np.nan), np.zeros(1, np.int32))
+            div = np.zeros(1, np.int32)
+            ms = np.zeros(1, np.float32)
+            res = _lib.pm_result()
+            res.phases = _lib.C.c_void_p(d_ph[s].data_ptr())
+            res.gap, res.err_lit, res.err_dark = (_lib.ptr(res_py.gap), _lib.ptr(res_py.err_lit),
+                                                  _lib.ptr(res_py.err_dark))
+            res.iters_run, res.diverged_iter, res.device_ms = (_lib.ptr(res_py.iters_run), _lib.ptr(div),
+                                                               _lib.ptr(ms))
+            with plan.lock:
+                code = plan.lib.pm_solve_device(plan.handle, _lib.C.c_void_p(d_p[s].data_ptr()),
+                                                _lib.C.c_void_p(d_m[s].data_ptr()), None, 1, prm, None, None,
+                                                None, res)
+            if code == _lib.PM_ERR_DIVERGED or div.any():
+                raise SolveDivergedError(int(div[0]) or 1)
+            _lib.check(code, "pm_solve_device")
+            res_py.device_ms = float(ms[0])
+            ev_done[s].record(compute)
+            host = outs[s] if outs[s] is not None else np.empty((1, ny, nx))
+            with torch.cuda.stream(down):
+                down.wait_event(ev_done[s])
+                torch.from_numpy(host).view(ny, nx).copy_(d_ph[s], non_blocking=True)
+                ev_down[s].record(down)
+            if pending is not None:                # frame i-1: its download ran during this solve
+                ps, pres, phost = pending
+                ev_down[ps].synchronize()
+                pres.phases = phost
+                yield pres
+            pending = (s, res_py, host)
+            item, i = nxt, i + 1
+        ps, pres, phost = pending
+        ev_down[ps].synchronize()
+        pres.phases = phost
+        yield pres
+    finally:
+        torch.cuda.synchronize(dev)
+    del keep
+
+
 def solve_batch(p: np.ndarray, m_stack: np.ndarray, cfg: SolveConfig,
                 devices: list[int] | None = None, **kw) -> BatchResult:
     """Shard a stack of masks across local GPUs (one host thread per device).

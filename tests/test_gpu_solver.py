@@ -367,3 +367,27 @@ def test_tma_batch_variant_is_bitwise_equal_to_single_solves(n, tag, algo, B):
         np.testing.assert_array_equal(r.mask.phases, whole.phases[i])
         assert r.iters_run == whole.iters_run[i]
         assert [h.gap for h in r.history] == list(whole.gap[i][~np.isnan(whole.gap[i])])
+
+
+def test_solve_stream_matches_solve_stack_frame_by_frame():
+    """batch.solve_stream (pipelined frames: uploads / downloads overlap the
+    solves) returns every frame's solve_stack result bitwise, in order."""
+    import torch
+    from paper_1302_0120_b200.batch import solve_stream
+    p, _ = make_problem(256, 8, 7)
+    ms = [make_problem(256, 8, s)[1] for s in (21, 22, 23, 24, 25)]
+    cfg = pm.SolveConfig(max_iters=12, precision=pm.SINGLE, record_every=3)
+    outs = [torch.empty((1, 256, 256), dtype=torch.float64).pin_memory().numpy() for _ in range(2)]
+    for out_phases in (None, outs):
+        got = []
+        for r in solve_stream(((p, m) for m in ms), cfg, out_phases=out_phases):
+            got.append((r.phases.copy(), r.gap.copy(), r.iters_run.copy()))
+        assert len(got) == len(ms)
+        for (ph, gap, its), m in zip(got, ms):
+            ref = solve_stack(p.astype(np.float32), m[None].astype(np.float32), cfg)
+            np.testing.assert_array_equal(ph, ref.phases)
+            np.testing.assert_array_equal(gap, ref.gap)
+            assert its[0] == ref.iters_run[0] == 12
+    assert list(solve_stream(iter(()), cfg)) == []
+    with pytest.raises(ValueError, match="different grids"):
+        list(solve_stream([(p, ms[0]), (p, ms[1][:128])], cfg))
