@@ -21,6 +21,7 @@ which CTA or device handled the mask.
 
 from __future__ import annotations
 
+import warnings
 from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass
 
@@ -185,7 +186,9 @@ def solve_stream(items, cfg: SolveConfig, device: int = 0, out_phases: list | No
         mm = np.ascontiguousarray(item[1], dtype=fdt)
         if pp.shape != (ny, nx) or mm.shape != (ny, nx):
             raise ValueError("amplitude and target constraints live on different grids")
-        with torch.cuda.stream(up):
+        with torch.cuda.stream(up), warnings.catch_warnings():
+            # read-only host arrays are only read here (torch warns on any non-writable array)
+            warnings.simplefilter("ignore", UserWarning)
             up.wait_event(ev_done[slot])               # the solve two frames back read this slot
             d_p[slot].copy_(torch.from_numpy(pp), non_blocking=True)
             d_m[slot].copy_(torch.from_numpy(mm), non_blocking=True)

@@ -391,3 +391,18 @@ def test_solve_stream_matches_solve_stack_frame_by_frame():
     assert list(solve_stream(iter(()), cfg)) == []
     with pytest.raises(ValueError, match="different grids"):
         list(solve_stream([(p, ms[0]), (p, ms[1][:128])], cfg))
+
+
+def test_solve_stream_mixed_radix_raar_and_random_start():
+    """solve_stream on the mixed-radix path, with RAAR and a seeded random
+    start drawn on the device: each frame equals its solve_stack result."""
+    from paper_1302_0120_b200.batch import solve_stream
+    p, _ = make_problem(120, 6, 3, n_y=90)
+    ms = [make_problem(120, 6, s, n_y=90)[1] for s in (5, 6, 7)]
+    for cfg in (pm.SolveConfig(max_iters=9, algorithm="raar", beta=0.8, record_every=2),
+                pm.SolveConfig(max_iters=9, random_phase_init=True, seed=4, record_every=3)):
+        got = [(r.phases.copy(), r.gap.copy()) for r in solve_stream(((p, m) for m in ms), cfg)]
+        for (ph, gap), m in zip(got, ms):
+            ref = solve_stack(p, m[None], cfg)
+            np.testing.assert_array_equal(ph, ref.phases)
+            np.testing.assert_array_equal(gap, ref.gap)
