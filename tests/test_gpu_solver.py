@@ -144,6 +144,13 @@ def test_transposed_m_column_staging_matches_sweep_path():
     assert orc.relative_l2(a.u_star.data, b.u_star.data) <= 1e-5
     np.testing.assert_allclose([r.gap for r in a.history], [r.gap for r in b.history], rtol=1e-6)
     np.testing.assert_allclose([r.err_lit for r in a.history], [r.err_lit for r in b.history], rtol=1e-5)
+    # the stepping API (callbacks) keeps the transposed copy across its launches
+    seen = []
+    c3 = pm.SolveConfig(max_iters=3, precision=pm.SINGLE)
+    stepped = pm.solve(c, m, c3, on_record=seen.append)
+    whole = pm.solve(c, m, c3)
+    assert [x.gap for x in seen] == [x.gap for x in whole.history]
+    np.testing.assert_array_equal(stepped.mask.phases, whole.mask.phases)
 
 
 def test_backend_selector_does_not_change_results():
