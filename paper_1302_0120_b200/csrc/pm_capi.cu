@@ -1532,12 +1532,14 @@ bool persistent(const pm_plan* pl) {
 // of m per column task instead of n_y runs shorter than a 32-byte sector):
 // 4096^2 fp32 335 -> 300 us per iteration, 2048^2 67.3 -> 65.6; neutral or
 // slightly worse where the runs are already >= 32 bytes (1024^2 fp32, fp64),
-// so only below that. Not for the TMA variant, which streams m boxes itself.
+// so only below that. Not when the TMA variant streams m boxes itself (its
+// field-only form, 2048^2 / 4096^2, stages m from this copy).
 int enqueue_mT(pm_plan* pl) {
     static const bool off = getenv("PM_NO_MT") != nullptr;
     auto& s = pl->s;
     s.mT = nullptr;
-    if (off || !persistent(pl) || tma_wanted(pl) || (size_t)solve_cols(pl) * pl->rsz >= 32) return PM_OK;
+    const bool tma_streams_m = tma_wanted(pl) && kset(pl->prec, pl->lgx).solve_tma_m;
+    if (off || !persistent(pl) || tma_streams_m || (size_t)solve_cols(pl) * pl->rsz >= 32) return PM_OK;
     const size_t bytes = (size_t)s.batch * pl->N * pl->rsz;
     if (bytes > pl->mT_bytes) {
         CK(cudaStreamSynchronize(pl->stream));

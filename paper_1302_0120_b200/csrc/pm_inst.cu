@@ -42,6 +42,7 @@ KernelSet PM_CAT3(make_set_, PM_TAG, PM_LG)() {
     s.solve_raar_tma = nullptr;
     s.solve_smem_tma = 0;
     s.solve_smem_raar_tma = 0;
+    s.solve_tma_m = 0;
     s.solve_smem = 0;
     s.solve_smem_raar = 0;
     s.solve_threads = 0;
@@ -55,6 +56,7 @@ KernelSet PM_CAT3(make_set_, PM_TAG, PM_LG)() {
             s.solve_raar_tma = (const void*)&solve_kernel<PM_T, PM_LG, PM_LGR_ROW, PM_LGR_COL, 1, true>;
             s.solve_smem_tma = LT::BYTES_ALL + 128;
             s.solve_smem_raar_tma = LT::BYTES_ALL_RAAR + 128;
+            s.solve_tma_m = LT::TMA_M ? 1 : 0;
         }
         s.solve_smem = SolveSmem<PM_T, PM_LG, PM_LGR_ROW, PM_LGR_COL>::BYTES_ALL + 128;
         s.solve_smem_raar = SolveSmem<PM_T, PM_LG, PM_LGR_ROW, PM_LGR_COL>::BYTES_ALL_RAAR + 128;

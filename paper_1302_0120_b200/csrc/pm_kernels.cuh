@@ -702,7 +702,7 @@ __device__ __forceinline__ void final_task(const FinalArgs<T>& a, int b, int row
 template <typename T>
 struct TmaTask {
     const cx<T>* ft;              // [n_y][C] input
-    const T* mt;                  // [n_y][MC] m
+    const T* mt;                  // [n_y][MC] m (null: m staged by cp.async, TMA_F)
     unsigned long long* bars;     // [0] input, [1] m
     unsigned parity;
     int MC;
@@ -761,7 +761,8 @@ __device__ __forceinline__ void col_task(const ColArgs<T>& a, int b, int col0, i
         }
         return;
     }
-    if constexpr (PS && !TM) {
+    if constexpr (PS) {
+      if (!TM || !tma.mt) {
         // CC: the persistent kernel's compile-time column count (division-free copy loop)
         static_assert(CC > 0, "staged m needs the compile-time column count");
         if (a.mT)     // transposed m: the task's CC columns are one contiguous run
@@ -770,6 +771,7 @@ __device__ __forceinline__ void col_task(const ColArgs<T>& a, int b, int col0, i
         else
             stage_tile<T, (1 << LG_L), CC, CC * F::TG>(ms, a.m + b * a.m_stride + col0, nx, threadIdx.x);
         cp_async_commit();
+      }
     }
     prefetch();
     cp_async_commit();
@@ -795,7 +797,7 @@ __device__ __forceinline__ void col_task(const ColArgs<T>& a, int b, int col0, i
         }
         const T thr = T(scaled ? a.thr_m[b] : a.thr_ms[b]);
         T mm[F::R];
-        if constexpr (TM) {
+        if (TM && tma.mt) {
             mbar_wait(&tma.bars[1], tma.parity);
 #pragma unroll
             for (int k = 0; k < F::R; ++k) mm[k] = tma.mt[(j + F::TG * k) * tma.MC + c];
@@ -1130,7 +1132,14 @@ struct SolveSmem {
     // loads then spill at 2048^2 / 4096^2, so only A is enabled)
     static constexpr bool TMA_B = false && WANT && !TMA_A && EX + ST + TMAB <= LIMIT;
     static constexpr bool TMA_C = false && WANT && !TMA_A && !TMA_B && EX + TMAB <= LIMIT;
-    static constexpr bool TMA = TMA_A || TMA_B || TMA_C;
+    // F: the column tile only, when the m tile does not fit as well (2048^2,
+    // 4096^2); m is then staged by cp.async from its transposed copy
+#ifndef PM_TMA_F
+#define PM_TMA_F 1
+#endif
+    static constexpr bool TMA_F = PM_TMA_F && WANT && !TMA_A && BASE0 + FTB + 16 + 128 <= LIMIT;
+    static constexpr bool TMA = TMA_A || TMA_B || TMA_C || TMA_F;
+    static constexpr bool TMA_M = TMA && !TMA_F;                 // m streamed by TMA too
     static constexpr bool TS = (TMA_B || TMA_C) ? false : TS0;
     static constexpr bool PS = (TMA_B || TMA_C) ? true : PS0;
     static constexpr int OFF_ST = EX;
@@ -1140,7 +1149,7 @@ struct SolveSmem {
     static constexpr int up128(int x) { return (x + 127) / 128 * 128; }
     static constexpr int OFF_FT = TMA_C ? EX : up128(BYTES);
     static constexpr int OFF_MT = OFF_FT + FTB;
-    static constexpr int OFF_BAR = OFF_MT + MTB;
+    static constexpr int OFF_BAR = OFF_MT + (TMA_M ? MTB : 0);
     static constexpr int TMA_END = TMA ? OFF_BAR + 16 : 0;
     static constexpr int BYTES_T = TMA_END > BYTES ? TMA_END : BYTES;
     static constexpr bool XS = PS && BYTES_T + XSB <= LIMIT;
@@ -1306,15 +1315,15 @@ __device__ __forceinline__ void col_phase(const ColArgs<T>& a, int batch, unsign
             };
             if (threadIdx.x == 0 && (int)blockIdx.x < total) {
                 issue_f(blockIdx.x);
-                issue_m(blockIdx.x);
+                if constexpr (L::TMA_M) issue_m(blockIdx.x);
             }
             for (int t = blockIdx.x; t < total; t += gridDim.x) {
                 const int b = t / tpm, tt = t - b * tpm;
                 const bool act = mask_live(a.st + b);
                 const int tn = t + gridDim.x;
                 auto next_f = [&]() { if (tn < total) issue_f(tn); };
-                auto next_m = [&]() { if (tn < total) issue_m(tn); };
-                TmaTask<T> tk{ft, mt + ((tt * C) & (MA - 1)), bars, *ct.count & 1u, L::MC};
+                auto next_m = [&]() { if (L::TMA_M && tn < total) issue_m(tn); };
+                TmaTask<T> tk{ft, L::TMA_M ? mt + ((tt * C) & (MA - 1)) : nullptr, bars, *ct.count & 1u, L::MC};
                 double acc[3];
                 col_task<T, LG, LGR_C, NX, L::TS, L::PS, L::C, NoPrefetch, true, decltype(next_f), decltype(next_m)>(
                     a, b, tt * C, C, smem, tw.cf, ms, act, acc, nullptr, NoPrefetch{}, tk, next_f, next_m);

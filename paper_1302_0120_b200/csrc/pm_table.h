@@ -30,6 +30,7 @@ struct KernelSet {
     const void* solve_raar_tma;
     int solve_smem_tma;
     int solve_smem_raar_tma;
+    int solve_tma_m;        // the TMA variant streams m too (else it stages m by cp.async)
     int solve_threads;      // its CTA size
     AxisShape row, col;
 };
