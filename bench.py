@@ -169,6 +169,33 @@ def run_reference(args, world, rank):
     print(json.dumps(line), flush=True)
 
 
+def paper_config(device: int) -> dict:
+    """Context, not the bench metric: the paper's own benchmark (PAPER:409,
+    416-417), 25 GS iterations on an 800x600 SLM in fp32 (mixed-radix path),
+    end to end through solve_stack with pinned buffers, median of 10."""
+    import torch
+
+    import paper_1302_0120_b200 as pm
+    from paper_1302_0120_b200.batch import solve_stack
+    from paper_1302_0120_b200.patterns import make_problem
+    p, m = make_problem(800, 50, 7, n_y=600)
+    cfg = pm.SolveConfig(max_iters=25, precision=pm.SINGLE, record_every=25, device=device)
+    pp = torch.from_numpy(p.astype(np.float32)).pin_memory().numpy()
+    mm = torch.from_numpy(m[None].astype(np.float32)).pin_memory().numpy()
+    out = torch.empty((1, 600, 800), dtype=torch.float64).pin_memory().numpy()
+    e2e, dev = [], []
+    for i in range(13):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r = solve_stack(pp, mm, cfg, device=device, out_phases=out)
+        if i >= 3:
+            e2e.append((time.perf_counter() - t0) * 1e3)
+            dev.append(r.device_ms)
+    return {"workload": "gs_800x600_fp32_25iter_50spots (mixed radix)", "device_ms": float(np.median(dev)),
+            "e2e_ms": float(np.median(e2e)), "paper_ms": 45.0,
+            "paper_hw": "Tesla C2070, incl. ~1 ms target upload (PAPER:416-417)"}
+
+
 def flush_l2(buf):
     buf.fill_(1.0)      # 256 MiB write > the 126 MB L2
 
@@ -353,6 +380,8 @@ def main():
             "clocks": clocks.summary(),
             "gpu_launches": launches,
         }
+        if world == 1:
+            line["paper_config"] = paper_config(local)
         if not args.no_cpu_baseline and world == 1:
             line["cpu_baseline"] = cpu_baseline()
         print(json.dumps(line), flush=True)
