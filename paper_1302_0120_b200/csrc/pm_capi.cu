@@ -901,6 +901,14 @@ int launch_solve(pm_plan* pl, int do_init, int it_begin, int it_end, int do_fina
     }
     const bool raar = pl->s.prm.algorithm == PM_ALGO_RAAR;
     const bool use_tma = a.tma && tma_wanted(pl);
+    {   // p and m resident in shared memory when every CTA has one row and one column task
+        static const bool off = getenv("PM_NO_RES") != nullptr;
+        const long long grid = pl->solve_grid, nx = pl->nx;
+        const int G = std::max(1, k.solve_threads / std::max(1, k.row.TG));
+        const long long rows_per_cta = ((long long)pl->s.batch * nx + grid - 1) / std::max(1LL, grid);
+        const long long col_tasks = (long long)pl->s.batch * (nx / solve_cols(pl));
+        a.res = (!off && !use_tma && rows_per_cta <= G && col_tasks <= grid) ? 1 : 0;
+    }
     a.tma = use_tma ? 1 : 0;
     const void* fn = use_tma ? (raar ? k.solve_raar_tma : k.solve_tma) : (raar ? k.solve_raar : k.solve);
     void* args[] = {&a};

@@ -523,7 +523,7 @@ template <typename T, int LG_L, int LG_R, class Sync, int ALG = -1, bool TS = fa
 __device__ __forceinline__ void row_task(const RowArgs<T>& a, int b, int row, int j, cx<T>* sm,
                                          const twe<T>* tw, T* ps, bool inb_arg, bool live, Sync sync,
                                          const cx<T>* tile = nullptr, Prefetch prefetch = Prefetch{},
-                                         cx<T>* xs = nullptr) {
+                                         cx<T>* xs = nullptr, bool stage_p = true) {
     using F = FftShape<LG_L, LG_R>;
     const size_t N = (size_t)a.nx * a.ny;
     // whole-warp groups never run out of bounds (the row phase skips them)
@@ -543,7 +543,7 @@ __device__ __forceinline__ void row_task(const RowArgs<T>& a, int b, int row, in
         for (int k = 0; k < F::R; ++k) v[k] = inb ? ld_field(f + F::TG * k) : mk<T>(T(0), T(0));   // conj(z')
     }
     if constexpr (PS) {
-        if (inb && a.mode != kRowInit) stage_tile<T, 1, (1 << LG_L), F::TG>(ps, p - j, 0, j);
+        if (inb && a.mode != kRowInit && stage_p) stage_tile<T, 1, (1 << LG_L), F::TG>(ps, p - j, 0, j);
         if constexpr (XS) {
             if (inb && (a.mode == kRowRaar || a.mode == kRowProbe))
                 stage_tile<cx<T>, 1, (1 << LG_L), F::TG>(xs, a.x + b * N + (size_t)row * a.nx, 0, j);
@@ -714,7 +714,7 @@ __device__ __forceinline__ void col_task(const ColArgs<T>& a, int b, int col0, i
                                          const twe<T>* tw, T* ms, bool live, double (&acc)[3],
                                          const cx<T>* tile = nullptr, Prefetch prefetch = Prefetch{},
                                          TmaTask<T> tma = TmaTask<T>{}, NextF next_f = NextF{},
-                                         NextM next_m = NextM{}) {
+                                         NextM next_m = NextM{}, bool stage_m = true) {
     using F = FftShape<LG_L, LG_R>;
     const int c = threadIdx.x % C, j = threadIdx.x / C;
     const size_t nx = NX > 0 ? (size_t)NX : (size_t)a.nx;
@@ -765,7 +765,9 @@ __device__ __forceinline__ void col_task(const ColArgs<T>& a, int b, int col0, i
       if (!TM || !tma.mt) {
         // CC: the persistent kernel's compile-time column count (division-free copy loop)
         static_assert(CC > 0, "staged m needs the compile-time column count");
-        if (a.mT)     // transposed m: the task's CC columns are one contiguous run
+        if (!stage_m) {
+            // resident: loaded by this CTA's first column phase of the launch
+        } else if (a.mT)     // transposed m: the task's CC columns are one contiguous run
             stage_tile_s<T, CC, (1 << LG_L), MtStride<T, (1 << LG_L), CC>::V, CC * F::TG>(
                 ms, a.mT + b * a.m_stride + (size_t)col0 * (1 << LG_L), (size_t)(1 << LG_L), threadIdx.x);
         else
@@ -1049,6 +1051,7 @@ struct SolveArgs {
     int init_mode;             // column init from real m (0) or complex field (1)
     int do_probe;              // RAAR: end with the gap / decision of the last iterate
     unsigned long long* stamps; // optional: globaltimer at every phase boundary (CTA 0)
+    int res;                   // p and m may stay resident (one row and one column task per CTA)
     int tma;                   // the column phase's TMA maps below are valid
     CUtensorMap tm_in;         // column input w' ([batch][n_y][2 n_x] floats or doubles)
     CUtensorMap tm_m;          // m ([batch][n_y][n_x])
@@ -1154,8 +1157,17 @@ struct SolveSmem {
     static constexpr int BYTES_T = TMA_END > BYTES ? TMA_END : BYTES;
     static constexpr bool XS = PS && BYTES_T + XSB <= LIMIT;
     static constexpr int OFF_XS = BYTES_T;
-    static constexpr int BYTES_ALL = BYTES_T;
-    static constexpr int BYTES_ALL_RAAR = BYTES_T + (XS ? XSB : 0);
+    // Resident p and m (plain build, one row task and one column task per
+    // CTA: a single mask): the CTA's p rows and m columns stay in shared
+    // memory for the whole launch instead of being staged every phase.
+#ifndef PM_RES
+#define PM_RES 1
+#endif
+    static constexpr int XSE = XS ? XSB : 0;
+    static constexpr bool RES_GS = PM_RES && PS && !TV && BYTES_T + 2 * ST <= LIMIT;
+    static constexpr bool RES_RAAR = PM_RES && PS && !TV && BYTES_T + XSE + 2 * ST <= LIMIT;
+    static constexpr int BYTES_ALL = BYTES_T + (RES_GS ? 2 * ST : 0);
+    static constexpr int BYTES_ALL_RAAR = BYTES_T + XSE + (RES_RAAR ? 2 * ST : 0);
     static constexpr int CB = C * (int)sizeof(T);                 // bytes per m run of a column task
     static constexpr int CH = CB >= 16 ? 16 : CB;                 // cp.async size for it
 };
@@ -1198,15 +1210,25 @@ __device__ __forceinline__ void row_share(int total, int& start, int& count) {
 // time. The field loads of a task are issued before its mask state is known,
 // so the state's L2 round trip overlaps them. Groups of whole warps with no
 // row left skip the round (their barriers are their own).
+// Launch-long residency of p and m (SolveSmem::RES_*): region offsets and
+// whether this CTA has loaded them yet.
+struct Resident {
+    bool on;
+    bool p_ok, m_ok;
+    int off_p, off_m;
+};
+
 template <typename T, int LG, int LGR_R, int LGR_C, int ALG, bool TV = false>
 __device__ __forceinline__ void row_phase(const RowArgs<T>& a, int batch, unsigned char* smraw,
-                                          const Tables<T>& tw) {
+                                          const Tables<T>& tw, Resident* rs = nullptr) {
     using L = SolveSmem<T, LG, LGR_R, LGR_C, TV>;
     using F = FftShape<LG, LGR_R>;
     cx<T>* smem = reinterpret_cast<cx<T>*>(smraw);
     const int G = blockDim.x / F::TG;
     const int g = threadIdx.x / F::TG, j = threadIdx.x % F::TG;
-    T* ps = reinterpret_cast<T*>(smraw + L::OFF_ST) + ((size_t)g << LG);
+    const bool res = rs && rs->on;
+    T* ps = reinterpret_cast<T*>(smraw + (res ? rs->off_p : L::OFF_ST)) + ((size_t)g << LG);
+    const bool stage_p = !(res && rs->p_ok);
     cx<T>* tile = reinterpret_cast<cx<T>*>(smraw + L::OFF_TILE) + ((size_t)g << LG);
     constexpr int NX = 1 << LG;
     int start, count;
@@ -1229,8 +1251,9 @@ __device__ __forceinline__ void row_phase(const RowArgs<T>& a, int batch, unsign
         row_task<T, LG, LGR_R, decltype(group_sync<F::TG>(g)), ALG, L::TS, L::PS, decltype(prefetch), XS>(
             a, b, r & (NX - 1), j, smem + g * F::SM, tw.rf, ps, inb, live, group_sync<F::TG>(g),
             (pf && r0 > 0) ? tile : nullptr, prefetch,
-            XS ? reinterpret_cast<cx<T>*>(smraw + L::OFF_XS) + ((size_t)g << LG) : nullptr);
+            XS ? reinterpret_cast<cx<T>*>(smraw + L::OFF_XS) + ((size_t)g << LG) : nullptr, stage_p);
     }
+    if (res && a.mode != kRowInit) rs->p_ok = true;
 }
 
 template <typename T, int LG, int LGR_R, int LGR_C, bool TV = false>
@@ -1267,11 +1290,14 @@ struct ColTma {
 
 template <typename T, int LG, int LGR_R, int LGR_C, bool TV = false>
 __device__ __forceinline__ void col_phase(const ColArgs<T>& a, int batch, unsigned char* smraw,
-                                          const Tables<T>& tw, ColTma ct = ColTma{nullptr, nullptr, nullptr}) {
+                                          const Tables<T>& tw, ColTma ct = ColTma{nullptr, nullptr, nullptr},
+                                          Resident* rs = nullptr) {
     using L = SolveSmem<T, LG, LGR_R, LGR_C, TV>;
     using F = FftShape<LG, LGR_C>;
     cx<T>* smem = reinterpret_cast<cx<T>*>(smraw);
-    T* ms = reinterpret_cast<T*>(smraw + L::OFF_ST);
+    const bool res = rs && rs->on && a.mode == 2;
+    T* ms = reinterpret_cast<T*>(smraw + (res ? rs->off_m : L::OFF_ST));
+    const bool stage_m = !(res && rs->m_ok);
     cx<T>* tile = reinterpret_cast<cx<T>*>(smraw + L::OFF_TILE);
     constexpr int NX = 1 << LG;
     const int C = blockDim.x / F::TG;
@@ -1352,7 +1378,8 @@ __device__ __forceinline__ void col_phase(const ColArgs<T>& a, int batch, unsign
         };
         double acc[3];
         col_task<T, LG, LGR_C, NX, L::TS, L::PS, L::C>(a, b, tt * C, C, smem, tw.cf, ms, act, acc,
-                                                        (pf && t != (int)blockIdx.x) ? tile : nullptr, prefetch);
+                                                        (pf && t != (int)blockIdx.x) ? tile : nullptr, prefetch,
+                                                        TmaTask<T>{}, NoPrefetch{}, NoPrefetch{}, stage_m);
         if (metr && act) {
             double tot[3];
             block_reduce<3>(acc, tot);
@@ -1362,6 +1389,7 @@ __device__ __forceinline__ void col_phase(const ColArgs<T>& a, int batch, unsign
             }
         }
     }
+    if (res) rs->m_ok = true;
 }
 
 // Per-mask reduction of the column phase's task partials and the stop
@@ -1422,6 +1450,8 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const __grid_co
     unsigned epoch = 0;
     stamp(a.stamps, si);
     const Tables<T> tw = load_tables<T, LG, LGR_R, LGR_C, TV>(a.row, a.col, smraw);
+    Resident rs{a.res != 0 && (ALG == 1 ? L::RES_RAAR : L::RES_GS), false, false,
+                L::BYTES_T + (ALG == 1 ? L::XSE : 0), L::BYTES_T + (ALG == 1 ? L::XSE : 0) + L::ST};
     unsigned tma_count = 0;
     ColTma ct{nullptr, nullptr, &tma_count};
     if constexpr (L::TMA) {
@@ -1445,10 +1475,10 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const __grid_co
         grid_sync(a.bar, epoch);
         RowArgs<T> r = a.row;
         r.mode = kRowInit;
-        row_phase<T, LG, LGR_R, LGR_C, ALG, TV>(r, B, smraw, tw);     // u0 row half, w0 (RAAR: and x_0)
+        row_phase<T, LG, LGR_R, LGR_C, ALG, TV>(r, B, smraw, tw, &rs);     // u0 row half, w0 (RAAR: and x_0)
         grid_sync(a.bar, epoch);
         c.mode = 2;
-        col_phase<T, LG, LGR_R, LGR_C, TV>(c, B, smraw, tw, ct);      // z1
+        col_phase<T, LG, LGR_R, LGR_C, TV>(c, B, smraw, tw, ct, &rs);      // z1
         grid_sync(a.bar, epoch);
     }
     const bool early = a.col.ctl.early_tol >= 0.0;
@@ -1458,21 +1488,21 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const __grid_co
             RowArgs<T> r = a.row;
             r.mode = kRowRaar;
             r.it = it;
-            row_phase<T, LG, LGR_R, LGR_C, ALG, TV>(r, B, smraw, tw);   // gap of x_{it-1}, x_it, w_it
+            row_phase<T, LG, LGR_R, LGR_C, ALG, TV>(r, B, smraw, tw, &rs);   // gap of x_{it-1}, x_it, w_it
             grid_sync(a.bar, epoch);
             decide_phase_raar<T>(r, B, it - 1);
             if (early) grid_sync(a.bar, epoch);
             ColArgs<T> c = a.col;
             c.mode = 2;
             c.u_iter = it;
-            col_phase<T, LG, LGR_R, LGR_C, TV>(c, B, smraw, tw, ct);    // lit/dark of x_it, z_{it+1}
+            col_phase<T, LG, LGR_R, LGR_C, TV>(c, B, smraw, tw, ct, &rs);    // lit/dark of x_it, z_{it+1}
             grid_sync(a.bar, epoch);
         }
         if (a.do_probe) {
             RowArgs<T> r = a.row;
             r.mode = kRowProbe;
             r.it = a.it_end;
-            row_phase<T, LG, LGR_R, LGR_C, ALG, TV>(r, B, smraw, tw);   // gap of x_{it_end-1}
+            row_phase<T, LG, LGR_R, LGR_C, ALG, TV>(r, B, smraw, tw, &rs);   // gap of x_{it_end-1}
             grid_sync(a.bar, epoch);
             decide_phase_raar<T>(r, B, a.it_end - 1);
             grid_sync(a.bar, epoch);
@@ -1487,14 +1517,14 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const __grid_co
             RowArgs<T> r = a.row;
             r.mode = kRowGS;
             r.it = it;
-            row_phase<T, LG, LGR_R, LGR_C, ALG, TV>(r, B, smraw, tw);   // u_it, w_it
+            row_phase<T, LG, LGR_R, LGR_C, ALG, TV>(r, B, smraw, tw, &rs);   // u_it, w_it
             stamp(a.stamps, si);
             grid_sync(a.bar, epoch);
             stamp(a.stamps, si);
             ColArgs<T> c = a.col;
             c.mode = 2;
             c.u_iter = it;
-            col_phase<T, LG, LGR_R, LGR_C, TV>(c, B, smraw, tw, ct);    // metrics of u_it, z_{it+1}
+            col_phase<T, LG, LGR_R, LGR_C, TV>(c, B, smraw, tw, ct, &rs);    // metrics of u_it, z_{it+1}
             stamp(a.stamps, si);
             grid_sync(a.bar, epoch);
             stamp(a.stamps, si);
