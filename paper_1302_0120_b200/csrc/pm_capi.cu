@@ -533,6 +533,7 @@ struct pm_plan {
     // current solve session
     struct Session {
         bool active = false;
+        bool stepping = false;        // pm_solve_begin/step/finish (vs one enqueued solve)
         int batch = 0, it = 0;
         pm_params prm{};
         const void* p = nullptr;
@@ -1222,7 +1223,7 @@ int gen_row_sweep(pm_plan* pl, int it) {
     CK(cudaLaunchKernelEx(pdl_config(grid, pl->gnt_r, pl->gsm_r, pl->stream).get(), gen_row_sweep_kernel<T>,
                           (cx<T>*)pl->tmp, (cx<T>*)pl->field, (const T*)pl->s.p, (long long)pl->s.p_stride,
                           (const double*)pl->thrx, (const cx<T>*)pl->gtwx, pl->gx, pl->ny, lg_of(TC), pl->st,
-                          (long long)pl->N, it));
+                          (long long)pl->N, it, pl->s.stepping ? 1 : 0));
     pl->launches++;
     return PM_OK;
 }
@@ -1337,8 +1338,17 @@ int gen_finish(pm_plan* pl) {
         pl->launches++;
         u_iter = 0;                        // every decision is taken
     }
-    CKR(gen_rows_fwd(pl, 1));              // every mask from its last iterate (stopped ones included)
-    CKR(f32 ? gen_col_sweep<float>(pl, u_iter, 0, 1) : gen_col_sweep<double>(pl, u_iter, 0, 1));
+    if (pl->s.prm.algorithm != PM_ALGO_RAAR && !pl->s.stepping) {
+        // GS in one enqueued solve: the work buffer of a mask that stopped at
+        // u_j already holds ColIFFT(replace_m(ColFFT(RowFFT u_j))), the row
+        // pre-image of v* = P_M u_j (its row sweeps were skipped); the rest
+        // hold RowFFT(u_K) and get that column sweep now (with u_K's decision).
+        // The iterate itself is never stored.
+        CKR(f32 ? gen_col_sweep<float>(pl, u_iter, 0, 0) : gen_col_sweep<double>(pl, u_iter, 0, 0));
+    } else {
+        CKR(gen_rows_fwd(pl, 1));          // every mask from its last iterate (stopped ones included)
+        CKR(f32 ? gen_col_sweep<float>(pl, u_iter, 0, 1) : gen_col_sweep<double>(pl, u_iter, 0, 1));
+    }
     CKR(f32 ? gen_axis<float>(pl, pl->tmp, pl->tmp, 0, PM_INVERSE, pl->s.batch, pl->st, 1)
             : gen_axis<double>(pl, pl->tmp, pl->tmp, 0, PM_INVERSE, pl->s.batch, pl->st, 1));
     return f32 ? gen_final_t<float>(pl) : gen_final_t<double>(pl);
@@ -2341,6 +2351,7 @@ int pm_solve_begin(pm_plan* pl, const void* p, const void* m, const void* m_init
                        pl->stream));
     CK(cudaMemcpyAsync(pl->mbuf, m, batch * N * pl->rsz, cudaMemcpyHostToDevice, pl->stream));
     CKR(session_setup(pl, pl->pbuf, pl->mbuf, batch, prm, tol_p, tol_m, energy));
+    pl->s.stepping = true;
     CKR(stage_start(pl, m_init, cudaMemcpyHostToDevice));
     CK(cudaEventRecord(pl->ev0, pl->stream));
     CKR(enqueue_begin(pl));

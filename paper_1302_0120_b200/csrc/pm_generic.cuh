@@ -472,7 +472,7 @@ __global__ void gen_col_sweep_kernel(cx<T>* w, const T* m, const double* thr_m, 
 template <typename T>
 __global__ void gen_row_sweep_kernel(cx<T>* w, cx<T>* u, const T* p, long long p_stride, const double* thr_p,
                                      const cx<T>* __restrict__ tw, GenPlan gp, int ny, int lgTC, MaskState* st,
-                                     long long n, int it) {
+                                     long long n, int it, int store_u) {
     extern __shared__ __align__(16) unsigned char smraw[];
     const int TC = 1 << lgTC, L = gp.L;
     GenSmem<T> sm(smraw, L, TC);
@@ -506,7 +506,7 @@ __global__ void gen_row_sweep_kernel(cx<T>* w, cx<T>* u, const T* p, long long p
     }
     if (!isfinite(chk)) first_bad(&st[b].bad, it);
     __syncthreads();
-    gen_scatter<T>(A, ub, L, lgTC, t0, tc, L, 1, T(1));     // the iterate, coalesced along the row
+    if (store_u) gen_scatter<T>(A, ub, L, lgTC, t0, tc, L, 1, T(1));   // the iterate (stepping sessions)
     A = gen_passes<T>(A, B, sm.tw, gp, lgTC, -1);
     gen_scatter<T>(A, wb, L, lgTC, t0, tc, L, 1, sc);
 }
