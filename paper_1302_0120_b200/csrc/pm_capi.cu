@@ -1208,9 +1208,9 @@ int gen_col_sweep(pm_plan* pl, int u_iter, int metrics_only, int all_masks) {
     GenSolveArgs g = gen_args(pl);
     g.nblk = (int)grid.x;
     CK(cudaLaunchKernelEx(pdl_config(grid, pl->gnt_c, pl->gsm_c, pl->stream).get(), gen_col_sweep_kernel<T>,
-                          (cx<T>*)pl->tmp, (const T*)pl->s.m, (const double*)pl->thrm, (const double*)pl->escale,
-                          (const cx<T>*)pl->gtwy, pl->gy, pl->nx, lg_of(TC), g, u_iter, metrics_only, all_masks,
-                          pl->s.prm.algorithm == PM_ALGO_RAAR ? 1 : 0));
+                          (cx<T>*)pl->tmp, (const T*)pl->s.m, (const T*)pl->s.mT, (const double*)pl->thrm,
+                          (const double*)pl->escale, (const cx<T>*)pl->gtwy, pl->gy, pl->nx, lg_of(TC), g, u_iter,
+                          metrics_only, all_masks, pl->s.prm.algorithm == PM_ALGO_RAAR ? 1 : 0));
     pl->launches++;
     return PM_OK;
 }
@@ -1228,6 +1228,9 @@ int gen_row_sweep(pm_plan* pl, int it) {
     return PM_OK;
 }
 
+int ensure_mT(pm_plan* pl);
+int launch_transpose_m(pm_plan* pl);
+
 int gen_begin(pm_plan* pl) {
     auto& s = pl->s;
     const long long total = (long long)s.batch * pl->N;
@@ -1242,12 +1245,13 @@ int gen_begin(pm_plan* pl) {
         pl->launches++;
     }
     CKR(gen_fft2(pl, pl->field, pl->field, PM_INVERSE, s.batch, pl->st, 0));   // u0 = F^-1(m e^{i phi})
+    // m transposed per mask, so a column task's m is TC contiguous runs (buffer
+    // sized in session_setup, outside any capture)
+    s.mT = nullptr;
+    if (pl->mT_bytes >= (size_t)s.batch * pl->N * pl->rsz) CKR(launch_transpose_m(pl));
     return gen_rows_fwd(pl, 0);                                                  // w = RowFFT(u0)
 }
 
-// Two fused sweeps per iteration over the work buffer, which holds
-// RowFFT(u_{it-1}) on entry and RowFFT(u_it) on exit; the iterate itself is
-// kept in `field` so a mask that stops keeps its last iterate.
 // RAAR row sweep of iteration `it` (x_{it-1} from the buffer of its parity,
 // x_it into the other; upd = 0: gap + decision of x_{it-1} only).
 template <typename T>
@@ -1282,6 +1286,8 @@ int gen_raar_probe(pm_plan* pl, bool restore) {
                : gen_axis<double>(pl, x, pl->tmp, 0, PM_FORWARD, pl->s.batch, pl->st, 0);
 }
 
+// Two fused sweeps per iteration over the work buffer, which holds
+// RowFFT(u_{it-1}) on entry and RowFFT(u_it) on exit.
 int gen_steps(pm_plan* pl, int n, bool probe) {
     auto& s = pl->s;
     const bool f32 = pl->prec == PM_SINGLE;
@@ -1437,6 +1443,10 @@ int session_setup(pm_plan* pl, const void* d_p, const void* d_m, int batch, cons
     CKR(validate_params(prm, batch));
     CKR(ensure_capacity(pl, batch, prm->max_iters));
     if (prm->algorithm == PM_ALGO_RAAR) CKR(ensure_raar(pl));
+    if (pl->generic && getenv("PM_NO_MT") == nullptr) {
+        pl->s.batch = batch;                // ensure_mT sizes for this batch
+        CKR(ensure_mT(pl));
+    }
     auto& s = pl->s;
     s = pm_plan::Session();
     s.active = true;
@@ -1552,21 +1562,23 @@ bool persistent(const pm_plan* pl) {
 // slightly worse where the runs are already >= 32 bytes (1024^2 fp32, fp64),
 // so only below that. Not when the TMA variant streams m boxes itself (its
 // field-only form, 2048^2 / 4096^2, stages m from this copy).
-int enqueue_mT(pm_plan* pl) {
-    static const bool off = getenv("PM_NO_MT") != nullptr;
+// The transposed-m buffer for the session's batch (outside any capture;
+// captured graphs hold the old pointer, so they go when it is reallocated).
+int ensure_mT(pm_plan* pl) {
+    const size_t bytes = (size_t)pl->s.batch * pl->N * pl->rsz;
+    if (bytes <= pl->mT_bytes) return PM_OK;
+    CK(cudaStreamSynchronize(pl->stream));
+    drop_graphs(pl);
+    if (pl->mT) cudaFree(pl->mT);
+    pl->mT = nullptr;
+    pl->mT_bytes = 0;
+    CK(cudaMalloc(&pl->mT, bytes));
+    pl->mT_bytes = bytes;
+    return PM_OK;
+}
+
+int launch_transpose_m(pm_plan* pl) {
     auto& s = pl->s;
-    s.mT = nullptr;
-    const bool tma_streams_m = tma_wanted(pl) && kset(pl->prec, pl->lgx).solve_tma_m;
-    if (off || !persistent(pl) || tma_streams_m || (size_t)solve_cols(pl) * pl->rsz >= 32) return PM_OK;
-    const size_t bytes = (size_t)s.batch * pl->N * pl->rsz;
-    if (bytes > pl->mT_bytes) {
-        CK(cudaStreamSynchronize(pl->stream));
-        if (pl->mT) cudaFree(pl->mT);
-        pl->mT = nullptr;
-        pl->mT_bytes = 0;
-        CK(cudaMalloc(&pl->mT, bytes));
-        pl->mT_bytes = bytes;
-    }
     const dim3 grid((pl->nx + 31) / 32, (pl->ny + 31) / 32, s.batch), block(32, 8);
     if (pl->prec == PM_SINGLE)
         transpose_kernel<float><<<grid, block, 0, pl->stream>>>((const float*)s.m, (float*)pl->mT, pl->nx, pl->ny);
@@ -1577,6 +1589,15 @@ int enqueue_mT(pm_plan* pl) {
     pl->launches++;
     s.mT = pl->mT;
     return PM_OK;
+}
+
+int enqueue_mT(pm_plan* pl) {
+    static const bool off = getenv("PM_NO_MT") != nullptr;
+    pl->s.mT = nullptr;
+    const bool tma_streams_m = tma_wanted(pl) && kset(pl->prec, pl->lgx).solve_tma_m;
+    if (off || !persistent(pl) || tma_streams_m || (size_t)solve_cols(pl) * pl->rsz >= 32) return PM_OK;
+    CKR(ensure_mT(pl));
+    return launch_transpose_m(pl);
 }
 
 int enqueue_begin(pm_plan* pl) {

@@ -396,7 +396,7 @@ struct GenSolveArgs {
 // metrics and decision of u_{u_iter}) -> ColIFFT on the work buffer `w`
 // (rows already transformed), in place; metrics_only leaves `w` untouched.
 template <typename T>
-__global__ void gen_col_sweep_kernel(cx<T>* w, const T* m, const double* thr_m, const double* escale,
+__global__ void gen_col_sweep_kernel(cx<T>* w, const T* m, const T* mT, const double* thr_m, const double* escale,
                                      const cx<T>* __restrict__ tw, GenPlan gp, int nx, int lgTC, GenSolveArgs g,
                                      int u_iter, int metrics_only, int all_masks, int raar) {
     extern __shared__ __align__(16) unsigned char smraw[];
@@ -417,7 +417,11 @@ __global__ void gen_col_sweep_kernel(cx<T>* w, const T* m, const double* thr_m, 
     cx<T>* wb = w + b * g.n;
     gen_gather<cx<T>>(sm.A, wb, L, lgTC, t0, tc, 1, nx, mk<T>(T(0), T(0)));
     cp_async_commit();
-    gen_gather<T>(sm.g, m + b * g.n, L, lgTC, t0, tc, 1, nx, T(0));    // m, in flight during the passes
+    if (mT)   // m transposed per mask: each of the TC columns is one contiguous run
+        gen_gather<T>(sm.g, mT + b * g.n, L, lgTC, t0, tc, L, 1, T(0));
+    else
+        gen_gather<T>(sm.g, m + b * g.n, L, lgTC, t0, tc, 1, nx, T(0));
+    // (m stays in flight during the passes)
     cp_async_commit();
     cp_async_wait<1>();
     __syncthreads();
