@@ -278,3 +278,16 @@ def test_reconstruction_intensity_and_log_image(prec, shape):
     np.testing.assert_allclose(raw * (E / raw.sum()), got, rtol=1e-12 if prec is pm.DOUBLE else 1e-6)
     with pytest.raises(ValueError, match="reconstruction carries no energy"):
         reconstructed_intensity(pm.Field(spec, np.zeros(shape, prec.complex_dtype)), prov, E)
+
+
+def test_reconstruction_image_batch_matches_single():
+    spec = pm.GridSpec(48, 32)
+    plan = pm.transform.get_plan(spec, pm.DOUBLE)
+    rng = np.random.default_rng(9)
+    u = rng.standard_normal((3, 32, 48)) + 1j * rng.standard_normal((3, 32, 48))
+    E = np.array([1.0, 2.0, 3.0])
+    inten, img = plan.recon_image(u, E, 1e-6)
+    for b in range(3):
+        i1, g1 = plan.recon_image(u[b], E[b], 1e-6)
+        np.testing.assert_array_equal(inten[b], i1)
+        np.testing.assert_array_equal(img[b], g1)

@@ -413,3 +413,18 @@ def test_solve_stream_mixed_radix_raar_and_random_start():
             ref = solve_stack(p, m[None], cfg)
             np.testing.assert_array_equal(ph, ref.phases)
             np.testing.assert_array_equal(gap, ref.gap)
+
+
+def test_solve_stream_consumer_may_stop_early():
+    """Breaking out of a solve_stream loop leaves the plan usable (the
+    generator's cleanup waits for the copies in flight)."""
+    from paper_1302_0120_b200.batch import solve_stream
+    p, _ = make_problem(256, 8, 7)
+    ms = [make_problem(256, 8, s)[1] for s in (31, 32, 33, 34)]
+    cfg = pm.SolveConfig(max_iters=6, precision=pm.SINGLE)
+    for i, r in enumerate(solve_stream(((p, m) for m in ms), cfg)):
+        if i == 1:
+            break
+    ref = solve_stack(p.astype(np.float32), ms[2][None].astype(np.float32), cfg)
+    again = next(iter(solve_stream([(p, ms[2])], cfg)))
+    np.testing.assert_array_equal(again.phases, ref.phases)
