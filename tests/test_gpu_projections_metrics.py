@@ -291,3 +291,19 @@ def test_reconstruction_image_batch_matches_single():
         i1, g1 = plan.recon_image(u[b], E[b], 1e-6)
         np.testing.assert_array_equal(inten[b], i1)
         np.testing.assert_array_equal(img[b], g1)
+
+
+# --- norm homogeneity on the device reduction (reference tests/test_grid.py:81-88) ---
+from hypothesis import given, settings, strategies as st  # noqa: E402
+
+
+@given(st.floats(-1e3, 1e3).filter(lambda a: abs(a) > 1e-6))
+@settings(max_examples=25, deadline=None)
+def test_norm2_absolute_homogeneity(alpha):
+    from paper_1302_0120_b200.grid import norm2
+    rng = np.random.default_rng(7)
+    spec = pm.GridSpec(8, 8)
+    data = rng.standard_normal(spec.shape) + 1j * rng.standard_normal(spec.shape)
+    base = norm2(pm.Field(spec, data))
+    scaled = norm2(pm.Field(spec, alpha * data))
+    assert scaled == pytest.approx(abs(alpha) * base, rel=4 * np.finfo(float).eps * 10)

@@ -132,3 +132,19 @@ def test_plan_mismatch_error_is_value_error():
 def test_solve_diverged_error_message():
     e = pm.SolveDivergedError(7)
     assert e.iteration == 7 and "iteration 7" in str(e)
+
+
+# --- property tests of the grid helpers (reference tests/test_grid.py:21-26) ---
+from hypothesis import given, settings, strategies as st  # noqa: E402
+
+
+@given(st.integers(1, 37), st.integers(1, 23))
+@settings(max_examples=60, deadline=None)
+def test_index_round_trip_property(n_x, n_y):
+    spec = pm.GridSpec(n_x, n_y)
+    for x in range(0, spec.n, max(1, spec.n // 17)):
+        j, k = spec.unflatten_index(x)
+        assert spec.flatten_index(j, k) == x
+    a = np.arange(spec.n).reshape(spec.shape)
+    j, k = n_x - 1, n_y - 1
+    assert a[k, j] == spec.flatten_index(j, k)
