@@ -157,6 +157,36 @@ def _params(cfg: SolveConfig, p_per_mask: bool, init_complex: bool) -> _lib.pm_p
     return prm
 
 
+_PINNED_MIN = 1 << 20
+
+
+def _host_empty(shape, dtype) -> np.ndarray:
+    """An output array in page-locked memory when torch's caching host
+    allocator is at hand and the array is large (full-speed device-to-host
+    copies; the block returns to torch's cache when the array is dropped),
+    else a plain numpy array."""
+    n = int(np.prod(shape)) * np.dtype(dtype).itemsize
+    if n >= _PINNED_MIN:
+        try:
+            import torch
+            if torch.cuda.is_available():
+                t = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+                return t.numpy().view(dtype).reshape(shape)
+        except Exception:                       # no torch / no pinned memory: pageable output
+            pass
+    return np.empty(shape, dtype=dtype)
+
+
+def _host_cast(a: np.ndarray, dtype) -> np.ndarray:
+    """`a` as a C-contiguous `dtype` array; when a cast is needed anyway it is
+    written into (large: page-locked) memory from _host_empty."""
+    if a.dtype == np.dtype(dtype) and a.flags.c_contiguous:
+        return a
+    out = _host_empty(a.shape, dtype)
+    np.copyto(out, a, casting="unsafe")
+    return out
+
+
 def _history(it_ms, iters_run, gaps, lits, darks):
     out = []
     for i in range(1, iters_run + 1):
@@ -200,19 +230,20 @@ def solve(c: SlmConstraint, m: FourierConstraint, cfg: SolveConfig,
     prec = cfg.precision
     plan = get_plan(spec, prec, device)
     fdt = prec.float_dtype
-    p_dev = np.ascontiguousarray(c.p.data, dtype=fdt)
-    m_dev = np.ascontiguousarray(m.m.data, dtype=fdt)
-    tol_p = np.array([c.zero_tol])
-    tol_m = np.array([m.zero_tol])
-    energy = np.array([float((m.m.data.astype(np.float64) ** 2).sum())])
+    p_dev = _host_cast(c.p.data, fdt)
+    m_dev = _host_cast(m.m.data, fdt)
+    # the zero tolerances 1024 eps max(.) of the precision-cast p and m
+    # (src/projections.py:41-43) and the target energy sum(m^2) are reduced on
+    # the device from the uploaded arrays, as the batch API does
+    tol_p = tol_m = energy = None
     init = None                      # random-phase starts are drawn on the device
     prm = _params(cfg, False, False)
 
     K = cfg.max_iters
     N = spec.n
-    phases = np.empty(spec.shape, dtype=np.float64)
-    u_star = np.empty(spec.shape, dtype=prec.complex_dtype)
-    v_star = np.empty(spec.shape, dtype=prec.complex_dtype)
+    phases = _host_empty(spec.shape, np.float64)
+    u_star = _host_empty(spec.shape, prec.complex_dtype)
+    v_star = _host_empty(spec.shape, prec.complex_dtype)
     gaps = np.full(K, np.nan)
     lits = np.full(K, np.nan)
     darks = np.full(K, np.nan)
