@@ -29,7 +29,7 @@ import numpy as np
 
 from . import _lib
 from .grid import GridSpec, Precision
-from .solver import SolveConfig, SolveDivergedError, _params
+from .solver import SolveConfig, SolveDivergedError, _host_cast, _host_empty, _params
 from .transform import get_plan
 
 
@@ -101,13 +101,13 @@ def solve_stack(p: np.ndarray, m_stack: np.ndarray, cfg: SolveConfig, device: in
     prec = cfg.precision
     fdt = prec.float_dtype
     plan = get_plan(GridSpec(nx, ny), prec, device)
-    pp = np.ascontiguousarray(p, dtype=fdt)
-    mm = np.ascontiguousarray(m_stack, dtype=fdt)
+    pp = _host_cast(p, fdt)                  # page-locked when a cast is needed anyway
+    mm = _host_cast(m_stack, fdt)
     # the zero tolerances 1024 eps max(.) and the "identically zero" checks
     # (src/solver.py:122-125) run on the device, on the uploaded p and m
     tol_p = tol_m = None
     K = cfg.max_iters
-    phases = out_phases if out_phases is not None else np.empty((B, ny, nx))
+    phases = out_phases if out_phases is not None else _host_empty((B, ny, nx), np.float64)
     if phases.shape != (B, ny, nx) or phases.dtype != np.float64 or not phases.flags.c_contiguous:
         raise ValueError("out_phases must be a C-contiguous float64 (batch, n_y, n_x) array")
     out = BatchResult(phases, np.full((B, K), np.nan), np.full((B, K), np.nan),

@@ -157,16 +157,16 @@ def _params(cfg: SolveConfig, p_per_mask: bool, init_complex: bool) -> _lib.pm_p
     return prm
 
 
-_PINNED_MIN = 1 << 20
+_PINNED_MIN, _PINNED_MAX = 1 << 20, 256 << 20
 
 
 def _host_empty(shape, dtype) -> np.ndarray:
-    """An output array in page-locked memory when torch's caching host
-    allocator is at hand and the array is large (full-speed device-to-host
-    copies; the block returns to torch's cache when the array is dropped),
-    else a plain numpy array."""
+    """An array in page-locked memory when torch's caching host allocator is
+    at hand and the array is between 1 MiB and 256 MiB (full-speed copies; the
+    block returns to torch's cache when the array is dropped), else a plain
+    numpy array."""
     n = int(np.prod(shape)) * np.dtype(dtype).itemsize
-    if n >= _PINNED_MIN:
+    if _PINNED_MIN <= n <= _PINNED_MAX:
         try:
             import torch
             if torch.cuda.is_available():
