@@ -124,11 +124,19 @@ def project_modulus(uhat, m, tag):
     return replace_modulus(uhat, m, zero_tol(tag, m), tag)
 
 
+def _field_ok(a):
+    """Field's construction check (src/grid.py:100-110)."""
+    if not np.isfinite(a).all():
+        raise ValueError("field contains non-finite entries")
+    return a
+
+
 def project_fourier(u, m, tag, workers=1):
-    """P_M = F^-1 . replace_m . F (src/projections.py:86-91)."""
+    """P_M = F^-1 . replace_m . F (src/projections.py:86-91), with the Field
+    checks of every intermediate the reference builds."""
     cdt = DTYPES[tag][1]
-    vhat = project_modulus(fft2(u.astype(cdt, copy=False), workers), m, tag)
-    return ifft2(vhat, workers)
+    vhat = _field_ok(project_modulus(_field_ok(fft2(u.astype(cdt, copy=False), workers)), m, tag))
+    return _field_ok(ifft2(vhat, workers))
 
 
 # ---------------------------------------------------------------- metrics
@@ -141,12 +149,15 @@ def gap(u, p, m, tag, workers=1) -> float:
 def reconstructed_intensity(u, target_energy, tag, workers=1):
     """|F u|^2 rescaled to the target energy (src/metrics.py:74-88)."""
     cdt = DTYPES[tag][1]
-    amps = np.abs(fft2(u.astype(cdt, copy=False), workers)).astype(np.float64)
+    amps = np.abs(_field_ok(fft2(u.astype(cdt, copy=False), workers))).astype(np.float64)
     inten = amps * amps
     total = deterministic_sum(inten)
     if total == 0:
         raise ValueError("reconstruction carries no energy")
-    return inten * (target_energy / total)
+    out = inten * (target_energy / total)
+    if not np.isfinite(out).all():                # RealGrid check (src/grid.py:128-129)
+        raise ValueError("grid contains non-finite entries")
+    return out
 
 
 def physical_error(inten, target_inten, t_lit=T_LIT, t_dark=T_DARK):
@@ -190,6 +201,35 @@ def _finish(u, p, m, tag, workers):
     return v_star, u_star, phases_of(u_star, zero_tol(tag, p))
 
 
+class Diverged(FloatingPointError):
+    """SolveDivergedError of the reference (src/solver.py:27-32,162-165)."""
+
+    def __init__(self, iteration):
+        super().__init__(f"non-finite values at iteration {iteration}")
+        self.iteration = iteration
+
+
+def _finite(a, it):
+    if not np.isfinite(a).all():
+        raise Diverged(it)
+    return a
+
+
+def first_nonfinite_iteration(p, m, max_iters, tag="double", workers=1):
+    """The iteration whose loop body (src/solver.py:152-165) first builds a
+    non-finite Field — the SolveDivergedError iteration with the metrics path
+    left out — or 0. The batch API's per-mask divergence contract."""
+    u = initial_iterate(m, tag, workers)
+    for it in range(1, max_iters + 1):
+        try:
+            uhat = _finite(fft2(u, workers), it)
+            v = _finite(ifft2(_finite(project_modulus(uhat, m, tag), it), workers), it)
+            u = _finite(project_slm(v, p, tag), it)
+        except Diverged as e:
+            return e.iteration
+    return 0
+
+
 def solve(p, m, max_iters, tag="double", record_every=1, early_stop_tol=None,
           algorithm="gs", beta=0.9, workers=1, random_phase_init=False, seed=0,
           should_abort=None, keep_iterates=False):
@@ -211,7 +251,10 @@ def solve(p, m, max_iters, tag="double", record_every=1, early_stop_tol=None,
     prev, iters_run, aborted = None, 0, False
     cdt = DTYPES[tag][1]
     for it in range(1, max_iters + 1):
-        v = ifft2(project_modulus(fft2(u, workers), m, tag), workers)
+        # every Field the reference builds is checked finite (src/grid.py:100-110):
+        # uhat, vhat, v and the new iterate (src/solver.py:152-165)
+        uhat = _finite(fft2(u, workers), it)
+        v = _finite(ifft2(_finite(project_modulus(uhat, m, tag), it), workers), it)
         if algorithm == "gs":
             u = project_slm(v, p, tag)
         elif algorithm == "raar":
@@ -220,8 +263,7 @@ def solve(p, m, max_iters, tag="double", record_every=1, early_stop_tol=None,
                  + (1 - 2 * beta) * v).astype(cdt)
         else:
             raise ValueError(f"unknown algorithm {algorithm!r}")
-        if not np.isfinite(u).all():
-            raise FloatingPointError(f"non-finite values at iteration {it}")
+        _finite(u, it)
         iters_run = it
         if keep_iterates:
             iterates.append(u.copy())

@@ -132,10 +132,20 @@ def solve_stack(p: np.ndarray, m_stack: np.ndarray, cfg: SolveConfig, device: in
         code = plan.lib.pm_solve(plan.handle, _lib.ptr(pp), _lib.ptr(mm), _lib.ptr(init_c), B, prm,
                                  _lib.ptr(tol_p), _lib.ptr(tol_m), None, res)
     if code == _lib.PM_ERR_DIVERGED or div.any():
-        raise SolveDivergedError(int(div[div > 0][0]) if div.any() else 1)
+        raise _diverged(div)
     _lib.check(code, "pm_solve")
     out.device_ms = float(ms[0])
     return out
+
+
+def _diverged(div: np.ndarray) -> SolveDivergedError:
+    """The batch contract: SolveDivergedError of the first mask that diverged,
+    carrying the iteration whose loop body went non-finite
+    (src/solver.py:152-165) and, in ``per_mask``, every mask's (0 = finite)."""
+    bad = div[div > 0]
+    e = SolveDivergedError(int(bad[0]) if bad.size else 1)
+    e.per_mask = div.copy()
+    return e
 
 
 def solve_stream(items, cfg: SolveConfig, device: int = 0, out_phases: list | None = None):
@@ -221,7 +231,7 @@ def solve_stream(items, cfg: SolveConfig, device: int = 0, out_phases: list | No
                                                 _lib.C.c_void_p(d_m[s].data_ptr()), None, 1, prm, None, None,
                                                 None, res)
             if code == _lib.PM_ERR_DIVERGED or div.any():
-                raise SolveDivergedError(int(div[0]) or 1)
+                raise _diverged(div)
             _lib.check(code, "pm_solve_device")
             res_py.device_ms = float(ms[0])
             ev_done[s].record(compute)

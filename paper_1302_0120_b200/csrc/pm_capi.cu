@@ -55,14 +55,34 @@ int cuda_err(cudaError_t e, const char* what) {
 // ------------------------------------------------------- elementwise kernels
 namespace pm {
 
-// src/projections.py:46-66 as a stand-alone per-pixel kernel.
+// src/projections.py:46-66 as a stand-alone per-pixel kernel, through the
+// solve's own register-array projection (project_regs: fast pass, exact
+// re-decision inside the band) four pixels per thread, so the projection
+// KATs exercise the hot path's decision code.
 template <typename T>
-__global__ void replace_kernel(const cx<T>* in, const T* target, long long tstride, T tol,
+__global__ void replace_kernel(const cx<T>* in, const T* target, long long tstride, T tol_,
                                cx<T>* out, long long n) {
     const long long b = blockIdx.y;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-         i += (long long)gridDim.x * blockDim.x)
-        out[b * n + i] = replace_mod(in[b * n + i], target[b * tstride + i], tol);
+    const ZThr<T> z = zthr<T>(tol_);
+    const cx<T>* ib = in + b * n;
+    const T* tb = target + b * tstride;
+    cx<T>* ob = out + b * n;
+    auto keep = [](int, cx<T>, cx<T> o) { return o; };
+    for (long long i = (blockIdx.x * (long long)blockDim.x + threadIdx.x) * 4; i < n;
+         i += (long long)gridDim.x * blockDim.x * 4) {
+        if (i + 4 <= n) {
+            cx<T> v[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) v[k] = ib[i + k];
+            auto t_of = [&](int k) -> T { return tb[i + k]; };
+            if (z.ftz) project_regs<false, true>(v, z, t_of, keep);
+            else project_regs<false, false>(v, z, t_of, keep);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) ob[i + k] = v[k];
+        } else {
+            for (long long j = i; j < n; ++j) ob[j] = replace_mod(ib[j], tb[j], z);
+        }
+    }
 }
 
 // Fixed partition: block i reduces [i*chunk, (i+1)*chunk) with a fixed
@@ -105,12 +125,11 @@ template <> __device__ __forceinline__ double sq_mag<double>(const double* d, lo
 }
 template <> __device__ __forceinline__ double sq_mag<float2>(const float2* d, long long i) {
     const float2 u = d[i];
-    const double a = (double)sqrtf(u.x * u.x + u.y * u.y);   // |u| in field precision
+    const double a = (double)np_cabs(u);                    // np.abs in field precision
     return a * a;
 }
 template <> __device__ __forceinline__ double sq_mag<double2>(const double2* d, long long i) {
-    const double2 u = d[i];
-    const double a = sqrt(u.x * u.x + u.y * u.y);
+    const double a = np_cabs(d[i]);
     return a * a;
 }
 
@@ -133,14 +152,14 @@ __global__ void sum_partial_kernel(const double* d, long long n, long long chunk
 
 // |P_S u - w|^2 partials for metrics.gap (src/metrics.py:67-71).
 template <typename T>
-__global__ void gap_partial_kernel(const cx<T>* u, const cx<T>* pm_u, const T* p, T tol,
+__global__ void gap_partial_kernel(const cx<T>* u, const cx<T>* pm_u, const T* p, T tol_,
                                    long long n, long long chunk, double* part) {
     const long long lo = blockIdx.x * chunk, hi = min(n, lo + chunk);
+    const ZThr<T> tol = zthr<T>(tol_);
     double acc = 0.0;
     for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) {
         const cx<T> ps = replace_mod(u[i], p[i], tol);
-        const T dx = ps.x - pm_u[i].x, dy = ps.y - pm_u[i].y;
-        const double a = (double)sqrt(dx * dx + dy * dy);
+        const double a = (double)np_cabs(mk<T>(ps.x - pm_u[i].x, ps.y - pm_u[i].y));   // np.abs in field precision
         acc += a * a;
     }
     const double s = block_sum(acc);
@@ -161,8 +180,7 @@ __global__ void phases_kernel(const cx<T>* u, long long n, T tol, double* out) {
          i += (long long)gridDim.x * blockDim.x) {
         const cx<T> v = u[i];
         double th = phase_of((double)v.x, (double)v.y);
-        const T mag = sqrt(v.x * v.x + v.y * v.y);
-        if (tol > T(0) && mag < tol) th = 0.0;
+        if (tol > T(0) && np_cabs(v) < tol) th = 0.0;        // np.abs(u) < zero_tol
         out[i] = th;
     }
 }
@@ -292,15 +310,24 @@ __global__ void escale_kernel(const double* part, int nb, int per_mask, double* 
     escale[b] = energy[b] / s;
 }
 
-// fp32 zero-branch decision on s = |u|^2: the least float s with
-// sqrtf(s) >= (float)tol (the host's fp32_sq_threshold, bit for bit).
-__device__ double fp32_sq_threshold_dev(double tol) {
-    const float tf = (float)tol;
-    if (!(tf > 0.f)) return 0.0;
-    float s = __fmul_rn(tf, tf);
-    while (s > 0.f && __fsqrt_rn(s) >= tf) s = nextafterf(s, 0.f);
-    while (__fsqrt_rn(s) < tf) s = nextafterf(s, INFINITY);
-    return (double)s;
+// Decision tolerances of one mask (host and device): the reference's zero_tol
+// as the precision's float (src/projections.py:49-53 compares float32 mag with
+// the Python-float tolerance in float32, NEP 50). Every projection decides on
+// normalised values (pm_kernels.cuh, scaling convention), so the tolerances
+// are used as they are: thrp / thrx for P_S, thrm for the Fourier replace.
+__host__ __device__ inline void zero_thresholds(double tp, double tm, bool single, double* thrp, double* thrm,
+                                                double* thrx) {
+    const double qp = single ? (double)(float)tp : tp;
+    *thrp = qp;
+    *thrm = single ? (double)(float)tm : tm;
+    *thrx = qp;
+}
+
+// S p into `out` (the P_S target of the GS row sweeps: they write S u).
+template <typename T>
+__global__ void scale_grid_kernel(const T* in, T* out, long long n, T s) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        out[i] = in[i] * s;
 }
 
 // Per-mask zero tolerances 1024 eps max (src/grid.py:21,33-34) and the
@@ -347,18 +374,7 @@ __global__ void tol_final_kernel(const double* part, int nb, int batch, int sing
     const double eps = single ? 1.1920928955078125e-07 : 2.220446049250313e-16;
     const double tp = 1024.0 * eps * pmx, tm = 1024.0 * eps * mmx;
     tolp[b] = tp;
-    if (single) {
-        const double qp = fp32_sq_threshold_dev(tp), qm = fp32_sq_threshold_dev(tm);
-        thrp[b] = qp * nn;
-        thrm[b] = qm;
-        thrms[b] = qm * nn;
-        thrx[b] = qp;
-    } else {
-        thrp[b] = tp * sqrt(nn);
-        thrm[b] = tm;
-        thrms[b] = tm * sqrt(nn);
-        thrx[b] = tp;
-    }
+    zero_thresholds(tp, tm, single, thrp + b, thrm + b, thrx + b);
     const int z = (pmx == 0.0 ? 1 : 0) | (mmx == 0.0 ? 2 : 0);
     if (z) {
         st[b].zero = z;
@@ -435,17 +451,6 @@ int upload_twiddles(int prec, int lg, int lgR, int TW, void** fwd, void** inv) {
     return PM_OK;
 }
 
-// fp32 zero-branch decision on s = |u|^2: the least float s with
-// sqrtf(s) >= (float)tol, so `s >= thr` <=> `sqrtf(s) >= tol` exactly.
-double fp32_sq_threshold(double tol) {
-    const float tf = (float)tol;
-    if (!(tf > 0.f)) return 0.0;
-    float s = tf * tf;
-    while (s > 0.f && sqrtf(s) >= tf) s = nextafterf(s, 0.f);
-    while (sqrtf(s) < tf) s = nextafterf(s, INFINITY);
-    return (double)s;
-}
-
 std::map<const void*, size_t>& smem_configured() {
     static std::map<const void*, size_t> s;
     return s;
@@ -490,6 +495,8 @@ struct pm_plan {
     void* field2 = nullptr;           // RAAR: cap * N complex, second field buffer (w')
     void* mT = nullptr;               // persistent column phase: m transposed per mask
     size_t mT_bytes = 0;
+    void* ps = nullptr;               // GS sessions: S p, the row sweeps' P_S target
+    size_t ps_bytes = 0;
     void* xbuf = nullptr;             // RAAR: cap * N complex, the iterate x
     double* rpart = nullptr;          // RAAR: cap * ny * wpr * 2 row partials
     double* thrx = nullptr;           // cap P_S thresholds on true-scale values (RAAR, mixed-radix path)
@@ -539,6 +546,7 @@ struct pm_plan {
         const void* p = nullptr;
         const void* m = nullptr;
         const void* mT = nullptr;     // transposed m of this session (null: column tasks stage from m)
+        const void* ps = nullptr;     // S p (GS; the p grids of the session scaled on the device)
         long long p_stride = 0;
         void* phases = nullptr;
         void* levels = nullptr;
@@ -582,11 +590,11 @@ void free_buffers(pm_plan* pl) {
                     pl->thrm, pl->thrms, pl->escale, pl->energy, pl->psum};
     for (void* b : bufs)
         if (b) cudaFree(b);
-    void* rbufs[] = {pl->field2, pl->xbuf, pl->rpart, pl->thrx, pl->mT};
+    void* rbufs[] = {pl->field2, pl->xbuf, pl->rpart, pl->thrx, pl->mT, pl->ps};
     for (void* b : rbufs)
         if (b) cudaFree(b);
-    pl->field2 = pl->xbuf = pl->mT = nullptr;
-    pl->mT_bytes = 0;
+    pl->field2 = pl->xbuf = pl->mT = pl->ps = nullptr;
+    pl->mT_bytes = pl->ps_bytes = 0;
     pl->rpart = pl->thrx = nullptr;
     pl->raar_cap = 0;
     pl->field = pl->tmp = pl->pbuf = pl->mbuf = pl->ustar = pl->vstar = nullptr;
@@ -731,7 +739,7 @@ RowArgs<T> row_args(pm_plan* pl, int mode, int it) {
     RowArgs<T> a;
     a.field = (cx<T>*)pl->field;
     a.out = raar ? (cx<T>*)pl->field2 : a.field;
-    a.p = (const T*)pl->s.p;
+    a.p = (const T*)(raar ? pl->s.p : pl->s.ps);   // GS: S p (see scale_grid_kernel); RAAR: p
     a.p_stride = pl->s.p_stride;
     a.twf = (const twe<T>*)pl->tw_row;
     a.twi = (const twe<T>*)pl->tw_row_i;
@@ -814,8 +822,6 @@ ColArgs<T> col_args(pm_plan* pl, int mode, int u_iter) {
     a.ny = pl->ny;
     a.scale = (T)(1.0 / std::sqrt((double)pl->N));
     a.thr_m = pl->thrm;
-    a.thr_ms = pl->thrms;
-    a.scale_free = ((pl->lgx + pl->lgy) % 2 == 0) ? 1 : 0;
     a.escale = pl->escale;
     a.mode = mode;
     a.u_iter = u_iter;
@@ -1229,6 +1235,7 @@ int gen_row_sweep(pm_plan* pl, int it) {
 }
 
 int ensure_mT(pm_plan* pl);
+int ensure_ps(pm_plan* pl, int grids);
 int launch_transpose_m(pm_plan* pl);
 
 int gen_begin(pm_plan* pl) {
@@ -1455,6 +1462,10 @@ int session_setup(pm_plan* pl, const void* d_p, const void* d_m, int batch, cons
     s.p = d_p;
     s.m = d_m;
     s.p_stride = prm->p_per_mask ? (long long)pl->N : 0;
+    if (!pl->generic && prm->algorithm == PM_ALGO_GS) {
+        CKR(ensure_ps(pl, prm->p_per_mask ? batch : 1));
+        s.ps = pl->ps;
+    }
     pl->tm_m_ok = !pl->generic && tma_encode(&pl->tm_m, const_cast<void*>(d_m), pl->prec == PM_SINGLE, pl->nx, pl->ny,
                                              batch, tma_m_box(pl));
     // pinned-free small uploads: stage in the session's host vectors, which
@@ -1477,13 +1488,7 @@ int session_setup(pm_plan* pl, const void* d_p, const void* d_m, int batch, cons
     for (int b = 0; b < batch; ++b) {
         const double tp = tol_p[prm->p_per_mask ? b : 0];
         s.h_tolp[b] = tp;
-        // row projection runs on v' = v / S (S = 1/sqrt(N)): scale the threshold
-        s.h_thrp[b] = pl->prec == PM_SINGLE ? fp32_sq_threshold(tp) * (double)pl->N
-                                            : tp * std::sqrt((double)pl->N);
-        s.h_thrm[b] = pl->prec == PM_SINGLE ? fp32_sq_threshold(tol_m[b]) : tol_m[b];
-        // on S^-1 u^ (exact when N is a power of 4, the only case it is used)
-        s.h_thrms[b] = pl->prec == PM_SINGLE ? s.h_thrm[b] * (double)pl->N : s.h_thrm[b] * std::sqrt((double)pl->N);
-        s.h_thrx[b] = pl->prec == PM_SINGLE ? fp32_sq_threshold(tp) : tp;   // RAAR P_S on true scale
+        zero_thresholds(tp, tol_m[b], pl->prec == PM_SINGLE, &s.h_thrp[b], &s.h_thrm[b], &s.h_thrx[b]);
     }
     CK(cudaMemcpyAsync(pl->tolp, s.h_tolp.data(), batch * sizeof(double), cudaMemcpyHostToDevice, pl->stream));
     CK(cudaMemcpyAsync(pl->thrp, s.h_thrp.data(), batch * sizeof(double), cudaMemcpyHostToDevice, pl->stream));
@@ -1564,6 +1569,36 @@ bool persistent(const pm_plan* pl) {
 // field-only form, 2048^2 / 4096^2, stages m from this copy).
 // The transposed-m buffer for the session's batch (outside any capture;
 // captured graphs hold the old pointer, so they go when it is reallocated).
+// The S p buffer for `grids` amplitude grids (outside any capture; captured
+// graphs hold the old pointer, so they go when it is reallocated).
+int ensure_ps(pm_plan* pl, int grids) {
+    const size_t bytes = (size_t)grids * pl->N * pl->rsz;
+    if (bytes <= pl->ps_bytes) return PM_OK;
+    CK(cudaStreamSynchronize(pl->stream));
+    drop_graphs(pl);
+    if (pl->ps) cudaFree(pl->ps);
+    pl->ps = nullptr;
+    pl->ps_bytes = 0;
+    CK(cudaMalloc(&pl->ps, bytes));
+    pl->ps_bytes = bytes;
+    return PM_OK;
+}
+
+int enqueue_ps(pm_plan* pl) {
+    auto& s = pl->s;
+    if (!s.ps) return PM_OK;
+    const long long n = (long long)(s.prm.p_per_mask ? s.batch : 1) * (long long)pl->N;
+    const int blocks = (int)std::min<long long>((n + 255) / 256, 148 * 8);
+    const double S = 1.0 / std::sqrt((double)pl->N);
+    if (pl->prec == PM_SINGLE)
+        scale_grid_kernel<float><<<blocks, 256, 0, pl->stream>>>((const float*)s.p, (float*)pl->ps, n, (float)S);
+    else
+        scale_grid_kernel<double><<<blocks, 256, 0, pl->stream>>>((const double*)s.p, (double*)pl->ps, n, S);
+    CK(cudaGetLastError());
+    pl->launches++;
+    return PM_OK;
+}
+
 int ensure_mT(pm_plan* pl) {
     const size_t bytes = (size_t)pl->s.batch * pl->N * pl->rsz;
     if (bytes <= pl->mT_bytes) return PM_OK;
@@ -1607,6 +1642,7 @@ int enqueue_begin(pm_plan* pl) {
     CKR(enqueue_tolerances(pl));
     CKR(enqueue_escale(pl));
     if (pl->generic) return gen_begin(pl);
+    CKR(enqueue_ps(pl));
     if (persistent(pl)) {
         CKR(enqueue_mT(pl));
         return solve_launch(pl, 1, 1, 1, 0);
@@ -1653,7 +1689,7 @@ std::string graph_key(const pm_plan* pl) {
     snprintf(buf, sizeof buf, "%d|%d|%d|%d|%a|%a|%a|%d|%d|%a|%p|%p|%lld|%p|%p|%p|%p|%d", s.batch,
              s.prm.max_iters, s.prm.record_every, s.prm.init_complex, s.prm.early_stop_tol,
              s.prm.t_lit, s.prm.t_dark, s.prm.p_per_mask, s.prm.algorithm, s.prm.beta, s.p, s.m,
-             s.p_stride, s.phases, s.levels, s.ustar, s.vstar, (int)s.tol_on_device);
+             s.p_stride, s.phases, s.levels, s.ustar, s.vstar, (int)s.tol_on_device * 2 + (int)s.energy_on_device);
     return buf;
 }
 
@@ -1667,6 +1703,7 @@ int enqueue_full_solve(pm_plan* pl) {
         CK(cudaMemsetAsync(pl->hist, 0, (size_t)s.batch * pl->hist_cap * 4 * sizeof(double), pl->stream));
         CKR(enqueue_tolerances(pl));
         CKR(enqueue_escale(pl));
+        CKR(enqueue_ps(pl));
         CKR(enqueue_mT(pl));
         s.it = s.prm.max_iters;
         return solve_launch(pl, 1, 1, s.prm.max_iters + 1, 1);
@@ -1992,7 +2029,7 @@ static int replace_dev(pm_plan* pl, const void* in, const void* target, int per_
     if (pl->prec == PM_SINGLE)
         // fp32 decides on |u|^2 against the exact squared threshold (as the solve does)
         replace_kernel<float><<<dim3(blocks, batch), 256, 0, pl->stream>>>(
-            (const float2*)in, (const float*)target, per_field ? n : 0, (float)fp32_sq_threshold(tol), (float2*)out, n);
+            (const float2*)in, (const float*)target, per_field ? n : 0, (float)tol, (float2*)out, n);
     else
         replace_kernel<double><<<dim3(blocks, batch), 256, 0, pl->stream>>>(
             (const double2*)in, (const double*)target, per_field ? n : 0, tol, (double2*)out, n);
@@ -2071,7 +2108,7 @@ int pm_gap(pm_plan* pl, const void* u, const void* p, const void* m, double zero
     if (pl->prec == PM_SINGLE)
         gap_partial_kernel<float><<<nb, 256, 0, pl->stream>>>((const float2*)pl->tmp, (const float2*)pl->field,
                                                                (const float*)pl->pbuf,
-                                                               (float)fp32_sq_threshold(zero_tol_p), n, chunk,
+                                                               (float)zero_tol_p, n, chunk,
                                                                pl->red);
     else
         gap_partial_kernel<double><<<nb, 256, 0, pl->stream>>>((const double2*)pl->tmp,

@@ -429,20 +429,24 @@ __global__ void gen_col_sweep_kernel(cx<T>* w, const T* m, const T* mT, const do
     cx<T>* B = A == sm.A ? sm.B : sm.A;
     cp_async_wait<0>();
     __syncthreads();
-    const T thr = T(thr_m[b]);
+    const ZThr<T> thr = zthr<T>(T(thr_m[b]));
     const double es = escale[b];
     double acc[3] = {0.0, 0.0, 0.0};
+    cx<T> chk = mk<T>(T(0), T(0));
     for (int idx = threadIdx.x; idx < L * TC; idx += blockDim.x) {
         const int t = idx & (TC - 1);
         if (t >= tc) continue;
         const cx<T> u = cscale(A[idx], sc);                      // u^ = F(u)
+        fold_finite(chk, u);                                     // Field check of iteration u_iter + 1
         const T mm = sm.g[idx];
         const cx<T> vh = replace_mod(u, mm, thr);
         if (gneed) acc[0] += norm_sq_d(csub(u, vh));
         if (rec) {
             const double inten = norm_sq_d(u) * es;
             const double m2 = (double)mm * (double)mm;
-            if (m2 > 0.0) {
+            if (!(inten <= 1.7976931348623157e308)) {
+                acc[1] = __longlong_as_double(0x7ff8000000000000LL);       // RealGrid's check (src/grid.py:128-129)
+            } else if (m2 > 0.0) {
                 const double dev = fabs(m2 - inten);
                 if (dev > g.ctl.t_lit * m2 && dev / m2 > g.ctl.t_lit)
                     acc[1] += g.ctl.t_dark * dev / (g.ctl.t_lit * m2) - g.ctl.t_dark;
@@ -452,6 +456,7 @@ __global__ void gen_col_sweep_kernel(cx<T>* w, const T* m, const T* mT, const do
         }
         A[idx] = vh;
     }
+    if (!metrics_only && !all_finite(chk)) first_bad(&st->bad, u_iter + 1);
     __syncthreads();
     if (!metrics_only) {
         A = gen_passes<T>(A, B, sm.tw, gp, lgTC, +1);
@@ -498,17 +503,16 @@ __global__ void gen_row_sweep_kernel(cx<T>* w, cx<T>* u, const T* p, long long p
     cx<T>* B = A == sm.A ? sm.B : sm.A;
     cp_async_wait<0>();
     __syncthreads();
-    const T thr = T(thr_p[b]);
-    T chk = T(0);
+    const ZThr<T> thr = zthr<T>(T(thr_p[b]));
+    cx<T> chk = mk<T>(T(0), T(0));
     for (int idx = threadIdx.x; idx < L * TC; idx += blockDim.x) {
         const int t = idx & (TC - 1);                        // element idx >> lgTC of row t0 + t
         if (t >= tc) continue;
-        T s2;
-        const cx<T> uu = replace_mod(cscale(A[idx], sc), sm.g[idx], thr, s2);
-        chk += s2;
-        A[idx] = uu;
+        const cx<T> v = cscale(A[idx], sc);
+        fold_finite(chk, v);                                 // v = F^-1 v^ (reference Field check)
+        A[idx] = replace_mod(v, sm.g[idx], thr);
     }
-    if (!isfinite(chk)) first_bad(&st[b].bad, it);
+    if (!all_finite(chk)) first_bad(&st[b].bad, it);
     __syncthreads();
     if (store_u) gen_scatter<T>(A, ub, L, lgTC, t0, tc, L, 1, T(1));   // the iterate (stepping sessions)
     A = gen_passes<T>(A, B, sm.tw, gp, lgTC, -1);
@@ -557,7 +561,7 @@ __global__ void gen_row_raar_kernel(cx<T>* w, const cx<T>* x_in, cx<T>* x_out, c
     cx<T>* B = A == sm.A ? sm.B : sm.A;
     cp_async_wait<0>();
     __syncthreads();
-    const T thr = T(thr_p[b]);
+    const ZThr<T> thr = zthr<T>(T(thr_p[b]));
     const cx<T>* xb = x_in + b * g.n;
     cx<T>* xo = x_out + b * g.n;
     double g2 = 0.0, e2 = 0.0;
@@ -623,8 +627,7 @@ __global__ void gen_final_kernel(const cx<T>* vs, const T* p, long long p_stride
         if (u_star) u_star[x] = us;
         if (phases || levels) {
             double th = phase_of((double)us.x, (double)us.y);
-            const T mag = sqrt(us.x * us.x + us.y * us.y);
-            if (tol > T(0) && mag < tol) th = 0.0;
+            if (tol > T(0) && np_cabs(us) < tol) th = 0.0;        // np.abs(u*) < zero_tol
             if (phases) phases[x] = th;
             if (levels) levels[x] = level_of(th);
         }

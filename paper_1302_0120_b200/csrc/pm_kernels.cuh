@@ -92,14 +92,14 @@ struct RowArgs {
     const twe<T>* twi;        // inverse twiddles (fp64: same as twf)
     int nx, ny;
     T scale;                  // S = 1/sqrt(nx*ny)
-    const double* thr_p;      // [batch] zero-branch threshold on v' = v/S (fp32: on |v'|^2, fp64: on |v'|)
+    const double* thr_p;      // [batch] zero tolerance (T-rounded) of P_S
     int mode;                 // RowMode
     int it;                   // index of the iterate this sweep produces
     MaskState* st;
     // RAAR; unused by GS
     cx<T>* x;                 // [batch][N] iterate x (SLM plane, true scale)
     T beta, c1;               // beta and 1 - 2 beta, rounded to T as numpy does (NEP 50)
-    const double* thr_x;      // [batch] P_S threshold on true-scale values (fp32: on |.|^2)
+    const double* thr_x;      // [batch] P_S zero tolerance (T-rounded) on true-scale values
     double* rpart;            // [batch][ny * wpr][2]: gap^2 of x_{it-1}, |x_it|^2, per row warp
     int wpr;                  // partial slots per row: max(1, TG / 32)
     SolveCtl ctl;
@@ -151,9 +151,7 @@ struct ColArgs {
     const twe<T>* twi;
     int nx, ny;
     T scale;                  // S = 1/sqrt(nx*ny)
-    const double* thr_m;      // [batch] zero-branch threshold on u^ (fp32: on |u^|^2, fp64: on |u^|)
-    const double* thr_ms;     // [batch] the same on S^-1 u^ (used when scale_free)
-    int scale_free;           // N is a power of 4: S is a power of two and the replace is scale-invariant
+    const double* thr_m;      // [batch] zero tolerance (T-rounded) on u^
     const double* escale;     // [batch] sum m^2 / sum |u|^2 (reconstructed-intensity scale)
     int mode;                 // 0: init from real m, 1: init from complex field, 2: iterate
     int u_iter;               // metrics of iterate u_{u_iter} (0 = none)
@@ -270,8 +268,10 @@ __device__ __forceinline__ void decide(MaskState* st, double* hist_row, const So
                                        const double (&tot)[3]) {
     const double g = sqrt(tot[0]);
     int stop = 0;
-    if (!isfinite(tot[0]) || st->bad) {
-        st->diverged = st->bad ? st->bad : i;
+    // divergence = a non-finite field (the sweeps' explicit checks); an
+    // overflowing gap of a finite field is recorded as is, like the reference's
+    if (st->bad) {
+        st->diverged = st->bad;
         st->done = 1;
         stop = 1;
     }
@@ -357,6 +357,17 @@ template <typename C> __device__ __forceinline__ double norm_sq_d(C u) {
     return (double)u.x * (double)u.x + (double)u.y * (double)u.y;
 }
 
+// Non-finite detector of the reference's Field checks (src/grid.py:100-110):
+// chk stays 0 while every value folded in is finite (v * 0 is NaN for inf or
+// NaN), one packed FMA per complex value; magnitudes are never squared, so
+// large finite fields (|u|^2 beyond the float range) are not flagged.
+__device__ __forceinline__ void fold_finite(float2& chk, float2 v) { chk = fma2(v, make_float2(0.f, 0.f), chk); }
+__device__ __forceinline__ void fold_finite(double2& chk, double2 v) {
+    chk.x = fma(v.x, 0.0, chk.x);
+    chk.y = fma(v.y, 0.0, chk.y);
+}
+template <typename C> __device__ __forceinline__ bool all_finite(C chk) { return chk.x == 0 && chk.y == 0; }
+
 // Record the first iteration whose iterate went non-finite (decisions may be
 // taken only every few iterations; the reference reports the first).
 __device__ __forceinline__ void first_bad(int* bad, int it) {
@@ -371,13 +382,17 @@ template <> __device__ __forceinline__ double min_normal<double>() { return 2.22
 template <typename C> __device__ __forceinline__ C ld_field(const C* p) { return __ldcg(p); }
 
 // ------------------------------------------------------------------ tasks
-// Scaling convention: the field holds UNNORMALISED half transforms between
-// phases (w' = RowFFT(u), z' = ColIFFT(v^)); the unitary factor
-// S = 1/sqrt(n_x n_y) is applied once per iteration, where the column phase
-// forms u^ = F(u) = S * ColFFT(w'). The row projection works on
-// v' = RowIFFT(z') = v / S, with its zero-branch threshold pre-scaled on the
-// host (exact for power-of-two grids, where S is a power of two), because
-// P_S(v) = P_S(v / S).
+// Scaling convention: the unitary factor S = 1/sqrt(n_x n_y) is applied
+// once per half iteration, at the projections, as the targets' scale: P_S
+// writes S u (p pre-scaled by S on the device once per solve; RAAR scales
+// its combine), the column replace writes S v^. The field between phases
+// is then w'' = RowFFT(S u) = S RowFFT(u) and conj(z'') with
+// z'' = S ColIFFT(v^) (unnormalised transforms of the scaled values), so the
+// column phase's ColFFT(w'') IS u^ = F(u) and the row phase's RowFFT(conj z'')
+// IS conj(v): both projections decide on the normalised values against the
+// reference's zero_tol itself, and every intermediate stays within
+// sqrt(n) of a normalised transform, as scipy's (DUCC scales by S after
+// the first axis), so overflow happens where the reference's does.
 
 // ------------------------------------------------------- shared staging
 // cp.async copies of a task's real grid (p or m) into shared memory, issued
@@ -573,56 +588,47 @@ __device__ __forceinline__ void row_task(const RowArgs<T>& a, int b, int row, in
             sync();
         }
         if (ALG != 1 && a.mode == kRowGS) {
-            // u = P_S v = P_S v' = conj(P_S y) (src/projections.py:69-74), threshold pre-scaled
-            const T thr = T(a.thr_p[b]);
-            T chk = T(0);
-            if (thr >= min_normal<T>()) {
-#pragma unroll
-                for (int k = 0; k < F::R; ++k) {
-                    T s2;
-                    v[k] = replace_mod<true, true>(v[k], inb ? p_at(k) : T(0), thr, s2);
-                    chk += s2;                          // non-finite detector (reference Field checks)
-                }
-            } else {
-#pragma unroll
-                for (int k = 0; k < F::R; ++k) {
-                    T s2;
-                    v[k] = replace_mod<true>(v[k], inb ? p_at(k) : T(0), thr, s2);
-                    chk += s2;
-                }
-            }
-            if (act && !isfinite(chk)) first_bad(&a.st[b].bad, a.it);
+            // S u = S P_S v = conj(P_S(y; S p)) (src/projections.py:69-74): y = conj(v) is
+            // the normalised field, decided against zero_tol itself; p arrives pre-scaled by S
+            const ZThr<T> z = zthr<T>(T(a.thr_p[b]));
+            auto t_of = [&](int k) -> T { return inb ? p_at(k) : T(0); };
+            auto keep = [](int, cx<T>, cx<T> o) { return o; };
+            // false: v = F^-1 v^ was not finite (the reference's Field check)
+            const bool fin = z.ftz ? project_regs<true, true>(v, z, t_of, keep)
+                                   : project_regs<true, false>(v, z, t_of, keep);
+            if (act && !fin) first_bad(&a.st[b].bad, a.it);
         } else if (a.mode == kRowInit) {
             cx<T>* xp = (ALG != 0 && a.x) ? a.x + b * N + (size_t)row * a.nx + j : nullptr;
 #pragma unroll
             for (int k = 0; k < F::R; ++k) {
-                v[k] = cscale_conj(v[k], a.scale);                        // u0 = S * v'
-                if (xp && act) xp[F::TG * k] = v[k];                      // RAAR: x_0 = u0
+                const cx<T> u0 = cconj(v[k]);                             // u0 = F^-1 m (src/solver.py:105-108)
+                if (xp && act) xp[F::TG * k] = u0;                        // RAAR: x_0 = u0
+                v[k] = cscale(u0, a.scale);                               // the row FFT of S u0 follows
             }
         } else if (ALG != 0) {
-            // RAAR, v = P_M x_{it-1} = S * v' = S * conj(y):
+            // RAAR, v = P_M x_{it-1} = conj(y), p at true scale:
             //   gap of x_{it-1} = ||P_S x_{it-1} - v|| (src/metrics.py:67-71), when needed;
             //   x_it = beta x + beta P_S(2v - x) + (1 - 2 beta) v, numpy's operation order.
             const int gi = a.it - 1;
             const bool gneed = act && gi >= 1 && gap_needed(a.ctl, gi) && __ldcg(&a.st[b].decided) < gi;
             const bool upd = a.mode == kRowRaar;
-            const T thr = T(a.thr_x[b]);
+            const ZThr<T> z = zthr<T>(T(a.thr_x[b]));
             cx<T>* xp = a.x + b * N + (size_t)row * a.nx + j;
             double g2 = 0.0, e2 = 0.0;
 #pragma unroll
             for (int k = 0; k < F::R; ++k) {
-                const cx<T> vv = cscale_conj(v[k], a.scale);
+                const cx<T> vv = cconj(v[k]);
                 cx<T> xo;
                 if constexpr (XS) xo = inb ? xs[j + F::TG * k] : mk<T>(T(0), T(0));
                 else xo = inb ? ld_field(xp + F::TG * k) : mk<T>(T(0), T(0));
                 const T pk = inb ? p_at(k) : T(0);
-                if (gneed) g2 += norm_sq_d(csub_rn(replace_mod(xo, pk, thr), vv));
+                if (gneed) g2 += norm_sq_d(csub_rn(replace_mod(xo, pk, z), vv));
                 if (upd) {
-                    const cx<T> py = replace_mod(csub_rn(cscale(vv, T(2)), xo), pk, thr);
+                    const cx<T> py = replace_mod(csub_rn(cscale(vv, T(2)), xo), pk, z);
                     const cx<T> xn = cadd_rn(cadd_rn(cmul_rn(xo, a.beta), cmul_rn(py, a.beta)), cmul_rn(vv, a.c1));
                     if (act) xp[F::TG * k] = xn;
                     e2 += norm_sq_d(xn);
-                    v[k] = xn;
+                    v[k] = cscale(xn, a.scale);                           // the row FFT of S x_it follows
                 }
             }
             if (upd && act && !isfinite(e2)) first_bad(&a.st[b].bad, a.it);
@@ -655,17 +661,17 @@ __device__ __forceinline__ void final_task(const FinalArgs<T>& a, int b, int row
     for (int k = 0; k < F::R; ++k) v[k] = act ? ld_field(a.field + o + F::TG * k) : mk<T>(T(0), T(0));
     fft1d<T, LG_L, LG_R, -1, TS>(v, sm, tw, j, sync);
 #pragma unroll
-    for (int k = 0; k < F::R; ++k) v[k] = cscale_conj(v[k], a.scale);     // v*
+    for (int k = 0; k < F::R; ++k) v[k] = cconj(v[k]);                    // v* (normalised)
     if (a.x) {
         // RAAR: gap of the last iterate, ||P_S x_K - P_M x_K|| with P_M x_K = v*
         const int i = a.ctl.max_iters;
         const bool gneed = act && !__ldcg(&a.st[b].stop) && gap_needed(a.ctl, i) && __ldcg(&a.st[b].decided) < i;
         double g2 = 0.0;
         if (gneed) {
-            const T thr = T(a.thr_x[b]);
+            const ZThr<T> z = zthr<T>(T(a.thr_x[b]));
 #pragma unroll
             for (int k = 0; k < F::R; ++k)
-                g2 += norm_sq_d(csub_rn(replace_mod(ld_field(a.x + o + F::TG * k), p[F::TG * k], thr), v[k]));
+                g2 += norm_sq_d(csub_rn(replace_mod(ld_field(a.x + o + F::TG * k), p[F::TG * k], z), v[k]));
         }
         row_partials<F::TG>(g2, 0.0, a.rpart + ((size_t)b * a.ny + row) * a.wpr * 2, j, gneed);
     }
@@ -680,8 +686,7 @@ __device__ __forceinline__ void final_task(const FinalArgs<T>& a, int b, int row
         if (a.u_star) a.u_star[x] = us;
         if (a.phases || a.levels) {
             double th = phase_of((double)us.x, (double)us.y);
-            const T mag = sqrt(us.x * us.x + us.y * us.y);
-            if (tol > T(0) && mag < tol) th = 0.0;
+            if (tol > T(0) && np_cabs(us) < tol) th = 0.0;        // np.abs(u*) < zero_tol
             if (a.phases) a.phases[x] = th;
             if (a.levels) a.levels[x] = level_of(th);
         }
@@ -731,7 +736,7 @@ __device__ __forceinline__ void col_task(const ColArgs<T>& a, int b, int col0, i
         // u0 = F^-1(m e^{i0}) (src/solver.py:93-108): m is real, so the stored
         // conj(ColIFFT(m)) is ColFFT(m); the row phase finishes u0
 #pragma unroll
-        for (int k = 0; k < F::R; ++k) v[k] = mk<T>(m[k * rs], T(0));
+        for (int k = 0; k < F::R; ++k) v[k] = mk<T>(m[k * rs] * a.scale, T(0));
     } else if (TM && a.mode == 2) {
         mbar_wait(&tma.bars[0], tma.parity);
 #pragma unroll
@@ -750,7 +755,7 @@ __device__ __forceinline__ void col_task(const ColArgs<T>& a, int b, int col0, i
         for (int k = 0; k < F::R; ++k) v[k] = ld_field(src + k * rs);
         if (a.mode == 1) {
 #pragma unroll
-            for (int k = 0; k < F::R; ++k) v[k] = cconj(v[k]);          // complex start: conj in, conj(IFFT) out
+            for (int k = 0; k < F::R; ++k) v[k] = cscale_conj(v[k], a.scale);   // complex start: conj in, conj(IFFT) out
         }
     }
     if (a.mode < 2) {
@@ -790,14 +795,8 @@ __device__ __forceinline__ void col_task(const ColArgs<T>& a, int b, int col0, i
     for (int h = 0; h < trips; ++h) {
         fft1d<T, LG_L, LG_R, -1, TS>(v, sm, tw, j, SyncBlock{});   // h = 0: ColFFT(w'); h = 1: conj(z')
         if (h) break;
-        // u^ = F(u) = S * ColFFT(w'): the replace is invariant to the exact
-        // power-of-two S (threshold pre-scaled), so only metrics need u^ itself
-        const bool scaled = rec || gneed || !a.scale_free;
-        if (scaled) {
-#pragma unroll
-            for (int k = 0; k < F::R; ++k) v[k] = cscale(v[k], a.scale);
-        }
-        const T thr = T(scaled ? a.thr_m[b] : a.thr_ms[b]);
+        // u^ = F(u) = ColFFT(w''), w'' = S RowFFT(u): normalised, decided against zero_tol itself
+        const ZThr<T> z = zthr<T>(T(a.thr_m[b]));
         T mm[F::R];
         if (TM && tma.mt) {
             mbar_wait(&tma.bars[1], tma.parity);
@@ -843,9 +842,11 @@ __device__ __forceinline__ void col_task(const ColArgs<T>& a, int b, int col0, i
             }
 #pragma unroll
             for (int k = 0; k < F::R; ++k) {
-                const double inten = (double)norm_sq(v[k]) * sc;
+                const double inten = norm_sq_d(v[k]) * sc;    // fp64 square: no overflow for large fp32 fields
                 const double m2 = (double)mm[k] * (double)mm[k];
-                if (m2 > 0.0) {
+                if (!(inten <= 1.7976931348623157e308)) {
+                    acc[1] = __longlong_as_double(0x7ff8000000000000LL);   // RealGrid's check (src/grid.py:128-129)
+                } else if (m2 > 0.0) {
                     const double dev = fabs(m2 - inten);
                     if (dev > a.ctl.t_lit * m2 && dev / m2 > a.ctl.t_lit)
                         acc[1] += a.ctl.t_dark * dev / (a.ctl.t_lit * m2) - a.ctl.t_dark;
@@ -854,24 +855,18 @@ __device__ __forceinline__ void col_task(const ColArgs<T>& a, int b, int col0, i
                 }
             }
         }
-        T g2 = T(0);
-        if (thr >= min_normal<T>()) {
-#pragma unroll
-            for (int k = 0; k < F::R; ++k) {
-                const cx<T> vh = replace_mod<true, true>(v[k], mm[k], thr);   // conj(v^), v^ = replace_m(u^)
-                // G(u) = ||P_S u - P_M u|| = ||u^ - v^||  (Parseval; u is on S)
-                if (gneed) g2 += norm_sq(csub(v[k], cconj(vh)));
-                v[k] = vh;
-            }
-        } else {
-#pragma unroll
-            for (int k = 0; k < F::R; ++k) {
-                const cx<T> vh = replace_mod<true>(v[k], mm[k], thr);
-                if (gneed) g2 += norm_sq(csub(v[k], cconj(vh)));
-                v[k] = vh;
-            }
-        }
-        acc[0] = act ? (double)g2 : 0.0;
+        double g2 = 0.0;                              // fp64: |u^ - v^|^2 of a large finite field stays finite
+        // conj(v^), v^ = replace_m(u^); G(u) = ||P_S u - P_M u|| = ||u^ - v^|| (Parseval; u is on S);
+        // the column FFT of S conj(v^) follows
+        auto t_of = [&](int k) -> T { return mm[k]; };
+        auto epi = [&](int, cx<T> u, cx<T> vh) -> cx<T> {
+            if (gneed) g2 += norm_sq_d(csub(u, cconj(vh)));
+            return cscale(vh, a.scale);
+        };
+        // false: u^ = F(u_{u_iter}) was not finite, the reference's Field check of iteration u_iter + 1
+        const bool fin = z.ftz ? project_regs<true, true>(v, z, t_of, epi) : project_regs<true, false>(v, z, t_of, epi);
+        if (act && !fin) first_bad(&a.st[b].bad, a.u_iter + 1);
+        acc[0] = act ? g2 : 0.0;
     }
     if (act) {
 #pragma unroll

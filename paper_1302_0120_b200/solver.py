@@ -187,6 +187,33 @@ def _host_cast(a: np.ndarray, dtype) -> np.ndarray:
     return out
 
 
+def _reference_error(cfg: SolveConfig, diverged: int, gaps, lits, darks) -> Exception | None:
+    """The exception the reference's solve() raises for this outcome, in its
+    order of events (None: it returns normally).
+
+    ``diverged`` is the first iteration whose fields the device found
+    non-finite (0: none), i.e. the iteration whose body would raise
+    SolveDivergedError (src/solver.py:152-165). The reference evaluates the
+    metrics of iteration it-1 before that body when it-1 is recorded or early
+    stopping is on (:172-176), and their Field checks see the same non-finite
+    transform first: ValueError("field contains non-finite entries") from
+    metrics.gap (src/metrics.py:67-71, src/grid.py:108-109). A recorded
+    reconstructed intensity that is not finite fails RealGrid's check
+    (src/metrics.py:81-88, src/grid.py:128-129).
+    """
+    early = cfg.early_stop_tol is not None
+    last = diverged if diverged else len(gaps)
+    for it in range(1, last + 1):
+        if it == diverged:
+            return SolveDivergedError(it)
+        rec = (it - 1) % cfg.record_every == 0
+        if (rec or early) and diverged == it + 1 and cfg.algorithm == "gs":
+            return ValueError("field contains non-finite entries")
+        if rec and not (np.isfinite(lits[it - 1]) and np.isfinite(darks[it - 1])) and not np.isnan(gaps[it - 1]):
+            return ValueError("grid contains non-finite entries")
+    return None
+
+
 def _history(it_ms, iters_run, gaps, lits, darks):
     out = []
     for i in range(1, iters_run + 1):
@@ -288,8 +315,11 @@ def solve(c: SlmConstraint, m: FourierConstraint, cfg: SolveConfig,
                     break
             code = lib.pm_solve_finish(plan.handle, int(aborted), res)
     if code == _lib.PM_ERR_DIVERGED or div[0]:
-        raise SolveDivergedError(int(div[0]) or 1)
+        raise _reference_error(cfg, int(div[0]) or 1, gaps, lits, darks)
     _lib.check(code, "pm_solve")
+    err = _reference_error(cfg, 0, gaps[:int(iters[0])], lits, darks)
+    if err is not None:
+        raise err
     total_ms = (time.perf_counter() - t0) * 1e3
     iters_run = int(iters[0])
     it_ms = float(dev_ms[0]) / max(iters_run, 1)

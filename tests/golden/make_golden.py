@@ -170,5 +170,46 @@ def main():
          source="oracle-restatement")
 
 
+# Outcome of the reference's solve() on amplitudes scaled towards the float
+# range (the divergence / non-finite contract, src/solver.py:27-32,152-199,
+# src/grid.py:100-110,128-129): "ok", "div<it>" (SolveDivergedError) or
+# "VE:<message>" (ValueError from a Field / RealGrid check in the metrics).
+DIVERGENCE_CASES = [(n, ny, tag, c, rec, es)
+                    for n, ny in ((64, 64), (256, 256), (120, 90))
+                    for tag, c in (("single", 1e19), ("single", 1e36), ("single", 1e38),
+                                   ("double", 1e160), ("double", 1e308))
+                    for rec, es in ((1, None), (100, None), (100, 1e-3))]
+
+
+def divergence_outcomes():
+    from phasemask.solver import SolveDivergedError
+    out = []
+    for n, ny, tag, c, rec, es in DIVERGENCE_CASES:
+        p, m = make_problem(n, 8, 7, n_y=ny)
+        p = p / p.max() * c
+        try:
+            ref_solve(p, m, tag, 6, record_every=rec, early_stop_tol=es)
+            o = "ok"
+        except SolveDivergedError as e:
+            o = f"div{e.iteration}"
+        except ValueError as e:
+            o = f"VE:{e}"
+        out.append(o)
+    return out
+
+
+def main_divergence():
+    import json
+    with np.errstate(all="ignore"):
+        out = divergence_outcomes()
+    (HERE / "divergence_outcomes.json").write_text(json.dumps(
+        {"cases": [list(c) for c in DIVERGENCE_CASES], "K": 6, "spots": 8, "seed": 7, "outcomes": out}, indent=0))
+    print("divergence_outcomes.json", len(out))
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["divergence"]:
+        main_divergence()
+    else:
+        main()
+        main_divergence()

@@ -307,3 +307,68 @@ def test_norm2_absolute_homogeneity(alpha):
     base = norm2(pm.Field(spec, data))
     scaled = norm2(pm.Field(spec, alpha * data))
     assert scaled == pytest.approx(abs(alpha) * base, rel=4 * np.finfo(float).eps * 10)
+
+
+def _straddle(tag, tol, n, seed):
+    """n complex values whose numpy modulus np.abs(u) lies within 2 ulp of
+    float(tol) in the precision (the reference compares in the array dtype,
+    NEP 50), led by values on which np.abs and hypot fall on opposite sides of
+    the tolerance."""
+    prec = pm.Precision.from_tag(tag)
+    fdt, cdt = np.dtype(prec.float_dtype).type, np.dtype(prec.complex_dtype).type
+    itype = np.int32 if fdt == np.float32 else np.int64
+    tf = fdt(tol)
+    rng = np.random.default_rng(seed)
+    k = 2_000_000
+    th = rng.uniform(0.05, np.pi / 2 - 0.05, k) + rng.integers(0, 4, k) * (np.pi / 2)
+    r = float(tf) * (1.0 + rng.integers(-8, 9, k) * float(np.finfo(fdt).eps) * 0.5)
+    z = (r * np.cos(th)).astype(fdt) + 1j * (r * np.sin(th)).astype(fdt)
+    z = z.astype(cdt)
+    mag = np.abs(z)
+    ulps = np.abs(mag.view(itype).astype(np.int64) - np.array(tf).view(itype).astype(np.int64))
+    near = ulps <= 2
+    hyp = np.hypot(z.real, z.imag).astype(fdt)
+    split = near & ((hyp >= tf) != (mag >= tf))
+    pick = np.concatenate([np.nonzero(split)[0][: n // 4], np.nonzero(near & ~split)[0]])[:n]
+    assert pick.size == n and split.any()
+    return z[pick], int(split.sum())
+
+
+@pytest.mark.parametrize("tag", ["single", "double"])
+@pytest.mark.parametrize("which", ["slm", "modulus"])
+def test_zero_branch_straddling_tolerance_bitwise(tag, which):
+    """Pixels with |u| within +-2 ulp of zero_tol, including ones where numpy's
+    |u| and hypot disagree: the GPU takes numpy's decision on every one
+    (src/projections.py:49-53) and the replaced values agree to the ulp."""
+    prec = pm.Precision.from_tag(tag)
+    spec = pm.GridSpec(64, 64)
+    rng = np.random.default_rng(3)
+    t = rng.uniform(0.25, 1.0, spec.shape)
+    t[0, 0] = 1.0 + 2 * float(np.finfo(prec.float_dtype).eps)   # max(t): the tolerance scale
+    tol = prec.zero_tol(float(t.max()))
+    u, _ = _straddle(tag, tol, spec.n, seed=17 if which == "slm" else 19)
+    u = u.reshape(spec.shape)
+    if which == "slm":
+        got = project_slm(pm.Field(spec, u), pm.SlmConstraint(pm.RealGrid(spec, t), prec)).data
+    else:
+        got = project_modulus(pm.Field(spec, u, FOURIER_PLANE), pm.FourierConstraint(pm.RealGrid(spec, t), prec)).data
+    want = orc.replace_modulus(u, t, tol, tag)
+    tq = t.astype(prec.float_dtype)
+    zero_got = (got.real == tq) & (got.imag == 0)
+    zero_want = (want.real == tq) & (want.imag == 0)
+    assert zero_want.any() and (~zero_want).any()
+    np.testing.assert_array_equal(zero_got, zero_want)
+    np.testing.assert_allclose(got, want, rtol=4 * prec.eps_machine, atol=0)
+
+
+@pytest.mark.parametrize("tag", ["single", "double"])
+def test_phases_zero_decision_straddling(tag):
+    """phases_of's `np.abs(u) < zero_tol -> 0` (src/grid.py:174-175) on values at
+    the tolerance +-2 ulp: the device decision is numpy's."""
+    prec = pm.Precision.from_tag(tag)
+    tol = prec.zero_tol(1.0)
+    u, _ = _straddle(tag, tol, 4096, seed=23)
+    spec = pm.GridSpec(64, 64)
+    got = pm.phases_of(pm.Field(spec, u.reshape(spec.shape)), tol).phases
+    want = orc.phases_of(u.reshape(spec.shape), tol)
+    np.testing.assert_array_equal(got == 0.0, want == 0.0)

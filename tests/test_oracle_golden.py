@@ -11,7 +11,7 @@ import math
 import numpy as np
 import pytest
 
-from conftest import golden
+from conftest import GOLDEN as GOLDEN_DIR, golden
 from oracle import phasemask_oracle as orc
 from paper_1302_0120_b200.patterns import make_problem
 
@@ -132,3 +132,58 @@ def test_threaded_baseline_matches_serial_oracle():
             t.close()
         ref = orc.solve(p, m, 5, tag)["mask"]
         np.testing.assert_array_equal(mask, ref)
+
+
+def _np_cabs_formula(z):
+    """numpy's SIMD complex absolute value (numpy/_core/src/umath/
+    loops_unary_complex.dispatch.c.src): larger * sqrt(fma(r, r, 1)),
+    r = smaller / larger, with an exact fma (Fraction) and IEEE ops in the
+    array's precision. The CUDA path's np_cabs (csrc/pm_fft.cuh) restates it."""
+    from fractions import Fraction
+    fdt = np.float32 if z.dtype == np.complex64 else np.float64
+    out = np.empty(z.shape, fdt)
+    for i, v in enumerate(z.ravel()):
+        a, b = abs(v.real), abs(v.imag)
+        L, S = max(a, b), min(a, b)
+        r = fdt(0) if L == 0 else fdt(S / L)              # IEEE division in fdt
+        f = fdt(float(Fraction(float(r)) * Fraction(float(r)) + 1))   # fma, one rounding
+        out.flat[i] = fdt(np.sqrt(f) * L)
+    return out
+
+
+@pytest.mark.parametrize("dtype", [np.complex64, np.complex128])
+def test_numpy_complex_abs_is_the_simd_formula(dtype):
+    """The zero-branch decision of the reference is `np.abs(u) >= zero_tol`
+    (src/projections.py:49-53); np.abs is this formula, not hypot, bit for bit
+    (the GPU decides with the same formula)."""
+    rng = np.random.default_rng(11)
+    z = (rng.standard_normal(20000) + 1j * rng.standard_normal(20000)).astype(dtype)
+    z[::5] *= 1e-4
+    z[::7] = z[::7].real.astype(dtype)                    # exact axis values
+    z[:4] = [0, 1e-30, 3 + 4j, -2j]
+    np.testing.assert_array_equal(np.abs(z), _np_cabs_formula(z))
+    # and it is not hypot: some values differ by an ulp
+    assert (np.hypot(z.real, z.imag) != np.abs(z)).any()
+
+
+def test_oracle_divergence_outcomes_match_reference():
+    """The reference's outcome (normal return, SolveDivergedError or the
+    metrics' ValueError) on amplitudes scaled towards the float range, for
+    every case of tests/golden/divergence_outcomes.json (generated by running
+    the reference): the oracle reproduces each."""
+    import json
+    d = json.loads((GOLDEN_DIR / "divergence_outcomes.json").read_text())
+    for (n, ny, tag, c, rec, es), want in zip(d["cases"], d["outcomes"]):
+        if n > 128:
+            continue                                  # the 256^2 cases run on the GPU box (tests/test_gpu_divergence.py)
+        p, m = make_problem(n, d["spots"], d["seed"], n_y=ny)
+        p = p / p.max() * c
+        try:
+            with np.errstate(all="ignore"):
+                orc.solve(p, m, d["K"], tag, record_every=rec, early_stop_tol=es)
+            got = "ok"
+        except orc.Diverged as e:
+            got = f"div{e.iteration}"
+        except ValueError as e:
+            got = f"VE:{e}"
+        assert got == want, (n, ny, tag, c, rec, es)
