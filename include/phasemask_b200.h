@@ -23,7 +23,9 @@
  *    pm_last_error() returns the calling thread's last message.
  *  - "_device" variants take device pointers on the plan's device and run
  *    asynchronously on the plan's stream; the others take host pointers,
- *    copy through pinned staging and synchronise before returning.
+ *    copy with cudaMemcpyAsync straight from / into the caller's memory and
+ *    synchronise before returning (page-locked caller buffers copy at full
+ *    speed; pageable ones are staged by the CUDA driver).
  *  - No CPU fallback: without a CUDA device every compute call fails with
  *    PM_ERR_CUDA.
  */
@@ -150,6 +152,15 @@ int pm_norm2(int device, const void *data, long long count, int dtype, double *o
  * Replaces backends.deterministic_sum (src/backends.py:109-125).
  */
 int pm_sum(int device, const double *data, long long count, double *out);
+
+/*
+ * The reference's O(N^2) correctness oracle naive_dft (src/transform.py:56-81):
+ * the unitary DFT as the dense double sum W_rows X W_cols^T in fp64 on the
+ * device, for grids of at most 4096 pixels (NAIVE_DFT_MAX_PIXELS, :16; larger
+ * grids fail with PM_ERR_ARG and the reference's message). in / out:
+ * complex128 host arrays (n_y, n_x); direction PM_FORWARD | PM_INVERSE.
+ */
+int pm_naive_dft(int device, const void *in, int n_x, int n_y, int direction, void *out);
 
 /*
  * Phase extraction: out = mod(atan2(im, re), 2pi) in fp64, >= 2pi -> 0,

@@ -85,6 +85,7 @@ SIGNATURES = {
     "pm_norm2": (_I, [_I, _VP, _LL, _I, C.POINTER(_D)]),
     "pm_sum": (_I, [_I, _VP, _LL, C.POINTER(_D)]),
     "pm_phases": (_I, [_I, _VP, _LL, _I, _D, _VP]),
+    "pm_naive_dft": (_I, [_I, _VP, _I, _I, _I, _VP]),
     "pm_random_start": (_I, [_I, _VP, _LL, _I, _I, _VP, _VP]),
     "pm_recon_image": (_I, [_VP, _VP, _I, _VP, _D, _VP, _VP]),
     "pm_solve": (_I, [_VP, _VP, _VP, _VP, _I, C.POINTER(pm_params), _VP, _VP, _VP,
@@ -312,6 +313,14 @@ def phases(u: np.ndarray, zero_tol: float = 0.0, device: int = 0) -> np.ndarray:
     prec = 0 if a.dtype == np.complex64 else 1
     out = np.empty(a.shape, dtype=np.float64)
     check(load().pm_phases(device, ptr(a), a.size, prec, float(zero_tol), ptr(out)), "pm_phases")
+    return out
+
+
+def naive_dft(data: np.ndarray, direction: int, device: int = 0) -> np.ndarray:
+    """Dense fp64 unitary DFT of a (n_y, n_x) array on the device (pm_naive_dft)."""
+    a = np.ascontiguousarray(data, dtype=np.complex128)
+    out = np.empty_like(a)
+    check(load().pm_naive_dft(device, ptr(a), a.shape[1], a.shape[0], direction, ptr(out)), "pm_naive_dft")
     return out
 
 

@@ -185,6 +185,33 @@ __global__ void phases_kernel(const cx<T>* u, long long n, T tol, double* out) {
     }
 }
 
+// The reference's correctness oracle naive_dft (src/transform.py:56-81) on
+// the device: out = W_rows X W_cols^T with W[k][j] = exp(sign 2 pi i k j / n)
+// / sqrt(n), in fp64. One thread per output pixel, the double sum in a fixed
+// order; the phase of each term is reduced exactly (k j mod n) before sincospi.
+__global__ void naive_dft_kernel(const double2* x, int nx, int ny, double sign, double2* out) {
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= nx * ny) return;
+    const int r = idx / nx, c = idx % nx;
+    double re = 0.0, im = 0.0;
+    for (int a = 0; a < ny; ++a) {
+        const double fa = (double)((long long)r * a % ny) / ny;
+        double ta = 0.0, tb = 0.0;                        // (W_rows X)[r][b] W_cols[c][b] summed over b
+        for (int b = 0; b < nx; ++b) {
+            const double f = fa + (double)((long long)c * b % nx) / nx;
+            double sn, cs;
+            sincospi(2.0 * sign * f, &sn, &cs);
+            const double2 v = x[(size_t)a * nx + b];
+            ta += v.x * cs - v.y * sn;
+            tb += v.x * sn + v.y * cs;
+        }
+        re += ta;
+        im += tb;
+    }
+    const double s = 1.0 / (sqrt((double)nx) * sqrt((double)ny));
+    out[idx] = make_double2(re * s, im * s);
+}
+
 // Reconstructed intensity |F u|^2 (src/metrics.py:74-87): per mask (blockIdx.y)
 // fixed-partition partial sums and maxima of (double)|F u|^2, |.| taken in
 // the field precision and squared in fp64 as the reference does.
@@ -2287,6 +2314,35 @@ int pm_random_start(int device, const void* m, long long count, int batch, int p
     cudaFree(dout);
     if (rc != PM_OK) return rc;
     if (e != cudaSuccess) return cuda_err(e, "pm_random_start");
+    return PM_OK;
+}
+
+int pm_naive_dft(int device, const void* in, int n_x, int n_y, int direction, void* out) {
+    if (!in || !out || n_x < 1 || n_y < 1) return set_err(PM_ERR_ARG, "empty input");
+    if ((long long)n_x * n_y > 4096)
+        return set_err(PM_ERR_ARG, "grid with " + std::to_string((long long)n_x * n_y) +
+                                       " pixels too large for the O(N^2) oracle (limit 4096)");
+    if (direction != PM_FORWARD && direction != PM_INVERSE) return set_err(PM_ERR_ARG, "unknown direction");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return set_err(PM_ERR_CUDA, "no CUDA device available (phasemask_b200 has no CPU fallback)");
+    }
+    CK(cudaSetDevice(device));
+    const size_t bytes = (size_t)n_x * n_y * sizeof(double2);
+    void* d = nullptr;
+    CK(cudaMalloc(&d, 2 * bytes));
+    double2* din = (double2*)d;
+    double2* dout = din + (size_t)n_x * n_y;
+    cudaError_t e = cudaMemcpy(din, in, bytes, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) {
+        naive_dft_kernel<<<(n_x * n_y + 127) / 128, 128>>>(din, n_x, n_y, direction == PM_FORWARD ? -1.0 : 1.0,
+                                                           dout);
+        e = cudaGetLastError();
+        if (e == cudaSuccess) e = cudaMemcpy(out, dout, bytes, cudaMemcpyDeviceToHost);
+    }
+    cudaFree(d);
+    if (e != cudaSuccess) return cuda_err(e, "pm_naive_dft");
     return PM_OK;
 }
 

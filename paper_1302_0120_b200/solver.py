@@ -43,7 +43,8 @@ class SolveDivergedError(RuntimeError):
 
 
 def _default_device() -> int:
-    return int(os.environ.get("PM_DEVICE", os.environ.get("LOCAL_RANK", "0")))
+    from .transform import default_device
+    return default_device()
 
 
 @dataclass(frozen=True)
@@ -234,6 +235,13 @@ def solve(c: SlmConstraint, m: FourierConstraint, cfg: SolveConfig,
     on_record(record) fires for each recorded iteration; should_abort() is
     polled once per iteration for cooperative cancellation, as in the
     reference.
+
+    The physical-error metrics use the target energy sum(m^2) and intensity
+    m^2 of the precision-cast m, reduced on the device in a fixed order. The
+    reference squares the float64 m (src/solver.py:135-136); in SINGLE
+    precision the two differ by at most ~6e-8 relative (the float32 rounding
+    of m), far inside the fp32 record tolerance; in DOUBLE they differ only by
+    summation order.
     """
     spec = c.p.spec
     if m.m.spec != spec:
@@ -252,7 +260,9 @@ def solve(c: SlmConstraint, m: FourierConstraint, cfg: SolveConfig,
             raise PlanMismatchError(
                 f"field spec {spec.n_x}x{spec.n_y} does not match plan "
                 f"{provider.spec.n_x}x{provider.spec.n_y}")
-        device = getattr(provider, "device", device)
+        if cfg.device is None:
+            # an explicit SolveConfig.device wins; else the provider's (itself the process default)
+            device = getattr(provider, "device", device)
 
     prec = cfg.precision
     plan = get_plan(spec, prec, device)

@@ -24,6 +24,12 @@ class PlanMismatchError(ValueError):
     """Field spec or plane does not match the provider's plan (src/transform.py:19-20)."""
 
 
+def default_device() -> int:
+    """The process's CUDA device: PM_DEVICE, else LOCAL_RANK (one rank per GPU), else 0."""
+    import os
+    return int(os.environ.get("PM_DEVICE", os.environ.get("LOCAL_RANK", "0")))
+
+
 _plans: dict[tuple[int, int, int, int], _lib.Plan] = {}
 _plans_lock = threading.Lock()
 
@@ -58,11 +64,12 @@ class FftProvider:
     """
 
     def __init__(self, spec: GridSpec, precision: Precision = DOUBLE,
-                 fft_workers: int = 1, device: int = 0):
+                 fft_workers: int = 1, device: int | None = None):
         self.spec = spec
         self.precision = precision
         self.fft_workers = fft_workers
-        self.device = device
+        # None: the process default (PM_DEVICE, else LOCAL_RANK, else 0), as SolveConfig.device
+        self.device = default_device() if device is None else int(device)
 
     @property
     def plan(self) -> _lib.Plan:
@@ -96,3 +103,17 @@ def ifft2(data: np.ndarray, precision: Precision = DOUBLE, device: int = 0) -> n
     """Unitary inverse transform of a (n_y, n_x) or (batch, n_y, n_x) array."""
     spec = GridSpec(data.shape[-1], data.shape[-2])
     return get_plan(spec, precision, device).fft2(data, _lib.PM_INVERSE)
+
+
+def naive_dft(f: Field, direction: str = "forward") -> Field:
+    """The reference's textbook double-sum unitary DFT (src/transform.py:56-81),
+    always double precision, guarded to small grids: a correctness oracle, not
+    a production transform. Evaluated on the device (pm_naive_dft)."""
+    if f.spec.n > NAIVE_DFT_MAX_PIXELS:
+        raise ValueError(
+            f"grid with {f.spec.n} pixels too large for the O(N^2) oracle "
+            f"(limit {NAIVE_DFT_MAX_PIXELS})")
+    if direction not in ("forward", "inverse"):
+        raise ValueError(f"unknown direction {direction!r}")
+    out = _lib.naive_dft(f.data, _lib.PM_FORWARD if direction == "forward" else _lib.PM_INVERSE)
+    return Field(f.spec, out, FOURIER_PLANE if direction == "forward" else SLM_PLANE)

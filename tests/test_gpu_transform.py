@@ -151,3 +151,28 @@ def test_mixed_radix_transform_matches_scipy(nx, ny, tag, rng):
     assert orc.relative_l2(inv, x) <= tol
     if nx * ny <= 4096:
         assert np.abs(fwd - orc.naive_dft(x)).max() <= (1e-12 if tag == "double" else 1e-5)
+
+
+@pytest.mark.parametrize("nx,ny", [(8, 8), (16, 4), (64, 64), (60, 42)])
+def test_naive_dft_public_name_matches_reference_oracle(nx, ny):
+    """pm.naive_dft (the reference's src/transform.py:56-81, exported as in its
+    src/__init__.py:13) on the device: equal to the dense-matrix oracle and to
+    the provider's transform, both directions, fp64."""
+    rng = np.random.default_rng(nx * 100 + ny)
+    x = rng.standard_normal((ny, nx)) + 1j * rng.standard_normal((ny, nx))
+    spec = pm.GridSpec(nx, ny)
+    for d in ("forward", "inverse"):
+        plane = pm.grid.SLM_PLANE if d == "forward" else pm.grid.FOURIER_PLANE
+        got = pm.naive_dft(pm.Field(spec, x, plane), d)
+        assert got.domain_tag == (pm.grid.FOURIER_PLANE if d == "forward" else pm.grid.SLM_PLANE)
+        assert orc.relative_l2(got.data, orc.naive_dft(x, d)) <= 1e-13
+    prov = pm.FftProvider(spec)
+    assert orc.relative_l2(pm.naive_dft(pm.Field(spec, x)).data, prov.forward(pm.Field(spec, x)).data) <= 1e-12
+
+
+def test_naive_dft_guard_and_direction():
+    spec = pm.GridSpec(128, 64)
+    with pytest.raises(ValueError, match="too large for the O"):
+        pm.naive_dft(pm.Field(spec, np.zeros(spec.shape, complex)))
+    with pytest.raises(ValueError, match="unknown direction"):
+        pm.naive_dft(pm.Field(pm.GridSpec(4, 4), np.zeros((4, 4), complex)), "sideways")

@@ -148,3 +148,13 @@ def test_index_round_trip_property(n_x, n_y):
     a = np.arange(spec.n).reshape(spec.shape)
     j, k = n_x - 1, n_y - 1
     assert a[k, j] == spec.flatten_index(j, k)
+
+
+def test_naive_dft_is_a_public_name_with_the_reference_guard():
+    """The reference exports naive_dft (src/__init__.py:13); its size guard
+    (src/transform.py:67-70) is checked before any device work."""
+    import paper_1302_0120_b200 as pm
+    assert "naive_dft" in pm.__all__ and callable(pm.naive_dft)
+    spec = pm.GridSpec(128, 64)
+    with pytest.raises(ValueError, match="too large for the O"):
+        pm.naive_dft(pm.Field(spec, np.zeros(spec.shape, complex)))
