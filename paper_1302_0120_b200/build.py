@@ -84,6 +84,9 @@ def _units(build_dir):
             roll = int(os.environ.get("PM_ROLL", "0"))
             pf = int(os.environ.get("PM_PF", "0"))
             xd = os.environ.get("PM_XDEFS", "").split()        # experiment macros (-DNAME=V ...)
+            only = os.environ.get("PM_XONLY")                  # e.g. "f32_10,f64_8": macros for these units only
+            if only and f"{tag}_{lg}" not in only.split(","):
+                xd = []
             xs = "".join("_" + d.lstrip("-D").replace("=", "") for d in xd)
             units.append((CSRC / "pm_inst.cu", build_dir / f"pm_inst_{tag}_{lg}_{row}{col}_{nt}_r{roll}_p{pf}{xs}.o",
                           [f"-DPM_F64={f64}", f"-DPM_LG={lg}", f"-DPM_LGR_ROW={row}", f"-DPM_LGR_COL={col}",

@@ -381,6 +381,52 @@ template <> __device__ __forceinline__ double min_normal<double>() { return 2.22
 // Cross-CTA field loads bypass L1 (the field is rewritten between phases).
 template <typename C> __device__ __forceinline__ C ld_field(const C* p) { return __ldcg(p); }
 
+// Fine-grained clock64 stamps inside tasks (experiments only: PM_FINE=1):
+// CTA thread 0 writes the SM clock into slots 128.. of its stamp row.
+#ifndef PM_FINE
+#define PM_FINE 0
+#endif
+struct FineState {
+    unsigned long long* p;
+    int i;
+};
+__device__ __forceinline__ FineState& fine_state() {
+    __shared__ FineState s;
+    return s;
+}
+__device__ __forceinline__ void fine_init(unsigned long long* stamps) {
+    if constexpr (PM_FINE) {
+        if (threadIdx.x == 0) {
+            fine_state().p = stamps ? stamps + (size_t)blockIdx.x * 256 + 128 : nullptr;
+            fine_state().i = 0;
+        }
+        __syncthreads();
+    }
+}
+__device__ __forceinline__ void fine_stamp(int id) {
+    if constexpr (PM_FINE) {
+        if (threadIdx.x == 0) {
+            FineState& s = fine_state();
+            if (s.p && s.i < 126) {
+                s.p[s.i] = id;
+                s.p[s.i + 1] = clock64();
+                s.i += 2;
+            }
+        }
+    }
+}
+// A stamp taken once value x has arrived (forces the scoreboard wait).
+template <typename V>
+__device__ __forceinline__ void fine_stamp_after(V x, int id) {
+    if constexpr (PM_FINE) {
+        if (threadIdx.x == 0) {
+            FineState& s = fine_state();
+            if (s.p && x.x == 1.2345e-30f && x.y == 5.4321e-30f) s.p[127] = 0;
+        }
+        fine_stamp(id);
+    }
+}
+
 // ------------------------------------------------------------------ tasks
 // Scaling convention: the unitary factor S = 1/sqrt(n_x n_y) is applied
 // once per half iteration, at the projections, as the targets' scale: P_S
@@ -546,6 +592,10 @@ __device__ __forceinline__ void row_task(const RowArgs<T>& a, int b, int row, in
     const bool act = inb && live;
     cx<T>* f = a.field + b * N + (size_t)row * a.nx + j;
     const T* p = a.p + b * a.p_stride + (size_t)row * a.nx + j;
+    // the mask's zero tolerance, loaded with the field (its L2 latency then
+    // overlaps the loads instead of stalling the projection)
+    const double thr_b = (ALG != 1 && a.mode == kRowGS) ? __ldcg(a.thr_p + b)
+                       : (ALG != 0 && (a.mode == kRowRaar || a.mode == kRowProbe)) ? __ldcg(a.thr_x + b) : 0.0;
     cx<T> v[F::R];
     if (tile) {
         cp_async_wait<0>();
@@ -557,6 +607,7 @@ __device__ __forceinline__ void row_task(const RowArgs<T>& a, int b, int row, in
 #pragma unroll
         for (int k = 0; k < F::R; ++k) v[k] = inb ? ld_field(f + F::TG * k) : mk<T>(T(0), T(0));   // conj(z')
     }
+    fine_stamp_after(v[F::R - 1], 11);   // row: loads landed
     if constexpr (PS) {
         if (inb && a.mode != kRowInit && stage_p) stage_tile<T, 1, (1 << LG_L), F::TG>(ps, p - j, 0, j);
         if constexpr (XS) {
@@ -581,7 +632,9 @@ __device__ __forceinline__ void row_task(const RowArgs<T>& a, int b, int row, in
 #pragma unroll
 #endif
     for (int h = 0; h < trips; ++h) {
+        if (h) fine_stamp_after(v[F::R - 1], 14);               // row: after the projection
         fft1d<T, LG_L, LG_R, -1, TS>(v, sm, tw, j, sync);     // h = 0: y = conj(v'); h = 1: w' = RowFFT(u)
+        fine_stamp_after(v[F::R - 1], 12 + h);   // row: after FFT 1 / 2
         if (h) break;
         if constexpr (PS) {
             cp_async_wait<1>();                      // p of this task (the prefetch may stay in flight)
@@ -590,7 +643,7 @@ __device__ __forceinline__ void row_task(const RowArgs<T>& a, int b, int row, in
         if (ALG != 1 && a.mode == kRowGS) {
             // S u = S P_S v = conj(P_S(y; S p)) (src/projections.py:69-74): y = conj(v) is
             // the normalised field, decided against zero_tol itself; p arrives pre-scaled by S
-            const ZThr<T> z = zthr<T>(T(a.thr_p[b]));
+            const ZThr<T> z = zthr<T>(T(thr_b));
             auto t_of = [&](int k) -> T { return inb ? p_at(k) : T(0); };
             auto keep = [](int, cx<T>, cx<T> o) { return o; };
             // false: v = F^-1 v^ was not finite (the reference's Field check)
@@ -612,7 +665,7 @@ __device__ __forceinline__ void row_task(const RowArgs<T>& a, int b, int row, in
             const int gi = a.it - 1;
             const bool gneed = act && gi >= 1 && gap_needed(a.ctl, gi) && __ldcg(&a.st[b].decided) < gi;
             const bool upd = a.mode == kRowRaar;
-            const ZThr<T> z = zthr<T>(T(a.thr_x[b]));
+            const ZThr<T> z = zthr<T>(T(thr_b));
             cx<T>* xp = a.x + b * N + (size_t)row * a.nx + j;
             double g2 = 0.0, e2 = 0.0;
 #pragma unroll
@@ -644,6 +697,7 @@ __device__ __forceinline__ void row_task(const RowArgs<T>& a, int b, int row, in
 #pragma unroll
         for (int k = 0; k < F::R; ++k) o[F::TG * k] = v[k];
     }
+    fine_stamp(15);   // row: stores issued
 }
 
 // Best-approximation pair for one row: v* = P_M u_K = S * RowIFFT(z')
@@ -730,6 +784,9 @@ __device__ __forceinline__ void col_task(const ColArgs<T>& a, int b, int col0, i
     const T* m = a.m + b * a.m_stride + (size_t)j * nx + col0 + c;
     const bool act = live;
     acc[0] = acc[1] = acc[2] = 0.0;
+    // per-mask constants, loaded with the field (see row_task)
+    const double thr_b = a.mode == 2 ? __ldcg(a.thr_m + b) : 0.0;
+    const double esc_b = (a.mode == 2 && !a.raar && a.u_iter >= 1 && a.escale) ? __ldcg(a.escale + b) : 0.0;
 
     cx<T> v[F::R];
     if (a.mode == 0) {
@@ -753,6 +810,7 @@ __device__ __forceinline__ void col_task(const ColArgs<T>& a, int b, int col0, i
         const cx<T>* src = (a.mode == 2 ? a.in : a.field) + (f - a.field);
 #pragma unroll
         for (int k = 0; k < F::R; ++k) v[k] = ld_field(src + k * rs);
+        if (a.mode == 2) fine_stamp_after(v[F::R - 1], 21);          // col: loads landed
         if (a.mode == 1) {
 #pragma unroll
             for (int k = 0; k < F::R; ++k) v[k] = cscale_conj(v[k], a.scale);   // complex start: conj in, conj(IFFT) out
@@ -793,10 +851,12 @@ __device__ __forceinline__ void col_task(const ColArgs<T>& a, int b, int col0, i
 #pragma unroll
 #endif
     for (int h = 0; h < trips; ++h) {
+        if (h) fine_stamp_after(v[F::R - 1], 24);                    // col: after metrics + projection
         fft1d<T, LG_L, LG_R, -1, TS>(v, sm, tw, j, SyncBlock{});   // h = 0: ColFFT(w'); h = 1: conj(z')
+        fine_stamp_after(v[F::R - 1], 22 + h);                       // col: after FFT 1 / 2
         if (h) break;
         // u^ = F(u) = ColFFT(w''), w'' = S RowFFT(u): normalised, decided against zero_tol itself
-        const ZThr<T> z = zthr<T>(T(a.thr_m[b]));
+        const ZThr<T> z = zthr<T>(T(thr_b));
         T mm[F::R];
         if (TM && tma.mt) {
             mbar_wait(&tma.bars[1], tma.parity);
@@ -838,7 +898,7 @@ __device__ __forceinline__ void col_task(const ColArgs<T>& a, int b, int col0, i
                 sc = s_sc;
                 __syncthreads();
             } else {
-                sc = a.escale[b];
+                sc = esc_b;
             }
 #pragma unroll
             for (int k = 0; k < F::R; ++k) {
@@ -859,12 +919,17 @@ __device__ __forceinline__ void col_task(const ColArgs<T>& a, int b, int col0, i
         // conj(v^), v^ = replace_m(u^); G(u) = ||P_S u - P_M u|| = ||u^ - v^|| (Parseval; u is on S);
         // the column FFT of S conj(v^) follows
         auto t_of = [&](int k) -> T { return mm[k]; };
-        auto epi = [&](int, cx<T> u, cx<T> vh) -> cx<T> {
-            if (gneed) g2 += norm_sq_d(csub(u, cconj(vh)));
+        auto epi_gap = [&](int, cx<T> u, cx<T> vh) -> cx<T> {
+            g2 += norm_sq_d(csub(u, cconj(vh)));
             return cscale(vh, a.scale);
         };
-        // false: u^ = F(u_{u_iter}) was not finite, the reference's Field check of iteration u_iter + 1
-        const bool fin = z.ftz ? project_regs<true, true>(v, z, t_of, epi) : project_regs<true, false>(v, z, t_of, epi);
+        auto epi = [&](int, cx<T>, cx<T> vh) -> cx<T> { return cscale(vh, a.scale); };
+        // false: u^ = F(u_{u_iter}) was not finite, the reference's Field check of iteration u_iter + 1.
+        // Iterations without a gap take a copy of the loop with no fp64 work in it (predicated
+        // conversions and squares would still take issue slots).
+        bool fin;
+        if (gneed) fin = z.ftz ? project_regs<true, true>(v, z, t_of, epi_gap) : project_regs<true, false>(v, z, t_of, epi_gap);
+        else fin = z.ftz ? project_regs<true, true>(v, z, t_of, epi) : project_regs<true, false>(v, z, t_of, epi);
         if (act && !fin) first_bad(&a.st[b].bad, a.u_iter + 1);
         acc[0] = act ? g2 : 0.0;
     }
@@ -872,6 +937,7 @@ __device__ __forceinline__ void col_task(const ColArgs<T>& a, int b, int col0, i
 #pragma unroll
         for (int k = 0; k < F::R; ++k) f[k * rs] = v[k];
     }
+    fine_stamp(25);                                                     // col: stores issued
 }
 
 // Fixed-order CTA sum of NV accumulators; thread 0 gets the totals.
@@ -1444,6 +1510,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const __grid_co
     int si = 0;
     unsigned epoch = 0;
     stamp(a.stamps, si);
+    fine_init(a.stamps);
     const Tables<T> tw = load_tables<T, LG, LGR_R, LGR_C, TV>(a.row, a.col, smraw);
     Resident rs{a.res != 0 && (ALG == 1 ? L::RES_RAAR : L::RES_GS), false, false,
                 L::BYTES_T + (ALG == 1 ? L::XSE : 0), L::BYTES_T + (ALG == 1 ? L::XSE : 0) + L::ST};
@@ -1512,17 +1579,22 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const __grid_co
             RowArgs<T> r = a.row;
             r.mode = kRowGS;
             r.it = it;
+            fine_stamp(1);
             row_phase<T, LG, LGR_R, LGR_C, ALG, TV>(r, B, smraw, tw, &rs);   // u_it, w_it
             stamp(a.stamps, si);
+            fine_stamp(2);
             grid_sync(a.bar, epoch);
             stamp(a.stamps, si);
+            fine_stamp(3);
             ColArgs<T> c = a.col;
             c.mode = 2;
             c.u_iter = it;
             col_phase<T, LG, LGR_R, LGR_C, TV>(c, B, smraw, tw, ct, &rs);    // metrics of u_it, z_{it+1}
             stamp(a.stamps, si);
+            fine_stamp(4);
             grid_sync(a.bar, epoch);
             stamp(a.stamps, si);
+            fine_stamp(5);
             // decisions: records, early stop, max_iters, and the last iterate
             // of this launch (the stepping API reads state after every launch)
             if (gap_needed(c.ctl, it) || it >= c.ctl.max_iters || it == a.it_end - 1) decide_phase<T, LG, LGR_C>(c, B);
