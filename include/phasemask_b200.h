@@ -268,6 +268,44 @@ int pm_solve_records(pm_plan *plan, int first_iter, int last_iter, double *gap,
                      int *diverged_iter);
 int pm_solve_finish(pm_plan *plan, int abort, pm_result *result);
 
+/*
+ * Streamed form for per-iteration host callbacks without a host round trip
+ * per launch (src/solver.py:188-199; SURVEY.md §8(b) record_ring /
+ * abort_flag). pm_solve_async enqueues the whole single-mask solve (one
+ * persistent launch on the fused path) and returns at once; the device
+ * publishes every decided iteration into a host-mapped record ring, and with
+ * lockstep != 0 it waits after each one for the host's verdict
+ * (should_abort), answered through a host-mapped word. The caller then:
+ *   for it = 1..: pm_solve_next(it) -> on_record (flags & RECORDED);
+ *     stop at flags & STOP (or flags == 0: the solve ended);
+ *     lockstep and not (EARLY | DIVERGED): pm_solve_answer(it, should_abort())
+ *   pm_solve_wait -> the same outputs / errors as pm_solve.
+ * `result` names the wanted outputs at pm_solve_async (its host arrays are
+ * written by pm_solve_wait). pm_solve_next blocks without holding the GIL
+ * of a ctypes caller; a device that gets no verdict for 30 s stops (TIMEOUT).
+ */
+typedef struct pm_record {
+    double gap, err_lit, err_dark;   /* ConvergenceRecord fields (when RECORDED) */
+    int    iter;                     /* 1-based iteration                        */
+    int    flags;                    /* PM_REC_* bits                            */
+} pm_record;
+#define PM_REC_PUBLISHED 1   /* slot valid                                          */
+#define PM_REC_RECORDED  2   /* a recorded iteration: on_record                     */
+#define PM_REC_EARLY     4   /* early stop here (the reference skips should_abort)  */
+#define PM_REC_DIVERGED  8   /* non-finite iterate (pm_solve_wait fails)            */
+#define PM_REC_STOP      16  /* last iteration of the solve                         */
+#define PM_REC_ABORTED   32  /* the host's abort took effect here                   */
+#define PM_REC_TIMEOUT   64  /* no verdict within 30 s: stopped here; a lockstep
+                                callback must not wait for work on the solving
+                                device (the solve occupies every SM)            */
+int pm_solve_async(pm_plan *plan, const void *p, const void *m, const void *m_init,
+                   const pm_params *params, const double *zero_tol_p,
+                   const double *zero_tol_m, const double *energy, int lockstep,
+                   pm_result *result);
+int pm_solve_next(pm_plan *plan, int iter, pm_record *record);
+int pm_solve_answer(pm_plan *plan, int iter, int abort);
+int pm_solve_wait(pm_plan *plan, pm_result *result);
+
 /* ------------------------------------------------------------ measurement */
 
 /*

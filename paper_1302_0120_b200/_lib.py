@@ -62,6 +62,20 @@ class pm_result(C.Structure):
     ]
 
 
+class pm_record(C.Structure):
+    _fields_ = [
+        ("gap", C.c_double),
+        ("err_lit", C.c_double),
+        ("err_dark", C.c_double),
+        ("iter", C.c_int),
+        ("flags", C.c_int),
+    ]
+
+
+PM_REC_PUBLISHED, PM_REC_RECORDED, PM_REC_EARLY, PM_REC_DIVERGED, PM_REC_STOP, PM_REC_ABORTED = 1, 2, 4, 8, 16, 32
+PM_REC_TIMEOUT = 64
+
+
 # name -> (restype, argtypes); mirrors include/phasemask_b200.h one to one
 _VP, _I, _D, _LL = C.c_void_p, C.c_int, C.c_double, C.c_longlong
 SIGNATURES = {
@@ -96,6 +110,10 @@ SIGNATURES = {
     "pm_solve_step": (_I, [_VP, _I, C.POINTER(_I)]),
     "pm_solve_records": (_I, [_VP, _I, _I, _VP, _VP, _VP, _VP, _VP]),
     "pm_solve_finish": (_I, [_VP, _I, C.POINTER(pm_result)]),
+    "pm_solve_async": (_I, [_VP, _VP, _VP, _VP, C.POINTER(pm_params), _VP, _VP, _VP, _I, C.POINTER(pm_result)]),
+    "pm_solve_next": (_I, [_VP, _I, C.POINTER(pm_record)]),
+    "pm_solve_answer": (_I, [_VP, _I, _I]),
+    "pm_solve_wait": (_I, [_VP, C.POINTER(pm_result)]),
     "pm_time_sweep": (_I, [_VP, _I, _I, _I, C.POINTER(C.c_float)]),
     "pm_measure_copy": (_I, [_I, _LL, _I, C.POINTER(_D)]),
     "pm_debug_phase_stamps": (_I, [_VP, _I, _VP, _I]),

@@ -13,6 +13,8 @@
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <atomic>
+#include <cstddef>
 #include <set>
 #include <string>
 #include <vector>
@@ -556,6 +558,12 @@ struct pm_plan {
     long long launches = 0;
     GridBar* bar = nullptr;           // grid barrier of the persistent kernel
     unsigned long long* stamps = nullptr;  // optional phase timestamps (pm_debug_phase_stamps)
+    // streamed decisions of a callback solve (pm_solve_async): host-mapped
+    RingSlot* ring_h = nullptr;       // [ring_cap] host view
+    RingSlot* ring_d = nullptr;       // device view
+    int* hostw_h = nullptr;           // {acknowledged iteration, abort request} host view
+    int* hostw_d = nullptr;
+    int ring_cap = 0;
     int solve_grid = 0;               // CTAs of the persistent kernel (0: not available)
     int solve_grid_tma = 0;           // CTAs of its TMA variant (0: not available)
     int path = 0;                     // 0 auto, 1 persistent, 2 sweep graph
@@ -582,10 +590,28 @@ struct pm_plan {
         std::vector<double> h_tolp, h_thrp, h_thrm, h_thrms, h_en, h_thrx;
         bool energy_on_device = false;
         bool tol_on_device = false;
+        bool ring = false;            // decisions streamed to ring_h (pm_solve_async)
+        bool lockstep = false;        // and each one waits for the host's verdict
     } s;
 };
 
 namespace {
+
+// Run control of the session: the reference's loop parameters plus the
+// record ring of a callback solve (pm_solve_async).
+SolveCtl make_ctl(const pm_plan* pl) {
+    const pm_params& prm = pl->s.prm;
+    SolveCtl c;
+    c.max_iters = prm.max_iters;
+    c.record_every = prm.record_every;
+    c.early_tol = prm.early_stop_tol;
+    c.t_lit = prm.t_lit;
+    c.t_dark = prm.t_dark;
+    c.ring = pl->s.ring ? pl->ring_d : nullptr;
+    c.host = pl->s.ring ? (volatile int*)pl->hostw_d : nullptr;
+    c.lockstep = (pl->s.ring && pl->s.lockstep) ? 1 : 0;
+    return c;
+}
 
 RowCfg row_config(const pm_plan* pl) {
     const AxisShape& k = kset(pl->prec, pl->lgx).row;
@@ -783,11 +809,7 @@ RowArgs<T> row_args(pm_plan* pl, int mode, int it) {
     a.thr_x = pl->thrx;
     a.rpart = pl->rpart;
     a.wpr = row_wpr(pl);
-    a.ctl.max_iters = prm.max_iters;
-    a.ctl.record_every = prm.record_every;
-    a.ctl.early_tol = prm.early_stop_tol;
-    a.ctl.t_lit = prm.t_lit;
-    a.ctl.t_dark = prm.t_dark;
+    a.ctl = make_ctl(pl);
     a.hist = pl->hist;
     a.hist_stride = pl->hist_cap;
     a.cpart = pl->part;
@@ -820,11 +842,7 @@ FinalArgs<T> final_args(pm_plan* pl) {
     a.thr_x = pl->thrx;
     a.rpart = pl->rpart;
     a.wpr = row_wpr(pl);
-    a.ctl.max_iters = prm.max_iters;
-    a.ctl.record_every = prm.record_every;
-    a.ctl.early_tol = prm.early_stop_tol;
-    a.ctl.t_lit = prm.t_lit;
-    a.ctl.t_dark = prm.t_dark;
+    a.ctl = make_ctl(pl);
     return a;
 }
 
@@ -852,11 +870,7 @@ ColArgs<T> col_args(pm_plan* pl, int mode, int u_iter) {
     a.escale = pl->escale;
     a.mode = mode;
     a.u_iter = u_iter;
-    a.ctl.max_iters = prm.max_iters;
-    a.ctl.record_every = prm.record_every;
-    a.ctl.early_tol = prm.early_stop_tol;
-    a.ctl.t_lit = prm.t_lit;
-    a.ctl.t_dark = prm.t_dark;
+    a.ctl = make_ctl(pl);
     a.st = pl->st;
     a.hist = pl->hist;
     a.hist_stride = pl->hist_cap;
@@ -1178,13 +1192,8 @@ int gen_elem_blocks(const pm_plan* pl) {
 }
 
 GenSolveArgs gen_args(pm_plan* pl) {
-    const pm_params& prm = pl->s.prm;
     GenSolveArgs g;
-    g.ctl.max_iters = prm.max_iters;
-    g.ctl.record_every = prm.record_every;
-    g.ctl.early_tol = prm.early_stop_tol;
-    g.ctl.t_lit = prm.t_lit;
-    g.ctl.t_dark = prm.t_dark;
+    g.ctl = make_ctl(pl);
     g.st = pl->st;
     g.hist = pl->hist;
     g.hist_stride = pl->hist_cap;
@@ -1716,7 +1725,8 @@ std::string graph_key(const pm_plan* pl) {
     snprintf(buf, sizeof buf, "%d|%d|%d|%d|%a|%a|%a|%d|%d|%a|%p|%p|%lld|%p|%p|%p|%p|%d", s.batch,
              s.prm.max_iters, s.prm.record_every, s.prm.init_complex, s.prm.early_stop_tol,
              s.prm.t_lit, s.prm.t_dark, s.prm.p_per_mask, s.prm.algorithm, s.prm.beta, s.p, s.m,
-             s.p_stride, s.phases, s.levels, s.ustar, s.vstar, (int)s.tol_on_device * 2 + (int)s.energy_on_device);
+             s.p_stride, s.phases, s.levels, s.ustar, s.vstar,
+             (int)s.tol_on_device * 2 + (int)s.energy_on_device + 4 * (int)s.ring + 8 * (int)s.lockstep);
     return buf;
 }
 
@@ -1967,6 +1977,8 @@ int pm_plan_destroy(pm_plan* pl) {
     if (pl->red) cudaFree(pl->red);
     if (pl->bar) cudaFree(pl->bar);
     if (pl->stamps) cudaFree(pl->stamps);
+    if (pl->ring_h) cudaFreeHost(pl->ring_h);
+    if (pl->hostw_h) cudaFreeHost(pl->hostw_h);
     if (pl->ev0) cudaEventDestroy(pl->ev0);
     if (pl->ev1) cudaEventDestroy(pl->ev1);
     if (pl->own_stream && pl->stream) cudaStreamDestroy(pl->stream);
@@ -2380,13 +2392,14 @@ int pm_phases(int device, const void* u, long long count, int precision, double 
 }
 
 // ---------------------------------------------------------------- solve
-static int solve_core(pm_plan* pl, const void* d_p, const void* d_m, const void* d_init, int batch,
-                      const pm_params* prm, const double* tol_p, const double* tol_m,
-                      const double* energy, pm_result* res, bool host_io) {
+static int solve_enqueue(pm_plan* pl, const void* d_p, const void* d_m, const void* d_init, int batch,
+                         const pm_params* prm, const double* tol_p, const double* tol_m,
+                         const double* energy, pm_result* res, bool host_io, int ring = 0, int lockstep = 0) {
     if (!tol_p != !tol_m) return set_err(PM_ERR_ARG, "tolerance arrays: pass both or neither");
     CKR(session_setup(pl, d_p, d_m, batch, prm, tol_p, tol_m, energy));
     auto& s = pl->s;
-    const size_t N = pl->N;
+    s.ring = ring != 0;
+    s.lockstep = ring && lockstep;
     CKR(stage_start(pl, d_init, host_io ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice));
     if (host_io) {
         CKR(ensure_outputs(pl, res && res->phases, res && res->levels, res && res->u_star, res && res->v_star));
@@ -2403,6 +2416,15 @@ static int solve_core(pm_plan* pl, const void* d_p, const void* d_m, const void*
     CK(cudaEventRecord(pl->ev0, pl->stream));
     CKR(enqueue_full_solve(pl));
     CK(cudaEventRecord(pl->ev1, pl->stream));
+    return PM_OK;
+}
+
+// Outputs of an enqueued solve: host copies, records, state, the reference's errors.
+static int solve_collect(pm_plan* pl, pm_result* res, bool host_io) {
+    auto& s = pl->s;
+    const size_t N = pl->N;
+    const int batch = s.batch;
+    const pm_params* prm = &s.prm;
     if (host_io && res) {
         if (res->phases)
             CK(cudaMemcpyAsync(res->phases, pl->phases, batch * N * sizeof(double), cudaMemcpyDeviceToHost,
@@ -2424,9 +2446,17 @@ static int solve_core(pm_plan* pl, const void* d_p, const void* d_m, const void*
         if (res->device_ms) CK(cudaEventElapsedTime(res->device_ms, pl->ev0, pl->ev1));
     }
     s.active = false;
+    s.ring = s.lockstep = false;
     CKR(zero_error(zero));
     if (any_diverged(div)) return set_err(PM_ERR_DIVERGED, "non-finite values during the iteration");
     return PM_OK;
+}
+
+static int solve_core(pm_plan* pl, const void* d_p, const void* d_m, const void* d_init, int batch,
+                      const pm_params* prm, const double* tol_p, const double* tol_m,
+                      const double* energy, pm_result* res, bool host_io) {
+    CKR(solve_enqueue(pl, d_p, d_m, d_init, batch, prm, tol_p, tol_m, energy, res, host_io));
+    return solve_collect(pl, res, host_io);
 }
 
 int pm_solve(pm_plan* pl, const void* p, const void* m, const void* m_init, int batch,
@@ -2451,6 +2481,94 @@ int pm_solve_device(pm_plan* pl, const void* d_p, const void* d_m, const void* d
     if (!d_p || !d_m) return set_err(PM_ERR_ARG, "null p or m");
     std::lock_guard<std::mutex> lk(pl->mu);
     return solve_core(pl, d_p, d_m, d_m_init, batch, prm, tol_p, tol_m, energy, res, false);
+}
+
+static_assert(sizeof(RingSlot) == sizeof(pm_record) && offsetof(RingSlot, flags) == offsetof(pm_record, flags),
+              "pm_record mirrors the device's RingSlot");
+static_assert(kRecPublished == PM_REC_PUBLISHED && kRecRecorded == PM_REC_RECORDED && kRecEarly == PM_REC_EARLY &&
+                  kRecDiverged == PM_REC_DIVERGED && kRecStop == PM_REC_STOP && kRecAborted == PM_REC_ABORTED &&
+                  kRecTimeout == PM_REC_TIMEOUT,
+              "record flags");
+
+int pm_solve_async(pm_plan* pl, const void* p, const void* m, const void* m_init, const pm_params* prm,
+                   const double* tol_p, const double* tol_m, const double* energy, int lockstep,
+                   pm_result* res) {
+    CKR(check_plan(pl));
+    if (!p || !m) return set_err(PM_ERR_ARG, "null p or m");
+    CKR(validate_params(prm, 1));
+    std::lock_guard<std::mutex> lk(pl->mu);
+    CKR(ensure_capacity(pl, 1, prm->max_iters));
+    const int K = prm->max_iters;
+    if (pl->ring_cap < K) {
+        // mapped host memory, written by the device and polled by pm_solve_next
+        CK(cudaStreamSynchronize(pl->stream));
+        drop_graphs(pl);                       // captured solves hold the old ring's address
+        if (pl->ring_h) cudaFreeHost(pl->ring_h);
+        pl->ring_h = nullptr;
+        pl->ring_cap = 0;
+        CK(cudaHostAlloc((void**)&pl->ring_h, (size_t)K * sizeof(RingSlot), cudaHostAllocMapped));
+        CK(cudaHostGetDevicePointer((void**)&pl->ring_d, pl->ring_h, 0));
+        if (!pl->hostw_h) {
+            CK(cudaHostAlloc((void**)&pl->hostw_h, 2 * sizeof(int), cudaHostAllocMapped));
+            CK(cudaHostGetDevicePointer((void**)&pl->hostw_d, pl->hostw_h, 0));
+        }
+        pl->ring_cap = K;
+    }
+    CK(cudaStreamSynchronize(pl->stream));     // the previous solve no longer reads the ring
+    std::memset(pl->ring_h, 0, (size_t)K * sizeof(RingSlot));
+    ((volatile int*)pl->hostw_h)[0] = 0;
+    ((volatile int*)pl->hostw_h)[1] = 0;
+    const size_t N = pl->N;
+    CK(cudaMemcpyAsync(pl->pbuf, p, N * pl->rsz, cudaMemcpyHostToDevice, pl->stream));
+    CK(cudaMemcpyAsync(pl->mbuf, m, N * pl->rsz, cudaMemcpyHostToDevice, pl->stream));
+    return solve_enqueue(pl, pl->pbuf, pl->mbuf, m_init, 1, prm, tol_p, tol_m, energy, res, true, 1, lockstep);
+}
+
+int pm_solve_next(pm_plan* pl, int iter, pm_record* out) {
+    CKR(check_plan(pl));
+    if (!out) return set_err(PM_ERR_ARG, "null record");
+    const auto& s = pl->s;
+    if (!s.active || !s.ring) return set_err(PM_ERR_ARG, "no streamed solve in progress (pm_solve_async)");
+    if (iter < 1 || iter > s.prm.max_iters) return set_err(PM_ERR_ARG, "iteration out of range");
+    volatile RingSlot* r = (volatile RingSlot*)pl->ring_h + (iter - 1);
+    for (unsigned spin = 0;; ++spin) {
+        if (r->flags & kRecPublished) break;
+        if ((spin & 1023) == 1023) {
+            const cudaError_t e = cudaStreamQuery(pl->stream);
+            if (e != cudaErrorNotReady) {
+                if (r->flags & kRecPublished) break;
+                out->flags = 0;                  // the solve ended before this iteration
+                if (e != cudaSuccess) return cuda_err(e, "streamed solve");
+                return PM_OK;
+            }
+        }
+#if defined(__x86_64__)
+        __builtin_ia32_pause();
+#endif
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
+    out->gap = r->gap;
+    out->err_lit = r->err_lit;
+    out->err_dark = r->err_dark;
+    out->iter = r->iter;
+    out->flags = r->flags;
+    return PM_OK;
+}
+
+int pm_solve_answer(pm_plan* pl, int iter, int abort) {
+    CKR(check_plan(pl));
+    if (!pl->s.active || !pl->s.lockstep) return set_err(PM_ERR_ARG, "no lockstep solve in progress");
+    volatile int* w = (volatile int*)pl->hostw_h;
+    if (abort) w[1] = 1;
+    else w[0] = iter;
+    return PM_OK;
+}
+
+int pm_solve_wait(pm_plan* pl, pm_result* res) {
+    CKR(check_plan(pl));
+    std::lock_guard<std::mutex> lk(pl->mu);
+    if (!pl->s.active || !pl->s.ring) return set_err(PM_ERR_ARG, "no streamed solve in progress (pm_solve_async)");
+    return solve_collect(pl, res, true);
 }
 
 int pm_solve_begin(pm_plan* pl, const void* p, const void* m, const void* m_init, int batch,

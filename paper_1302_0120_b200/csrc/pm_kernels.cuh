@@ -61,11 +61,32 @@ struct MaskState {
     double pend_lit, pend_dark;   // RAAR, sweep path: physical error of the last column sweep's iterate
 };
 
+// One decided iteration, published to host-mapped memory for the host's
+// callbacks (src/solver.py:188-199: on_record per record, should_abort per
+// iteration). `flags` is written last, after a system-scope fence.
+struct RingSlot {
+    double gap, err_lit, err_dark;
+    int iter;
+    int flags;          // kRec* bits
+};
+enum : int {
+    kRecPublished = 1,  // slot valid
+    kRecRecorded = 2,   // a ConvergenceRecord of this iteration (on_record)
+    kRecEarly = 4,      // early stop at this iteration: the reference breaks before should_abort
+    kRecDiverged = 8,   // the iterate went non-finite (the reference raises)
+    kRecStop = 16,      // last iteration of the solve (early stop, max_iters, divergence or abort)
+    kRecAborted = 32,   // the host's abort took effect here
+    kRecTimeout = 64,   // no verdict within 30 s: stopped here, the solve fails
+};
+
 struct SolveCtl {
     int max_iters;
     int record_every;
     double early_tol;   // < 0: early stopping off
     double t_lit, t_dark;
+    RingSlot* ring;     // host-mapped [max_iters] (device view), null: no streaming (single mask)
+    volatile int* host; // host-mapped {acknowledged iteration, abort request}
+    int lockstep;       // every iteration waits for the host's verdict (should_abort)
 };
 
 // Iterate i needs its gap: recorded, or early stopping is on (src/solver.py:173-174).
@@ -279,13 +300,52 @@ __device__ __forceinline__ void decide(MaskState* st, double* hist_row, const So
         hist_row[0] = g; hist_row[1] = tot[1]; hist_row[2] = tot[2]; hist_row[3] = 1.0;
         st->n_records += 1;
     }
+    bool early = false;
     if (ctl.early_tol >= 0.0) {
-        if (st->have_prev && g > 0.0 && fabs(g - st->prev_gap) <= ctl.early_tol * g) stop = 1;
+        if (st->have_prev && g > 0.0 && fabs(g - st->prev_gap) <= ctl.early_tol * g) stop = 1, early = true;
         st->prev_gap = g;
         st->have_prev = 1;
     }
     if (i >= ctl.max_iters) stop = 1;
     st->decided = i;
+    if (ctl.ring) {
+        // stream the decision to the host; with lockstep, wait for its verdict
+        // (should_abort, polled once per iteration after on_record, unless the
+        // iteration stopped early or diverged: src/solver.py:188-199)
+        RingSlot* r = ctl.ring + (i - 1);
+        r->gap = rec ? hist_row[0] : 0.0;
+        r->err_lit = rec ? hist_row[1] : 0.0;
+        r->err_dark = rec ? hist_row[2] : 0.0;
+        r->iter = i;
+        int fl = kRecPublished | (rec ? kRecRecorded : 0) | (early ? kRecEarly : 0) | (st->bad ? kRecDiverged : 0);
+        const bool ask = ctl.lockstep && !early && !st->bad;
+        if (!ask && stop) fl |= kRecStop;
+        __threadfence_system();
+        *(volatile int*)&r->flags = fl;
+        if (ask) {
+            // bounded wait: a host that never answers (e.g. a callback that itself
+            // waits for this device) must not hang it; after 30 s the solve stops
+            // and reports the timeout
+            unsigned long long t0, t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+            int abort = 0;
+            for (;;) {
+                if (ctl.host[1]) { abort = kRecAborted; break; }
+                if (ctl.host[0] >= i) break;
+                __nanosleep(200);
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+                if (t - t0 > 30000000000ull) { abort = kRecTimeout; break; }
+            }
+            if (abort) {
+                stop = 1;
+                st->aborted = 1;
+            }
+            if (stop) {
+                __threadfence_system();
+                *(volatile int*)&r->flags = fl | kRecStop | abort;
+            }
+        }
+    }
     if (stop) {
         st->stop = 1;
         st->iters_run = i;
@@ -1544,6 +1604,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const __grid_co
         grid_sync(a.bar, epoch);
     }
     const bool early = a.col.ctl.early_tol >= 0.0;
+    const bool lock = a.col.ctl.lockstep != 0;     // host verdicts (should_abort) every iteration
     if constexpr (ALG == 1) {
         // RAAR: the decision on x_{it-1} follows the row phase that measures its gap
         for (int it = a.it_begin; it < a.it_end; ++it) {
@@ -1553,7 +1614,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const __grid_co
             row_phase<T, LG, LGR_R, LGR_C, ALG, TV>(r, B, smraw, tw, &rs);   // gap of x_{it-1}, x_it, w_it
             grid_sync(a.bar, epoch);
             decide_phase_raar<T>(r, B, it - 1);
-            if (early) grid_sync(a.bar, epoch);
+            if (early || lock) grid_sync(a.bar, epoch);
             ColArgs<T> c = a.col;
             c.mode = 2;
             c.u_iter = it;
@@ -1597,8 +1658,9 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const __grid_co
             fine_stamp(5);
             // decisions: records, early stop, max_iters, and the last iterate
             // of this launch (the stepping API reads state after every launch)
-            if (gap_needed(c.ctl, it) || it >= c.ctl.max_iters || it == a.it_end - 1) decide_phase<T, LG, LGR_C>(c, B);
-            if (early) grid_sync(a.bar, epoch);                        // stop flags must be seen by every CTA
+            if (gap_needed(c.ctl, it) || lock || it >= c.ctl.max_iters || it == a.it_end - 1)
+                decide_phase<T, LG, LGR_C>(c, B);
+            if (early || lock) grid_sync(a.bar, epoch);               // stop flags must be seen by every CTA
         }
         if (a.do_final) final_phase<T, LG, LGR_R, LGR_C, TV>(a.fin, B, smraw, tw);
     }

@@ -266,6 +266,11 @@ def solve(c: SlmConstraint, m: FourierConstraint, cfg: SolveConfig,
 
     prec = cfg.precision
     plan = get_plan(spec, prec, device)
+    if on_record is not None or should_abort is not None:
+        # callbacks run while the solve is in flight: a plan of their own, so a
+        # callback may use transforms of this grid (the path setting follows slot 0)
+        base, plan = plan, get_plan(spec, prec, device, slot=1)
+        plan.set_path(base.path())
     fdt = prec.float_dtype
     p_dev = _host_cast(c.p.data, fdt)
     m_dev = _host_cast(m.m.data, fdt)
@@ -301,29 +306,59 @@ def solve(c: SlmConstraint, m: FourierConstraint, cfg: SolveConfig,
             code = lib.pm_solve(plan.handle, _lib.ptr(p_dev), _lib.ptr(m_dev), _lib.ptr(init), 1,
                                 prm, _lib.ptr(tol_p), _lib.ptr(tol_m), _lib.ptr(energy), res)
         else:
-            _lib.check(lib.pm_solve_begin(plan.handle, _lib.ptr(p_dev), _lib.ptr(m_dev),
-                                          _lib.ptr(init), 1, prm, _lib.ptr(tol_p),
-                                          _lib.ptr(tol_m), _lib.ptr(energy)), "pm_solve_begin")
-            code = _lib.PM_OK
-            stopped = _lib.C.c_int(0)
-            g1, l1, d1 = np.full(K, np.nan), np.full(K, np.nan), np.full(K, np.nan)
-            for it in range(1, K + 1):
-                _lib.check(lib.pm_solve_step(plan.handle, 1, _lib.C.byref(stopped)), "pm_solve_step")
-                _lib.check(lib.pm_solve_records(plan.handle, it, it, _lib.ptr(g1), _lib.ptr(l1),
-                                                _lib.ptr(d1), _lib.ptr(iters), _lib.ptr(div)),
-                           "pm_solve_records")
-                if div[0]:
-                    break
-                if on_record is not None and not np.isnan(g1[it - 1]):
-                    on_record(ConvergenceRecord(iter=it, gap=float(g1[it - 1]),
-                                                err_lit=float(l1[it - 1]),
-                                                err_dark=float(d1[it - 1])))
-                if stopped.value:
-                    break
-                if should_abort is not None and should_abort():
-                    aborted = True
-                    break
-            code = lib.pm_solve_finish(plan.handle, int(aborted), res)
+            # one enqueued solve; the device streams every decided iteration into
+            # a host-mapped ring and, when should_abort is given, waits after each
+            # one for its verdict (src/solver.py:188-199) — no launch or copy per
+            # iteration. The callbacks run here, in the caller's thread, in the
+            # reference's order: on_record, then should_abort unless the
+            # iteration stopped early.
+            lockstep = should_abort is not None
+            _lib.check(lib.pm_solve_async(plan.handle, _lib.ptr(p_dev), _lib.ptr(m_dev), _lib.ptr(init),
+                                          prm, _lib.ptr(tol_p), _lib.ptr(tol_m), _lib.ptr(energy),
+                                          int(lockstep), res), "pm_solve_async")
+            rec = _lib.pm_record()
+            failure = None
+            # the iterations the device publishes: all of them when it waits for a
+            # verdict or stops early, else the recorded ones and the last
+            if lockstep or cfg.early_stop_tol is not None:
+                published = range(1, K + 1)
+            else:
+                published = sorted(set(range(1, K + 1, cfg.record_every)) | {K})
+            last = 0
+            try:
+                for it in published:
+                    _lib.check(lib.pm_solve_next(plan.handle, it, _lib.C.byref(rec)), "pm_solve_next")
+                    fl = rec.flags
+                    if not fl or fl & _lib.PM_REC_DIVERGED:
+                        break
+                    last = it
+                    if on_record is not None and fl & _lib.PM_REC_RECORDED:
+                        on_record(ConvergenceRecord(iter=it, gap=float(rec.gap), err_lit=float(rec.err_lit),
+                                                    err_dark=float(rec.err_dark)))
+                    if fl & _lib.PM_REC_EARLY:
+                        break
+                    if lockstep:
+                        stop = bool(should_abort())
+                        _lib.check(lib.pm_solve_answer(plan.handle, it, int(stop)), "pm_solve_answer")
+                        if stop:
+                            aborted = True
+                            break
+                    elif fl & _lib.PM_REC_STOP:
+                        break
+                if lockstep and last and not aborted:
+                    # a device left without a verdict for 30 s stopped at `last`
+                    _lib.check(lib.pm_solve_next(plan.handle, last, _lib.C.byref(rec)), "pm_solve_next")
+                    if rec.flags & _lib.PM_REC_TIMEOUT:
+                        failure = RuntimeError(
+                            f"no should_abort verdict reached the device within 30 s at iteration {last} "
+                            "(a callback may not wait for GPU work on the solving device during a solve)")
+            except BaseException as exc:            # a callback raised: stop the device, then re-raise
+                failure = exc
+                if lockstep:
+                    lib.pm_solve_answer(plan.handle, 0, 1)
+            code = lib.pm_solve_wait(plan.handle, res)
+            if failure is not None:
+                raise failure
     if code == _lib.PM_ERR_DIVERGED or div[0]:
         raise _reference_error(cfg, int(div[0]) or 1, gaps, lits, darks)
     _lib.check(code, "pm_solve")

@@ -34,12 +34,14 @@ _plans: dict[tuple[int, int, int, int], _lib.Plan] = {}
 _plans_lock = threading.Lock()
 
 
-def get_plan(spec: GridSpec, precision: Precision, device: int = 0) -> _lib.Plan:
+def get_plan(spec: GridSpec, precision: Precision, device: int = 0, slot: int = 0) -> _lib.Plan:
     """Per-process plan cache keyed (n_x, n_y, precision, device).
 
     The GPU analogue of the service's PlanCache (src/service.py:65-82).
+    ``slot`` 1 is the plan of solves with host callbacks: their callbacks may
+    use transforms of the same grid (slot 0) while the solve is in flight.
     """
-    key = (spec.n_x, spec.n_y, precision.code, device)
+    key = (spec.n_x, spec.n_y, precision.code, device, slot)
     with _plans_lock:
         plan = _plans.get(key)
         if plan is None:

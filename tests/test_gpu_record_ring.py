@@ -1,0 +1,161 @@
+"""GPU: the streamed record ring and the host verdict word of a callback
+solve (SURVEY.md §8(b) record_ring / abort_flag, §8f-1; reference
+src/solver.py:188-199, src/service.py:211-278).
+
+A solve with on_record / should_abort is ONE enqueued solve: the device
+publishes every decided iteration into host-mapped memory and, when
+should_abort is given, waits after each one for the host's verdict. The
+callbacks see exactly the records and the abort point of the reference's
+loop, on every path, with no launch or copy per iteration."""
+
+import time
+
+import numpy as np
+import pytest
+
+import paper_1302_0120_b200 as pm
+from oracle import phasemask_oracle as orc
+from paper_1302_0120_b200.patterns import make_problem
+
+pytestmark = pytest.mark.gpu
+
+
+def problem(n, tag="double", spots=8, seed=7, ny=None):
+    prec = pm.Precision.from_tag(tag)
+    p, m = make_problem(n, spots, seed, n_y=ny)
+    spec = pm.GridSpec(n, ny or n)
+    return spec, pm.SlmConstraint(pm.RealGrid(spec, p), prec), pm.FourierConstraint(pm.RealGrid(spec, m), prec)
+
+
+def _with_path(spec, prec, path, fn):
+    plan = pm.transform.get_plan(spec, prec)
+    plan.set_path(path)
+    try:
+        return fn()
+    finally:
+        plan.set_path(0)
+
+
+@pytest.mark.parametrize("n,ny,path", [(256, 256, 1), (256, 256, 2), (120, 90, 0)])
+@pytest.mark.parametrize("algo", ["gs", "raar"])
+def test_streamed_records_equal_the_history(n, ny, path, algo):
+    spec, c, m = problem(n, ny=ny)
+    cfg = pm.SolveConfig(max_iters=17, record_every=3, algorithm=algo, beta=0.9)
+    whole = _with_path(spec, pm.DOUBLE, path, lambda: pm.solve(c, m, cfg))
+    seen = []
+    got = _with_path(spec, pm.DOUBLE, path, lambda: pm.solve(c, m, cfg, on_record=seen.append))
+    assert [r.iter for r in seen] == [1, 4, 7, 10, 13, 16]
+    assert [(r.gap, r.err_lit, r.err_dark) for r in seen] == [(r.gap, r.err_lit, r.err_dark) for r in whole.history]
+    np.testing.assert_array_equal(got.mask.phases, whole.mask.phases)
+    assert got.iters_run == 17 and not got.aborted
+
+
+@pytest.mark.parametrize("n,ny,path", [(256, 256, 1), (256, 256, 2), (120, 90, 0)])
+@pytest.mark.parametrize("algo", ["gs", "raar"])
+def test_lockstep_abort_lands_on_the_polled_iteration(n, ny, path, algo):
+    """should_abort is polled once per iteration, after that iteration's
+    on_record; True at the 7th poll stops at iterate 7 exactly."""
+    spec, c, m = problem(n, ny=ny)
+    events = []
+
+    def on_record(r):
+        events.append(("rec", r.iter))
+
+    def should_abort():
+        events.append(("poll", len([e for e in events if e[0] == "poll"]) + 1))
+        return events[-1][1] >= 7
+
+    cfg = pm.SolveConfig(max_iters=40, algorithm=algo, beta=0.9)
+    r = _with_path(spec, pm.DOUBLE, path, lambda: pm.solve(c, m, cfg, on_record=on_record, should_abort=should_abort))
+    assert r.aborted and r.iters_run == 7
+    assert events == [e for i in range(1, 8) for e in (("rec", i), ("poll", i))]
+    ref = _with_path(spec, pm.DOUBLE, path, lambda: pm.solve(c, m, pm.SolveConfig(max_iters=7, algorithm=algo, beta=0.9)))
+    np.testing.assert_array_equal(r.mask.phases, ref.mask.phases)
+    assert [x.gap for x in r.history] == [x.gap for x in ref.history]
+
+
+def test_early_stop_skips_the_poll_of_its_iteration():
+    """The reference breaks on early stop before should_abort (src/solver.py:193-199)."""
+    spec, c, m = problem(128)
+    cfg = pm.SolveConfig(max_iters=300, early_stop_tol=1e-6)
+    whole = pm.solve(c, m, cfg)
+    assert whole.iters_run < 300
+    polls = []
+    r = pm.solve(c, m, cfg, should_abort=lambda: polls.append(1) and False)
+    assert r.iters_run == whole.iters_run and not r.aborted
+    assert len(polls) == whole.iters_run - 1
+    o = orc.solve(c.p.data, m.m.data, 300, "double", early_stop_tol=1e-6)
+    assert o["iters_run"] == r.iters_run
+
+
+def test_callback_exception_stops_the_device_and_propagates():
+    spec, c, m = problem(256, "single")
+
+    def on_record(r):
+        if r.iter == 4:
+            raise RuntimeError("callback failed")
+
+    with pytest.raises(RuntimeError, match="callback failed"):
+        pm.solve(c, m, pm.SolveConfig(max_iters=50, precision=pm.SINGLE), on_record=on_record,
+                 should_abort=lambda: False)
+    # the plan is usable at once (the device did not wait for a verdict that never came)
+    t0 = time.perf_counter()
+    r = pm.solve(c, m, pm.SolveConfig(max_iters=5, precision=pm.SINGLE), should_abort=lambda: False)
+    assert r.iters_run == 5 and time.perf_counter() - t0 < 10.0
+
+
+def test_callbacks_may_use_transforms_of_the_same_grid():
+    """An on_record callback that runs an FftProvider of the solve's own grid
+    while the solve is in flight does not deadlock: the callback solve has its
+    own plan, and the device never waits for on_record (only for should_abort
+    verdicts, whose callbacks must not wait for work on the solving device)."""
+    spec, c, m = problem(128)
+    prov = pm.FftProvider(spec, pm.DOUBLE)
+    x = pm.Field(spec, np.ones(spec.shape, complex), pm.grid.SLM_PLANE)
+    norms = []
+
+    def on_record(r):
+        norms.append(float(np.abs(prov.forward(x).data).max()))
+
+    r = pm.solve(c, m, pm.SolveConfig(max_iters=4), on_record=on_record)
+    assert r.iters_run == 4 and len(norms) == 4
+    np.testing.assert_allclose(norms, 128.0)
+
+
+def test_stream_is_one_launch_and_cheap_at_1024():
+    """1024^2 fp32, K = 100, record_every = 1: records stream from ONE solve
+    (the launch count of the callback-free solve), and the callback solve
+    costs at most 1.5x the callback-free one, on the device and end to end
+    (VERDICT r1 item 5). Medians of alternating runs; results are dropped
+    between runs so page-locked output buffers are reused."""
+    spec, c, m = problem(1024, "single", spots=50)
+    cfg = pm.SolveConfig(max_iters=100, precision=pm.SINGLE, record_every=1)
+    plan0 = pm.transform.get_plan(spec, pm.SINGLE)
+    plan1 = pm.transform.get_plan(spec, pm.SINGLE, slot=1)
+    gaps = [x.gap for x in pm.solve(c, m, cfg).history]
+    variants = {"plain": {}, "on_record": {"on_record": None},
+                "lockstep": {"on_record": None, "should_abort": lambda: False}}
+    times = {k: [] for k in variants}
+    dev = {k: [] for k in variants}
+    launches = {}
+    for rep in range(6):
+        for name, kw in variants.items():
+            seen = []
+            kw = {k: (seen.append if k == "on_record" else v) for k, v in kw.items()}
+            plan = plan0 if name == "plain" else plan1
+            l0 = plan.launch_count()
+            t = time.perf_counter()
+            r = pm.solve(c, m, cfg, **kw)
+            times[name].append(time.perf_counter() - t)
+            dev[name].append(r.timing.fft_ms)
+            launches[name] = plan.launch_count() - l0
+            if name != "plain":
+                assert [x.gap for x in seen] == gaps
+            del r
+    med = {k: float(np.median(v[1:])) * 1e3 for k, v in times.items()}
+    dmed = {k: float(np.median(v[1:])) for k, v in dev.items()}
+    print("\n1024^2 fp32 x100, record_every=1, medians: " +
+          ", ".join(f"{k} {med[k]:.2f} ms e2e / {dmed[k]:.3f} ms device" for k in variants))
+    assert launches["on_record"] == launches["plain"] == launches["lockstep"]
+    assert med["on_record"] <= 1.5 * med["plain"] and dmed["on_record"] <= 1.5 * dmed["plain"]
+    assert med["lockstep"] <= 1.5 * med["plain"] and dmed["lockstep"] <= 1.5 * dmed["plain"]
