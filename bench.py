@@ -47,6 +47,14 @@ METRIC = "ms per 1024² phase mask (100 iters) and AP iterations/s; % of HBM/L2 
 BYTES_PER_ITER = 40 * N_PIX * N_PIX          # fp32 GS, two fused sweeps
 
 
+def workload_config(world: int, plan_path: str = "persistent") -> dict:
+    """The `config` of both arms (ours and --impl reference): the same keys."""
+    return {"workload": "gs_1024x1024_fp32_100iter_50spots_single_mask", "n_x": N_PIX, "n_y": N_PIX,
+            "iters": ITERS, "spots": SPOTS, "seed": SEED, "masks_per_step": world, "masks_per_rank": 1,
+            "record_every": ITERS, "parallelism": f"masks sharded over {world} GPU(s), no collective",
+            "l2": "flushed by a 256 MiB write before every timed step", "path": plan_path}
+
+
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -159,8 +167,8 @@ def run_reference(args, world, rank):
     line = {"impl": "reference", "metric": METRIC, "value": ms, "unit": "ms/mask", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": "gs_1024x1024_fp32_100iter_50spots_single_mask", "n_x": N_PIX, "n_y": N_PIX,
-                       "iters": ITERS, "masks_per_step": 1, "record_every": ITERS},
+            "config": dict(workload_config(1), path="host CPU (reference algorithm, scipy.fft)",
+                           l2="n/a (host)", parallelism=f"one mask per step on {cores} host threads"),
             "iters_per_s": ITERS / (ms / 1e3),
             "cpu_baseline": {"value": ms, "unit": "ms/mask", "cores": cores, "kind": "port",
                              "sample": f"one full {ITERS}-iteration 1024^2 fp32 mask per step, "
@@ -196,6 +204,139 @@ def paper_config(device: int) -> dict:
             "paper_hw": "Tesla C2070, incl. ~1 ms target upload (PAPER:416-417)"}
 
 
+def run_batch(args, world, rank, local):
+    """--config 4 (BASELINE.json configs[3]): a batch of 256 independent
+    1024^2 masks (distinct 50-spot OSPs, seeds 1000..1255, one shared
+    Gaussian p) sharded in contiguous blocks over the N ranks, 100 GS
+    iterations fp32, no collective on the iteration path (SURVEY.md §8e;
+    the reference loops the images one by one, src/estimator.py:85-93).
+    A step solves the whole job once: value = whole-job ms per mask, i.e.
+    max-over-ranks device ms per step / 256; `ms_per_batch` beside it, to
+    compare with the HBM-lockstep floors 164 / 82 / 41 / 20.5 ms (§8d)."""
+    import torch
+    import torch.distributed as dist
+    import paper_1302_0120_b200 as pm
+    from paper_1302_0120_b200 import _lib
+    from paper_1302_0120_b200.batch import shard_bounds, solve_stack
+    from paper_1302_0120_b200.patterns import make_problem, spot_targets
+    from paper_1302_0120_b200.solver import _params
+
+    total_masks = 256
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    lo, hi = shard_bounds(total_masks, world, rank)
+    B = hi - lo
+    prec = pm.SINGLE
+    p, m0 = make_problem(N_PIX, SPOTS, 1000)
+    ms = spot_targets(N_PIX, SPOTS, range(1000 + lo, 1000 + hi), dtype=np.float32)
+    if lo == 0:
+        assert np.array_equal(ms[0], m0.astype(np.float32))
+    spec = pm.GridSpec(N_PIX, N_PIX)
+    plan = pm.transform.get_plan(spec, prec, local)
+    stream = torch.cuda.Stream(device=local)
+    plan.set_stream(stream.cuda_stream)
+    d_p = torch.from_numpy(p.astype(np.float32)).cuda(local)
+    d_m = torch.from_numpy(ms).cuda(local)
+    d_phase = torch.empty((B, N_PIX, N_PIX), dtype=torch.float64, device=f"cuda:{local}")
+    tol_p = np.full(B, prec.zero_tol(p.astype(np.float32).max()))
+    tol_m = np.full(B, prec.zero_tol(1.0))
+    energy = np.full(B, float(SPOTS))               # sum m^2 of every target
+    cfg = pm.SolveConfig(max_iters=ITERS, precision=prec, record_every=ITERS, device=local)
+    prm = _params(cfg, False, False)
+    gaps = np.full(B * ITERS, np.nan)
+    iters = np.zeros(B, np.int32)
+
+    def solve_device():
+        res = _lib.pm_result()
+        res.phases = _lib.C.c_void_p(d_phase.data_ptr())
+        res.gap = _lib.ptr(gaps)
+        res.iters_run = _lib.ptr(iters)
+        _lib.check(plan.lib.pm_solve_device(plan.handle, _lib.C.c_void_p(d_p.data_ptr()),
+                                            _lib.C.c_void_p(d_m.data_ptr()), None, B, prm, _lib.ptr(tol_p),
+                                            _lib.ptr(tol_m), _lib.ptr(energy), res), "pm_solve_device")
+
+    for _ in range(args.warmup):
+        solve_device()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    step_ms = []
+    with ClockSampler(local) as clocks:
+        clocks.wait_first()
+        launches0 = plan.launch_count()
+        for _ in range(args.steps):                 # working set 3 GB per GPU: no L2 flush needed
+            with torch.cuda.stream(stream):
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+            solve_device()
+            with torch.cuda.stream(stream):
+                e1.record(stream)
+            e1.synchronize()
+            step_ms.append(e0.elapsed_time(e1))
+        launches = plan.launch_count() - launches0
+        time.sleep(0.2)
+    assert (iters == ITERS).all() and np.isfinite(gaps[::ITERS]).all()
+    total = torch.tensor([sum(step_ms)], dtype=torch.float64, device=f"cuda:{local}")
+    if world > 1:
+        dist.barrier()
+        dist.all_reduce(total, op=dist.ReduceOp.MAX)
+    ms_per_batch = float(total.item()) / args.steps
+    value = ms_per_batch / total_masks
+
+    # end to end through solve_stack: the rank's targets uploaded from pinned
+    # memory, the 8-bit SLM levels (what an SLM displays) downloaded
+    p_pin = torch.from_numpy(p.astype(np.float32)).pin_memory().numpy()
+    m_pin = torch.from_numpy(ms).pin_memory().numpy()
+    lv_pin = torch.empty((B, N_PIX, N_PIX), dtype=torch.uint8).pin_memory().numpy()
+    e2e_ms = []
+    for i in range(1 + min(args.steps, 5)):
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        r = solve_stack(p_pin, m_pin, cfg, device=local, phases=False, levels=True, out_levels=lv_pin)
+        if i:
+            e2e_ms.append((time.perf_counter() - t0) * 1e3)
+        assert (r.iters_run == ITERS).all()
+    e2e = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device=f"cuda:{local}")
+    if world > 1:
+        dist.all_reduce(e2e, op=dist.ReduceOp.MAX)
+    e2e_batch = float(e2e.item()) / len(e2e_ms)
+    if rank == 0:
+        peaks = measured_peaks()
+        hbm = peaks.get("hbm_gbs")
+        achieved = BYTES_PER_ITER * ITERS * B / (ms_per_batch * 1e-3) / 1e9   # per GPU (rank 0's share)
+        floor = 40 * N_PIX * N_PIX * ITERS * total_masks / world / (6550.7e9) * 1e3
+        line = {
+            "metric": METRIC, "value": value, "unit": "ms/mask", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_batch, "higher_is_better": False,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "gs_1024x1024_fp32_100iter_50spots_batch256", "n_x": N_PIX, "n_y": N_PIX,
+                       "iters": ITERS, "spots": SPOTS, "seeds": "1000..1255", "masks_per_step": total_masks,
+                       "masks_per_rank": B, "record_every": ITERS,
+                       "parallelism": f"256 masks in contiguous blocks over {world} GPU(s), no collective",
+                       "l2": "working set 3 GB per GPU (> L2): no flush needed", "path": "persistent (TMA build)"},
+            "ms_per_batch": ms_per_batch, "hbm_floor_ms_per_batch": floor,
+            "iters_per_s": ITERS * total_masks / (ms_per_batch / 1e3),
+            "e2e": {"value": e2e_batch / total_masks, "unit": "ms/mask", "ms_per_batch": e2e_batch,
+                    "h2d_bytes_per_step": p_pin.nbytes + m_pin.nbytes, "d2h_bytes_per_step": lv_pin.nbytes,
+                    "api": "paper_1302_0120_b200.batch.solve_stack(levels=True, phases=False): pinned "
+                           "targets up, uint8 SLM levels down"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                         "frac": achieved / hbm if hbm else None, "traffic": None,
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs",
+                         "kernel": "solve_kernel TMA build (whole batch in one launch)",
+                         "bytes_per_iter": BYTES_PER_ITER},
+            "clocks": clocks.summary(), "gpu_launches": launches,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def flush_l2(buf):
     buf.fill_(1.0)      # 256 MiB write > the 126 MB L2
 
@@ -207,8 +348,14 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--config", type=int, choices=[3, 4], default=3,
+                    help="BASELINE.json config: 3 = one 1024^2 mask per GPU (default, the headline), "
+                         "4 = a 256-mask batch sharded over the GPUs")
     args = ap.parse_args()
     world, rank, local = dist_env()
+    if args.config == 4 and args.impl == "ours":
+        run_batch(args, world, rank, local)
+        return
 
     if args.impl == "reference":
         run_reference(args, world, rank)
@@ -345,38 +492,69 @@ def main():
     h2d_s = p_pin.nbytes + m2.nbytes
     d2h_s = outs[0].nbytes + 3 * ITERS * 8 + 4 * 2
 
+    # ---- end to end through the drop-in itself: the reference's entry point
+    # solve(c, m, cfg) (src/solver.py:111-113) with the caller's float64 grids
+    # on the host and a SolveResult (mask, u*, v*, history) back
+    c_in = pm.SlmConstraint(pm.RealGrid(spec, p), prec)
+    m_in = pm.FourierConstraint(pm.RealGrid(spec, m), prec)
+    dropin_ms = []
+    for i in range(args.warmup + args.steps):
+        with torch.cuda.stream(plan_stream):
+            flush_l2(flush)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        r_d = pm.solve(c_in, m_in, cfg)
+        t1 = time.perf_counter()
+        assert r_d.iters_run == ITERS
+        if i >= args.warmup:
+            dropin_ms.append((t1 - t0) * 1e3)
+        del r_d
+    dropin = torch.tensor([sum(dropin_ms)], dtype=torch.float64, device=f"cuda:{local}")
+    if world > 1:
+        dist.all_reduce(dropin, op=dist.ReduceOp.MAX)
+    dropin_value = float(dropin.item()) / args.steps / world
+    h2d_d = 2 * N_PIX * N_PIX * 4                      # p and m, cast to float32 on the host
+    d2h_d = N_PIX * N_PIX * (8 + 8 + 8) + 3 * ITERS * 8 + 8   # mask (float64), u*, v* (complex64), records
+
     if rank == 0:
         peaks = measured_peaks()
         hbm = peaks.get("hbm_gbs")
         solve_ms = ms_per_step                          # one persistent launch per step
         achieved = BYTES_PER_ITER * ITERS / (solve_ms * 1e-3) / 1e9
-        l2 = _lib.measure_copy(32 << 20, 20, local)
+        # the roof: the 8 MB field (and p, m) stay in the 126 MB L2 across the
+        # solve's iterations, so the bound is the L2-resident copy bandwidth
+        # (read + write bytes, as the sweeps' traffic), measured here
+        l2 = _lib.measure_l2(32 << 20, 50, 1, local)
         traffic = None
-        tfile = REPO / "profiles" / "r01_ncu_traffic.json"
-        if tfile.exists():
-            traffic = json.loads(tfile.read_text()).get("dram_bytes_per_launch")
+        tfiles = sorted((REPO / "profiles").glob("r*_ncu_traffic.json"))
+        if tfiles:
+            traffic = json.loads(tfiles[-1].read_text()).get("dram_bytes_per_launch")
         line = {
             "metric": METRIC, "value": value, "unit": "ms/mask", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": False, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": "gs_1024x1024_fp32_100iter_50spots_single_mask", "n_x": N_PIX, "n_y": N_PIX,
-                       "iters": ITERS, "spots": SPOTS, "masks_per_step": world, "masks_per_rank": 1,
-                       "record_every": ITERS, "parallelism": f"masks sharded over {world} GPU(s), no collective",
-                       "l2": "flushed by a 256 MiB write before every timed step",
-                       "path": "persistent" if plan.path() == 1 else "sweep-graph"},
+            "config": workload_config(world, "persistent" if plan.path() == 1 else "sweep-graph"),
             "iters_per_s": ITERS * world / (ms_per_step / 1e3),
             "e2e": {"value": e2e_value, "unit": "ms/mask", "h2d_bytes_per_step": h2d_s, "d2h_bytes_per_step": d2h_s,
                     "api": "paper_1302_0120_b200.batch.solve_stream (pinned host buffers; the uploads and "
                            "downloads of neighbouring frames overlap each solve)",
                     "latency": {"value": e2e_latency, "unit": "ms/mask", "h2d_bytes_per_step": h2d,
                                 "d2h_bytes_per_step": d2h,
-                                "api": "paper_1302_0120_b200.batch.solve_stack, one synchronous call per mask"}},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": (achieved / hbm) if hbm else None, "traffic": traffic,
-                         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if hbm else None,
+                                "api": "paper_1302_0120_b200.batch.solve_stack, one synchronous call per mask"},
+                    "dropin": {"value": dropin_value, "unit": "ms/mask", "h2d_bytes_per_step": h2d_d,
+                               "d2h_bytes_per_step": d2h_d,
+                               "api": "paper_1302_0120_b200.solve(c, m, cfg): the reference's entry point, "
+                                      "float64 host grids in, SolveResult (mask, u*, v*, history) out"}},
+            "roofline": {"bound": "l2", "achieved": achieved, "peak": l2, "unit": "GB/s",
+                         "frac": achieved / l2 if l2 else None, "traffic": traffic,
+                         "peak_source": "measured in this run: pm_measure_l2, 32 MiB L2-resident copy, "
+                                        "50 passes in one launch, read + write bytes",
                          "kernel": "solve_kernel (persistent; whole solve in one launch)",
-                         "bytes_per_iter": BYTES_PER_ITER, "l2_copy_gbs_measured": l2,
-                         "frac_of_l2_copy": achieved / l2 if l2 else None},
+                         "bytes_per_iter": BYTES_PER_ITER, "hbm_peak": hbm,
+                         "hbm_frac": (achieved / hbm) if hbm else None,
+                         "hbm_peak_source": "MEASURED_PEAKS.json hbm_gbs" if hbm else None},
             "clocks": clocks.summary(),
             "gpu_launches": launches,
         }

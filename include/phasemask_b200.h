@@ -324,6 +324,11 @@ int pm_debug_phase_stamps(pm_plan *plan, int enable, unsigned long long *out, in
  * `reps`, for the HBM (bytes >> L2) and L2 (bytes << L2) roofs. */
 int pm_measure_copy(int device, long long bytes, int reps, double *gbs);
 
+/* L2 roof (SURVEY.md §8(d) "Which roof"): `passes` sweeps over an
+ * L2-resident buffer of `bytes` inside one launch, L1 bypassed; mode 0 reads
+ * only (bytes read), 1 copies (read + write bytes counted). Best of 4. */
+int pm_measure_l2(int device, long long bytes, int passes, int mode, double *gbs);
+
 #ifdef __cplusplus
 }
 #endif

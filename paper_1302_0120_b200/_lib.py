@@ -116,6 +116,7 @@ SIGNATURES = {
     "pm_solve_wait": (_I, [_VP, C.POINTER(pm_result)]),
     "pm_time_sweep": (_I, [_VP, _I, _I, _I, C.POINTER(C.c_float)]),
     "pm_measure_copy": (_I, [_I, _LL, _I, C.POINTER(_D)]),
+    "pm_measure_l2": (_I, [_I, _LL, _I, _I, C.POINTER(_D)]),
     "pm_debug_phase_stamps": (_I, [_VP, _I, _VP, _I]),
 }
 
@@ -370,3 +371,10 @@ def measure_copy(nbytes: int, reps: int = 10, device: int = 0) -> float:
     g = C.c_double(0.0)
     check(load().pm_measure_copy(device, int(nbytes), reps, C.byref(g)), "pm_measure_copy")
     return g.value
+
+
+def measure_l2(nbytes: int, passes: int = 50, mode: int = 1, device: int = 0) -> float:
+    """L2-resident bandwidth in GB/s (mode 1: copy, read + write bytes; 0: reads)."""
+    v = C.c_double(0.0)
+    check(load().pm_measure_l2(device, nbytes, passes, mode, C.byref(v)), "pm_measure_l2")
+    return v.value

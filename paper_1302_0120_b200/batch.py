@@ -46,7 +46,7 @@ def shard_bounds(n_items: int, world: int, rank: int) -> tuple[int, int]:
 class BatchResult:
     """Per-mask outputs of a batch solve, stacked along axis 0."""
 
-    phases: np.ndarray          # (B, n_y, n_x) float64 in [0, 2pi)
+    phases: np.ndarray | None   # (B, n_y, n_x) float64 in [0, 2pi) (None: levels-only solve)
     gap: np.ndarray             # (B, K) gap history, NaN where not recorded
     err_lit: np.ndarray         # (B, K)
     err_dark: np.ndarray        # (B, K)
@@ -56,9 +56,10 @@ class BatchResult:
 
     @staticmethod
     def concat(parts: list["BatchResult"]) -> "BatchResult":
-        parts = [q for q in parts if q.phases.shape[0]]
+        parts = [q for q in parts if q.iters_run.shape[0]]
         levels = None if any(q.levels is None for q in parts) else np.concatenate([q.levels for q in parts])
-        return BatchResult(np.concatenate([q.phases for q in parts]),
+        phases = None if any(q.phases is None for q in parts) else np.concatenate([q.phases for q in parts])
+        return BatchResult(phases,
                            np.concatenate([q.gap for q in parts]),
                            np.concatenate([q.err_lit for q in parts]),
                            np.concatenate([q.err_dark for q in parts]),
@@ -72,7 +73,8 @@ def _maxes(a: np.ndarray, k: int) -> np.ndarray:
 
 def solve_stack(p: np.ndarray, m_stack: np.ndarray, cfg: SolveConfig, device: int = 0,
                 out_phases: np.ndarray | None = None, levels: bool = False,
-                init: np.ndarray | None = None) -> BatchResult:
+                init: np.ndarray | None = None, phases: bool = True,
+                out_levels: np.ndarray | None = None) -> BatchResult:
     """Solve a stack of targets on one device in one launch.
 
     p: (n_y, n_x) shared amplitude or (B, n_y, n_x) per mask; m_stack:
@@ -80,7 +82,10 @@ def solve_stack(p: np.ndarray, m_stack: np.ndarray, cfg: SolveConfig, device: in
     precision's dtype are used without a host copy (pass pinned buffers for
     full-speed transfers); ``out_phases`` (B, n_y, n_x) float64 may be a
     caller-owned (e.g. pinned) buffer for the mask; ``levels=True`` also
-    returns the 8-bit SLM levels computed on the device; ``init`` (B, n_y, n_x)
+    returns the 8-bit SLM levels computed on the device, and with
+    ``phases=False`` they are the only per-pixel output (1 byte per pixel
+    downloaded instead of 8; ``out_levels`` may be a caller-owned (B, n_y,
+    n_x) uint8 buffer); ``init`` (B, n_y, n_x)
     complex are caller-chosen Fourier-plane starts instead of m; without it,
     ``cfg.random_phase_init`` draws the seeded phases on the device
     (src/solver.py:100-103, the same draws for every mask, as a reference
@@ -107,9 +112,14 @@ def solve_stack(p: np.ndarray, m_stack: np.ndarray, cfg: SolveConfig, device: in
     # (src/solver.py:122-125) run on the device, on the uploaded p and m
     tol_p = tol_m = None
     K = cfg.max_iters
-    phases = out_phases if out_phases is not None else _host_empty((B, ny, nx), np.float64)
-    if phases.shape != (B, ny, nx) or phases.dtype != np.float64 or not phases.flags.c_contiguous:
-        raise ValueError("out_phases must be a C-contiguous float64 (batch, n_y, n_x) array")
+    want_phases = phases
+    if not want_phases and not levels:
+        raise ValueError("phases=False needs levels=True (no per-pixel output otherwise)")
+    phases = None
+    if want_phases:
+        phases = out_phases if out_phases is not None else _host_empty((B, ny, nx), np.float64)
+        if phases.shape != (B, ny, nx) or phases.dtype != np.float64 or not phases.flags.c_contiguous:
+            raise ValueError("out_phases must be a C-contiguous float64 (batch, n_y, n_x) array")
     out = BatchResult(phases, np.full((B, K), np.nan), np.full((B, K), np.nan),
                       np.full((B, K), np.nan), np.zeros(B, np.int32))
     div = np.zeros(B, np.int32)
@@ -120,7 +130,12 @@ def solve_stack(p: np.ndarray, m_stack: np.ndarray, cfg: SolveConfig, device: in
     res.iters_run, res.diverged_iter, res.device_ms = _lib.ptr(out.iters_run), _lib.ptr(div), _lib.ptr(ms)
     if levels:
         # 8-bit SLM levels computed on the device (reference src/grid.py:152-154)
-        out.levels = np.empty((B, ny, nx), dtype=np.uint8)
+        if out_levels is not None:
+            if out_levels.shape != (B, ny, nx) or out_levels.dtype != np.uint8 or not out_levels.flags.c_contiguous:
+                raise ValueError("out_levels must be a C-contiguous uint8 (batch, n_y, n_x) array")
+            out.levels = out_levels
+        else:
+            out.levels = _host_empty((B, ny, nx), np.uint8)
         res.levels = _lib.ptr(out.levels)
     init_c = None
     if init is not None:
@@ -148,7 +163,8 @@ def _diverged(div: np.ndarray) -> SolveDivergedError:
     return e
 
 
-def solve_stream(items, cfg: SolveConfig, device: int = 0, out_phases: list | None = None):
+def solve_stream(items, cfg: SolveConfig, device: int = 0, out_phases: list | None = None,
+                 levels_only: bool = False):
     """A real-time sequence of masks on one device (the paper's interactive
     use: a new target pattern per frame), pipelined.
 
@@ -161,7 +177,10 @@ def solve_stream(items, cfg: SolveConfig, device: int = 0, out_phases: list | No
     (pinned) host buffers, used alternately for the masks (a yielded mask
     stays valid until two more have been produced); otherwise fresh arrays.
     Every solve is :func:`solve_stack`'s (device tolerances and energy),
-    bitwise.
+    bitwise. ``levels_only``: each frame downloads the uint8 SLM levels (1
+    byte per pixel, what an SLM displays) instead of the
+    float64 mask (BatchResult.levels set, .phases None); ``out_phases`` then
+    holds uint8 buffers.
     """
     import torch                                        # streams and events only (plumbing)
 
@@ -185,7 +204,8 @@ def solve_stream(items, cfg: SolveConfig, device: int = 0, out_phases: list | No
     up, down = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
     d_p = [torch.empty((ny, nx), dtype=tdt, device=dev) for _ in range(2)]
     d_m = [torch.empty((ny, nx), dtype=tdt, device=dev) for _ in range(2)]
-    d_ph = [torch.empty((ny, nx), dtype=torch.float64, device=dev) for _ in range(2)]
+    odt = torch.uint8 if levels_only else torch.float64
+    d_ph = [torch.empty((ny, nx), dtype=odt, device=dev) for _ in range(2)]
     ev_up = [torch.cuda.Event() for _ in range(2)]
     ev_done = [torch.cuda.Event() for _ in range(2)]
     ev_down = [torch.cuda.Event() for _ in range(2)]
@@ -221,7 +241,10 @@ def solve_stream(items, cfg: SolveConfig, device: int = 0, out_phases: list | No
             div = np.zeros(1, np.int32)
             ms = np.zeros(1, np.float32)
             res = _lib.pm_result()
-            res.phases = _lib.C.c_void_p(d_ph[s].data_ptr())
+            if levels_only:
+                res.levels = _lib.C.c_void_p(d_ph[s].data_ptr())
+            else:
+                res.phases = _lib.C.c_void_p(d_ph[s].data_ptr())
             res.gap, res.err_lit, res.err_dark = (_lib.ptr(res_py.gap), _lib.ptr(res_py.err_lit),
                                                   _lib.ptr(res_py.err_dark))
             res.iters_run, res.diverged_iter, res.device_ms = (_lib.ptr(res_py.iters_run), _lib.ptr(div),
@@ -235,7 +258,7 @@ def solve_stream(items, cfg: SolveConfig, device: int = 0, out_phases: list | No
             _lib.check(code, "pm_solve_device")
             res_py.device_ms = float(ms[0])
             ev_done[s].record(compute)
-            host = outs[s] if outs[s] is not None else np.empty((1, ny, nx))
+            host = outs[s] if outs[s] is not None else np.empty((1, ny, nx), np.uint8 if levels_only else np.float64)
             with torch.cuda.stream(down):
                 down.wait_event(ev_done[s])
                 torch.from_numpy(host).view(ny, nx).copy_(d_ph[s], non_blocking=True)
@@ -243,13 +266,19 @@ def solve_stream(items, cfg: SolveConfig, device: int = 0, out_phases: list | No
             if pending is not None:                # frame i-1: its download ran during this solve
                 ps, pres, phost = pending
                 ev_down[ps].synchronize()
-                pres.phases = phost
+                if levels_only:
+                    pres.levels = phost
+                else:
+                    pres.phases = phost
                 yield pres
             pending = (s, res_py, host)
             item, i = nxt, i + 1
         ps, pres, phost = pending
         ev_down[ps].synchronize()
-        pres.phases = phost
+        if levels_only:
+            pres.levels = phost
+        else:
+            pres.phases = phost
         yield pres
     finally:
         torch.cuda.synchronize(dev)

@@ -303,6 +303,32 @@ __global__ void transpose_kernel(const T* __restrict__ in, T* __restrict__ out, 
     }
 }
 
+// L2 roof: `passes` sweeps over an L2-resident buffer inside ONE launch (mode
+// 0: reads only, 1: copy a -> b), L1 bypassed, 4 independent 16-byte
+// accesses in flight per thread.
+__global__ void __launch_bounds__(512) l2_kernel(const float4* __restrict__ a, float4* __restrict__ b, long long n,
+                                                  int passes, int mode, float* sink) {
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    float acc = 0.f;
+    for (int pass = 0; pass < passes; ++pass) {
+        for (long long i = t; i < n; i += 4 * stride) {
+            float4 v[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) v[k] = i + k * stride < n ? __ldcg(a + i + k * stride) : make_float4(0, 0, 0, 0);
+            if (mode) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (i + k * stride < n) __stcg(b + i + k * stride, v[k]);
+            } else {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) acc += v[k].x + v[k].y + v[k].z + v[k].w;
+            }
+        }
+    }
+    if (acc == 1.2345e-30f) *sink = acc;
+}
+
 __global__ void copy_kernel(const float4* __restrict__ a, float4* __restrict__ b, long long n) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x)
@@ -1781,7 +1807,7 @@ int enqueue_full_solve(pm_plan* pl) {
 
 // Copy history / state back and fill the host-side result fields.
 int read_records(pm_plan* pl, int first, int last, double* gap, double* lit, double* dark,
-                 int* iters, int* diverged, int* aborted = nullptr, int* zero = nullptr) {
+                 int* iters, int* diverged, int* aborted = nullptr, int* zero = nullptr, int* pair_bad = nullptr) {
     auto& s = pl->s;
     const int B = s.batch, K = s.prm.max_iters;
     std::vector<MaskState> st(B);
@@ -1794,8 +1820,10 @@ int read_records(pm_plan* pl, int first, int last, double* gap, double* lit, dou
     }
     CK(cudaStreamSynchronize(pl->stream));
     if (zero) *zero = 0;
+    if (pair_bad) *pair_bad = 0;
     for (int b = 0; b < B; ++b) {
         if (zero) *zero |= st[b].zero;
+        if (pair_bad && !st[b].diverged) *pair_bad |= st[b].pair_bad;
         if (iters) iters[b] = st[b].iters_run;
         if (diverged) diverged[b] = st[b].diverged;
         if (aborted) aborted[b] = st[b].aborted;
@@ -2437,9 +2465,9 @@ static int solve_collect(pm_plan* pl, pm_result* res, bool host_io) {
             CK(cudaMemcpyAsync(res->v_star, pl->vstar, batch * N * pl->csz, cudaMemcpyDeviceToHost, pl->stream));
     }
     std::vector<int> iters(batch), div(batch);
-    int zero = 0;
+    int zero = 0, pair_bad = 0;
     CKR(read_records(pl, 1, prm->max_iters, res ? res->gap : nullptr, res ? res->err_lit : nullptr,
-                     res ? res->err_dark : nullptr, iters.data(), div.data(), nullptr, &zero));
+                     res ? res->err_dark : nullptr, iters.data(), div.data(), nullptr, &zero, &pair_bad));
     if (res) {
         if (res->iters_run) std::copy(iters.begin(), iters.end(), res->iters_run);
         if (res->diverged_iter) std::copy(div.begin(), div.end(), res->diverged_iter);
@@ -2449,6 +2477,7 @@ static int solve_collect(pm_plan* pl, pm_result* res, bool host_io) {
     s.ring = s.lockstep = false;
     CKR(zero_error(zero));
     if (any_diverged(div)) return set_err(PM_ERR_DIVERGED, "non-finite values during the iteration");
+    if (pair_bad) return set_err(PM_ERR_ARG, "field contains non-finite entries");
     return PM_OK;
 }
 
@@ -2644,9 +2673,9 @@ int pm_solve_finish(pm_plan* pl, int abort, pm_result* res) {
             CK(cudaMemcpyAsync(res->v_star, pl->vstar, batch * N * pl->csz, cudaMemcpyDeviceToHost, pl->stream));
     }
     std::vector<int> iters(batch), div(batch);
-    int zero = 0;
+    int zero = 0, pair_bad = 0;
     CKR(read_records(pl, 1, s.prm.max_iters, res ? res->gap : nullptr, res ? res->err_lit : nullptr,
-                     res ? res->err_dark : nullptr, iters.data(), div.data(), nullptr, &zero));
+                     res ? res->err_dark : nullptr, iters.data(), div.data(), nullptr, &zero, &pair_bad));
     if (res) {
         if (res->iters_run) std::copy(iters.begin(), iters.end(), res->iters_run);
         if (res->diverged_iter) std::copy(div.begin(), div.end(), res->diverged_iter);
@@ -2655,6 +2684,7 @@ int pm_solve_finish(pm_plan* pl, int abort, pm_result* res) {
     s.active = false;
     CKR(zero_error(zero));
     if (any_diverged(div)) return set_err(PM_ERR_DIVERGED, "non-finite values during the iteration");
+    if (pair_bad) return set_err(PM_ERR_ARG, "field contains non-finite entries");
     return PM_OK;
 }
 
@@ -2751,6 +2781,53 @@ int pm_measure_copy(int device, long long bytes, int reps, double* gbs) {
     cudaFree(b);
     if (e != cudaSuccess) return cuda_err(e, "copy_kernel");
     *gbs = 2.0 * n4 * 16 / (best * 1e-3) / 1e9;
+    return PM_OK;
+}
+
+int pm_measure_l2(int device, long long bytes, int passes, int mode, double* gbs) {
+    if (!gbs || bytes < 16 || passes < 1 || (mode != 0 && mode != 1)) return set_err(PM_ERR_ARG, "bad arguments");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return set_err(PM_ERR_CUDA, "no CUDA device available");
+    }
+    CK(cudaSetDevice(device));
+    const long long n4 = bytes / 16;
+    float4 *a = nullptr, *b = nullptr;
+    float* sink = nullptr;
+    CK(cudaMalloc((void**)&a, n4 * 16));
+    cudaError_t e = cudaMalloc((void**)&b, n4 * 16);
+    if (e == cudaSuccess) e = cudaMalloc((void**)&sink, 16);
+    if (e != cudaSuccess) {
+        cudaFree(a);
+        cudaFree(b);
+        return cuda_err(e, "cudaMalloc");
+    }
+    cudaMemset(a, 0, n4 * 16);
+    cudaMemset(b, 0, n4 * 16);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
+    float best = 1e30f;
+    for (int i = 0; i < 5; ++i) {
+        cudaEventRecord(e0);
+        l2_kernel<<<nsm * 4, 512>>>(a, b, n4, passes, mode, sink);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (i >= 1) best = std::min(best, ms);    // the first launch brings the buffers into L2
+    }
+    e = cudaGetLastError();
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(a);
+    cudaFree(b);
+    cudaFree(sink);
+    if (e != cudaSuccess) return cuda_err(e, "l2_kernel");
+    *gbs = (mode ? 2.0 : 1.0) * n4 * 16 * passes / (best * 1e-3) / 1e9;
     return PM_OK;
 }
 

@@ -618,10 +618,12 @@ __global__ void gen_final_kernel(const cx<T>* vs, const T* p, long long p_stride
     const int b = blockIdx.y;
     if (st[b].done) return;
     const T tol = T(tol_p[b]);
+    cx<T> chk = mk<T>(T(0), T(0));
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
         const long long x = b * n + i;
         const cx<T> v = vs[x];
+        fold_finite(chk, v);
         if (v_star) v_star[x] = v;
         const cx<T> us = replace_mod_exact<T>(v, p[b * p_stride + i], tol);
         if (u_star) u_star[x] = us;
@@ -632,6 +634,7 @@ __global__ void gen_final_kernel(const cx<T>* vs, const T* p, long long p_stride
             if (levels) levels[x] = level_of(th);
         }
     }
+    if (!all_finite(chk)) const_cast<MaskState*>(st)[b].pair_bad = 1;
 }
 
 // Real m -> complex field (the initial iterate's Fourier-plane start).

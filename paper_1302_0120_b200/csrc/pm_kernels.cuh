@@ -59,6 +59,8 @@ struct MaskState {
     int decided;     // last iteration whose record / stop decision is taken
     int zero;        // device-side validation: 1 = p identically zero, 2 = m all dark
     double pend_lit, pend_dark;   // RAAR, sweep path: physical error of the last column sweep's iterate
+    int pair_bad;    // the best-approximation pair v* went non-finite (the reference's Field check
+                     // of provider.inverse in the pair, src/solver.py:202-204: a ValueError)
 };
 
 // One decided iteration, published to host-mapped memory for the host's
@@ -774,8 +776,13 @@ __device__ __forceinline__ void final_task(const FinalArgs<T>& a, int b, int row
 #pragma unroll
     for (int k = 0; k < F::R; ++k) v[k] = act ? ld_field(a.field + o + F::TG * k) : mk<T>(T(0), T(0));
     fft1d<T, LG_L, LG_R, -1, TS>(v, sm, tw, j, sync);
+    cx<T> chk = mk<T>(T(0), T(0));
 #pragma unroll
-    for (int k = 0; k < F::R; ++k) v[k] = cconj(v[k]);                    // v* (normalised)
+    for (int k = 0; k < F::R; ++k) {
+        v[k] = cconj(v[k]);                                                // v* (normalised)
+        fold_finite(chk, v[k]);
+    }
+    if (act && !all_finite(chk)) a.st[b].pair_bad = 1;
     if (a.x) {
         // RAAR: gap of the last iterate, ||P_S x_K - P_M x_K|| with P_M x_K = v*
         const int i = a.ctl.max_iters;

@@ -134,3 +134,18 @@ def make_problem(n_x: int, n_spots: int = 50, seed: int = 7, n_y: int | None = N
     p = g * math.sqrt(float(np.sum(m ** 2)) / float(np.sum(g ** 2)))
     return np.ascontiguousarray(p), np.ascontiguousarray(m)
 
+
+def spot_targets(n_x: int, n_spots: int, seeds, n_y: int | None = None, dtype=np.float64) -> np.ndarray:
+    """Stack of the §8(d) targets m for several seeds (BASELINE config 4: 256
+    distinct OSPs), equal to ``make_problem(n_x, n_spots, seed)[1]`` for each
+    seed, built directly: a radius-1 spot lights its centre pixel only, and m
+    is 1 there, rolled into DFT order. Every target has sum m^2 = n_spots, so
+    one amplitude p serves the whole stack."""
+    spec = GridSpec(n_x, n_x if n_y is None else n_y)
+    seeds = list(seeds)
+    out = np.zeros((len(seeds), spec.n_y, spec.n_x), dtype=dtype)
+    sy, sx = spec.n_y // 2, spec.n_x // 2
+    for i, seed in enumerate(seeds):
+        for j0, k0 in random_spot_centers(spec, n_spots, seed):
+            out[i, (k0 + sy) % spec.n_y, (j0 + sx) % spec.n_x] = 1.0
+    return out

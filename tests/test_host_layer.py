@@ -158,3 +158,13 @@ def test_naive_dft_is_a_public_name_with_the_reference_guard():
     spec = pm.GridSpec(128, 64)
     with pytest.raises(ValueError, match="too large for the O"):
         pm.naive_dft(pm.Field(spec, np.zeros(spec.shape, complex)))
+
+
+def test_spot_targets_equal_make_problem():
+    """The config-4 target stack builder equals make_problem's m per seed."""
+    from paper_1302_0120_b200.patterns import make_problem, spot_targets
+    for n, spots in ((64, 8), (256, 50), (120, 6)):
+        seeds = [1000, 1001, 7]
+        st = spot_targets(n, spots, seeds)
+        for i, sd in enumerate(seeds):
+            assert np.array_equal(st[i], make_problem(n, spots, sd)[1])
