@@ -337,6 +337,148 @@ def run_batch(args, world, rank, local):
         dist.destroy_process_group()
 
 
+# BASELINE.json configs 1, 2, 5 (single mask per GPU): (name, n, tag, algorithm, iters, spots)
+SINGLE_CONFIGS = {
+    1: [("gs_256x256_fp64_100iter_8spots", 256, "double", "gs", 100, 8)],
+    2: [("raar_b0.9_512x512_fp32_200iter_8spots", 512, "single", "raar", 200, 8),
+        ("raar_b0.9_512x512_fp64_200iter_8spots", 512, "double", "raar", 200, 8)],
+    5: [("gs_4096x4096_fp32_100iter_50spots", 4096, "single", "gs", 100, 50),
+        ("gs_2048x2048_fp32_100iter_50spots", 2048, "single", "gs", 100, 50)],
+}
+
+
+def run_single_configs(args, world, rank, local):
+    """--config 1 / 2 / 5: BASELINE.json configs[0], [1], [4] with the same
+    rigour as the headline (device time with CUDA events on the solve's
+    stream, L2 flushed before every step, clocks sampled under load, max over
+    ranks; roofline against the L2 copy roof when the working set fits L2,
+    else HBM; e2e through solve() with float64 host grids). The first
+    workload is the line's value, the others follow under "also"."""
+    import torch
+    import torch.distributed as dist
+    import paper_1302_0120_b200 as pm
+    from paper_1302_0120_b200 import _lib
+    from paper_1302_0120_b200.patterns import make_problem
+    from paper_1302_0120_b200.solver import _params
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    peaks = measured_peaks()
+    hbm = peaks.get("hbm_gbs")
+    l2 = _lib.measure_l2(32 << 20, 50, 1, local)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=f"cuda:{local}")
+    out = []
+    for name, n, tag, algo, K, spots in SINGLE_CONFIGS[args.config]:
+        prec = pm.Precision.from_tag(tag)
+        fdt = prec.float_dtype
+        p, m = make_problem(n, spots, SEED + rank)
+        spec = pm.GridSpec(n, n)
+        plan = pm.transform.get_plan(spec, prec, local)
+        stream = torch.cuda.Stream(device=local)
+        plan.set_stream(stream.cuda_stream)
+        tdt = torch.float32 if fdt == np.float32 else torch.float64
+        d_p = torch.from_numpy(p.astype(fdt)).to(f"cuda:{local}", tdt)
+        d_m = torch.from_numpy(m.astype(fdt)).to(f"cuda:{local}", tdt)
+        d_phase = torch.empty((n, n), dtype=torch.float64, device=f"cuda:{local}")
+        tol_p = np.array([prec.zero_tol(float(p.astype(fdt).max()))])
+        tol_m = np.array([prec.zero_tol(float(m.astype(fdt).max()))])
+        energy = np.array([float((m ** 2).sum())])
+        cfg = pm.SolveConfig(max_iters=K, precision=prec, record_every=K, device=local, algorithm=algo, beta=0.9)
+        prm = _params(cfg, False, False)
+        iters = np.zeros(1, np.int32)
+
+        def solve_device():
+            res = _lib.pm_result()
+            res.phases = _lib.C.c_void_p(d_phase.data_ptr())
+            res.iters_run = _lib.ptr(iters)
+            _lib.check(plan.lib.pm_solve_device(plan.handle, _lib.C.c_void_p(d_p.data_ptr()),
+                                                _lib.C.c_void_p(d_m.data_ptr()), None, 1, prm, _lib.ptr(tol_p),
+                                                _lib.ptr(tol_m), _lib.ptr(energy), res), "pm_solve_device")
+
+        for _ in range(args.warmup):
+            solve_device()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        step_ms = []
+        with ClockSampler(local) as clocks:
+            clocks.wait_first()
+            t_load = time.time()
+            while time.time() - t_load < 0.3:
+                solve_device()
+            launches0 = plan.launch_count()
+            for _ in range(args.steps):
+                with torch.cuda.stream(stream):
+                    flush_l2(flush)
+                    e0 = torch.cuda.Event(enable_timing=True)
+                    e1 = torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                solve_device()
+                with torch.cuda.stream(stream):
+                    e1.record(stream)
+                e1.synchronize()
+                step_ms.append(e0.elapsed_time(e1))
+            launches = plan.launch_count() - launches0
+            time.sleep(0.2)
+        assert iters[0] == K
+        total = torch.tensor([sum(step_ms)], dtype=torch.float64, device=f"cuda:{local}")
+        if world > 1:
+            dist.all_reduce(total, op=dist.ReduceOp.MAX)
+        ms = float(total.item()) / args.steps
+        # e2e: the drop-in solve() with the caller's float64 grids
+        c_in = pm.SlmConstraint(pm.RealGrid(spec, p), prec)
+        m_in = pm.FourierConstraint(pm.RealGrid(spec, m), prec)
+        e2e_ms = []
+        for i in range(args.warmup + min(args.steps, 10)):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            r = pm.solve(c_in, m_in, cfg)
+            if i >= args.warmup:
+                e2e_ms.append((time.perf_counter() - t0) * 1e3)
+            del r
+        e2e_t = torch.tensor([sum(e2e_ms) / len(e2e_ms)], dtype=torch.float64, device=f"cuda:{local}")
+        if world > 1:
+            dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+        csz = 8 if tag == "single" else 16
+        per_iter = (4 * csz + 2 * (csz // 2) + (4 * csz if algo == "raar" else 0)) * n * n   # SURVEY §8(d)
+        achieved = per_iter * K / (ms * 1e-3) / 1e9
+        working = (2 * csz + 2 * (csz // 2) + (2 * csz if algo == "raar" else 0)) * n * n
+        in_l2 = working <= (96 << 20)
+        roof = l2 if in_l2 else hbm
+        out.append({
+            "workload": name, "value": ms / world, "unit": "ms/mask", "ms_per_step": ms,
+            "iters_per_s": K * world / (ms / 1e3), "dtype": "f32" if tag == "single" else "f64",
+            "config": {"workload": name, "n_x": n, "n_y": n, "iters": K, "spots": spots, "seed": SEED,
+                       "algorithm": algo, "beta": 0.9 if algo == "raar" else None, "masks_per_step": world,
+                       "masks_per_rank": 1, "record_every": K, "path": "persistent" if plan.path() == 1 else "sweep-graph",
+                       "l2": "flushed by a 256 MiB write before every timed step",
+                       "parallelism": f"one mask per GPU over {world} GPU(s), no collective"},
+            "e2e": {"value": float(e2e_t.item()) / world, "unit": "ms/mask",
+                    "h2d_bytes_per_step": 2 * n * n * (csz // 2),
+                    "d2h_bytes_per_step": n * n * (8 + 2 * csz) + 3 * K * 8 + 8,
+                    "api": "paper_1302_0120_b200.solve(c, m, cfg), float64 host grids in, SolveResult out"},
+            "roofline": {"bound": "l2" if in_l2 else "hbm", "achieved": achieved, "peak": roof, "unit": "GB/s",
+                         "frac": achieved / roof if roof else None, "traffic": None,
+                         "peak_source": ("measured in this run: pm_measure_l2 32 MiB copy" if in_l2
+                                         else "MEASURED_PEAKS.json hbm_gbs"),
+                         "bytes_per_iter": per_iter, "working_set_bytes": working,
+                         "hbm_frac": achieved / hbm if hbm else None},
+            "clocks": clocks.summary(), "gpu_launches": launches})
+    if rank == 0:
+        first = out[0]
+        line = {"metric": METRIC, "value": first["value"], "unit": "ms/mask", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": first["ms_per_step"], "higher_is_better": False,
+                "scaling": "weak", "vs_baseline": None, "dtype": first["dtype"], "data": "synthetic",
+                "config": first["config"], "iters_per_s": first["iters_per_s"], "e2e": first["e2e"],
+                "roofline": first["roofline"], "clocks": first["clocks"], "gpu_launches": first["gpu_launches"],
+                "baseline_config": args.config, "also": out[1:]}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def flush_l2(buf):
     buf.fill_(1.0)      # 256 MiB write > the 126 MB L2
 
@@ -348,13 +490,17 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--config", type=int, choices=[3, 4], default=3,
-                    help="BASELINE.json config: 3 = one 1024^2 mask per GPU (default, the headline), "
-                         "4 = a 256-mask batch sharded over the GPUs")
+    ap.add_argument("--config", type=int, choices=[1, 2, 3, 4, 5], default=3,
+                    help="BASELINE.json config (1-based): 3 = one 1024^2 mask per GPU (default, the headline), "
+                         "4 = a 256-mask batch sharded over the GPUs, 1 / 2 / 5 = 256^2 fp64 GS / 512^2 RAAR "
+                         "fp32+fp64 / 4096^2 + 2048^2 fp32 GS, one mask per GPU")
     args = ap.parse_args()
     world, rank, local = dist_env()
     if args.config == 4 and args.impl == "ours":
         run_batch(args, world, rank, local)
+        return
+    if args.config in SINGLE_CONFIGS and args.impl == "ours":
+        run_single_configs(args, world, rank, local)
         return
 
     if args.impl == "reference":

@@ -64,6 +64,9 @@ def default_config(tag: str, lg: int) -> tuple[int, int, int]:
 
 def _config(tag: str, lg: int) -> tuple[int, int, int]:
     row, col, nt = default_config(tag, lg)
+    only = os.environ.get("PM_XONLY")                  # experiment overrides for these units only
+    if only and f"{tag}_{lg}" not in only.split(","):
+        return row, col, nt
     env = os.environ.get("PM_LGR")
     if env:
         a = [int(x) for x in env.split(",")]

@@ -699,8 +699,10 @@ __device__ __forceinline__ void row_task(const RowArgs<T>& a, int b, int row, in
         fine_stamp_after(v[F::R - 1], 12 + h);   // row: after FFT 1 / 2
         if (h) break;
         if constexpr (PS) {
-            cp_async_wait<1>();                      // p of this task (the prefetch may stay in flight)
-            sync();
+            if (stage_p || XS) {                     // (resident p: nothing was copied for this task)
+                cp_async_wait<1>();                  // p of this task (the prefetch may stay in flight)
+                sync();
+            }
         }
         if (ALG != 1 && a.mode == kRowGS) {
             // S u = S P_S v = conj(P_S(y; S p)) (src/projections.py:69-74): y = conj(v) is
@@ -933,8 +935,10 @@ __device__ __forceinline__ void col_task(const ColArgs<T>& a, int b, int col0, i
             if (threadIdx.x == 0) next_m();
         } else {
             if constexpr (PS) {
-                cp_async_wait<1>();                  // m of this task (the prefetch may stay in flight)
-                __syncthreads();
+                if (stage_m) {                       // (resident m: nothing was copied for this task)
+                    cp_async_wait<1>();              // m of this task (the prefetch may stay in flight)
+                    __syncthreads();
+                }
             }
             if constexpr (PS) {
                 if (a.mT) {
