@@ -36,7 +36,7 @@ for w in $WHAT; do
       timeout 300 python scripts/paper_config.py > "$OUT/paper.log" 2>&1; echo "paper rc=$?"; cat "$OUT/paper.log" ;;
     full)
       timeout 1200 ncu --set full --clock-control none --import-source on -k regex:solve_kernel -s 2 -c 1 \
-        -o "$OUT/solve_full" -f python scripts/prof_solve.py > "$OUT/full.log" 2>&1
+        -o "$OUT/solve_full" -f python scripts/prof_solve.py 1024 single 100 > "$OUT/full.log" 2>&1
       echo "full rc=$?" ;;
   esac
 done

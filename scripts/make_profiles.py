@@ -102,7 +102,7 @@ def main(src, tag):
         summ = subprocess.run([sys.executable, str(REPO / "scripts" / "ncu_summary.py"), str(sf), "2"],
                               capture_output=True, text=True).stdout
         (prof / f"{tag}_ncu_solve_lines.txt").write_text(
-            "ncu --set full --import-source on of a 20-iteration 1024^2 fp32 solve (scripts/prof_solve.py)\n\n"
+            "ncu --set full --import-source on of a 100-iteration 1024^2 fp32 solve (scripts/prof_solve.py 1024 single 100)\n\n"
             + summ + "\nwarp-stall samples by source line (scripts/ncu_lines.py):\n" + buf.getvalue())
 
 
