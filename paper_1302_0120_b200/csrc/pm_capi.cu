@@ -77,8 +77,7 @@ __global__ void replace_kernel(const cx<T>* in, const T* target, long long tstri
 #pragma unroll
             for (int k = 0; k < 4; ++k) v[k] = ib[i + k];
             auto t_of = [&](int k) -> T { return tb[i + k]; };
-            if (z.ftz) project_regs<false, true>(v, z, t_of, keep);
-            else project_regs<false, false>(v, z, t_of, keep);
+            project_regs<false>(v, z, t_of, keep);
 #pragma unroll
             for (int k = 0; k < 4; ++k) ob[i + k] = v[k];
         } else {

@@ -448,6 +448,7 @@ template <typename C> __device__ __forceinline__ C ld_field(const C* p) { return
 #ifndef PM_FINE
 #define PM_FINE 0
 #endif
+
 struct FineState {
     unsigned long long* p;
     int i;
@@ -711,8 +712,7 @@ __device__ __forceinline__ void row_task(const RowArgs<T>& a, int b, int row, in
             auto t_of = [&](int k) -> T { return inb ? p_at(k) : T(0); };
             auto keep = [](int, cx<T>, cx<T> o) { return o; };
             // false: v = F^-1 v^ was not finite (the reference's Field check)
-            const bool fin = z.ftz ? project_regs<true, true>(v, z, t_of, keep)
-                                   : project_regs<true, false>(v, z, t_of, keep);
+            const bool fin = project_regs<true>(v, z, t_of, keep);
             if (act && !fin) first_bad(&a.st[b].bad, a.it);
         } else if (a.mode == kRowInit) {
             cx<T>* xp = (ALG != 0 && a.x) ? a.x + b * N + (size_t)row * a.nx + j : nullptr;
@@ -996,11 +996,11 @@ __device__ __forceinline__ void col_task(const ColArgs<T>& a, int b, int col0, i
         };
         auto epi = [&](int, cx<T>, cx<T> vh) -> cx<T> { return cscale(vh, a.scale); };
         // false: u^ = F(u_{u_iter}) was not finite, the reference's Field check of iteration u_iter + 1.
-        // Iterations without a gap take a copy of the loop with no fp64 work in it (predicated
-        // conversions and squares would still take issue slots).
         bool fin;
-        if (gneed) fin = z.ftz ? project_regs<true, true>(v, z, t_of, epi_gap) : project_regs<true, false>(v, z, t_of, epi_gap);
-        else fin = z.ftz ? project_regs<true, true>(v, z, t_of, epi) : project_regs<true, false>(v, z, t_of, epi);
+        // iterations without a gap take a copy of the loop with no fp64 work in it
+        // (predicated conversions and squares would still take issue slots)
+        if (gneed) fin = project_regs<true>(v, z, t_of, epi_gap);
+        else fin = project_regs<true>(v, z, t_of, epi);
         if (act && !fin) first_bad(&a.st[b].bad, a.u_iter + 1);
         acc[0] = act ? g2 : 0.0;
     }
