@@ -25,7 +25,10 @@ def run(nx, ny, tag, algo="gs", K=3, path=0, batch=1, rand=False):
         r = pm.solve(pm.SlmConstraint(pm.RealGrid(spec, p), prec), pm.FourierConstraint(pm.RealGrid(spec, m), prec), cfg)
         seen = []
         pm.solve(pm.SlmConstraint(pm.RealGrid(spec, p), prec), pm.FourierConstraint(pm.RealGrid(spec, m), prec), cfg,
-                 on_record=seen.append)
+                 on_record=seen.append)                        # record ring
+        polls = []
+        pm.solve(pm.SlmConstraint(pm.RealGrid(spec, p), prec), pm.FourierConstraint(pm.RealGrid(spec, m), prec), cfg,
+                 on_record=seen.append, should_abort=lambda: polls.append(1) and False)   # lockstep verdicts
         u = pm.Field(spec, r.u_star.data)
         project_fourier(u, pm.FourierConstraint(pm.RealGrid(spec, m), prec), pm.FftProvider(spec, prec))
         reconstruction_log_image(u, pm.FftProvider(spec, prec), float((m ** 2).sum()))
