@@ -63,6 +63,42 @@ __global__ void __launch_bounds__(256, 1) k(const float2* __restrict__ f, float*
             }
         }
     }
+    if (M >= 5) {
+        // store patterns (values from registers; a fence makes the time include completion)
+#pragma unroll
+        for (int q = 0; q < 32; ++q) v[q] = make_float2(q + threadIdx.x, q);
+        __syncthreads();
+        t0 = clock64();
+        float2* g = const_cast<float2*>(f);
+        if (M == 5) {
+            float2* row = g + (size_t)(blk * 8 + w) * L;
+#pragma unroll
+            for (int q = 0; q < 32; ++q) __stcg(row + j + 32 * q, v[q]);
+        } else if (M == 6) {
+            const int c = threadIdx.x & 7, jj = threadIdx.x >> 3;
+            float2* col = g + blk * 8 + c;
+#pragma unroll
+            for (int q = 0; q < 32; ++q) __stcg(col + (size_t)(jj + 32 * q) * L, v[q]);
+        } else {
+            // column block, adjacent columns paired through a shuffle: 16-byte stores
+            const int c = threadIdx.x & 7, jj = threadIdx.x >> 3;
+            const bool odd = c & 1;
+            float4* col = reinterpret_cast<float4*>(g + blk * 8 + (c & ~1));
+#pragma unroll
+            for (int q = 0; q < 32; q += 2) {
+                // even lane keeps row q, odd lane row q+1: exchange the other half
+                const float2 send = odd ? v[q] : v[q + 1];
+                float2 got;
+                got.x = __shfl_xor_sync(0xffffffffu, send.x, 1);
+                got.y = __shfl_xor_sync(0xffffffffu, send.y, 1);
+                const int qq = odd ? q + 1 : q;
+                const float4 o = odd ? make_float4(got.x, got.y, v[q + 1].x, v[q + 1].y)
+                                     : make_float4(v[q].x, v[q].y, got.x, got.y);
+                __stcg(col + ((size_t)(jj + 32 * qq) * L) / 2, o);
+            }
+        }
+        __threadfence();
+    }
     float s = 0.f;
 #pragma unroll
     for (int q = 0; q < 32; ++q) s += v[q].x + v[q].y;
@@ -80,12 +116,14 @@ int main() {
     cudaMalloc(&out, 148 * 256 * 4);
     cudaMalloc(&cyc, 148 * 8);
     const char* names[] = {"", "M1 rows, warp per row (row sweep today)", "M2 [1024][8] column block, (c,j) mapping (column sweep today)",
-                           "M3 tiled row stripe via smem", "M4 tiled column stripe via smem"};
-    for (int m = 1; m <= 4; ++m) {
-        void (*fn)(const float2*, float*, long long*) = m == 1 ? k<1> : m == 2 ? k<2> : m == 3 ? k<3> : k<4>;
+                           "M3 tiled row stripe via smem", "M4 tiled column stripe via smem",
+                           "S5 store rows, warp per row", "S6 store column block, (c,j), 8-byte",
+                           "S7 store column block, shuffle-paired 16-byte"};
+    for (int m = 1; m <= 7; ++m) {
+        void (*fn)(const float2*, float*, long long*) = m == 1 ? k<1> : m == 2 ? k<2> : m == 3 ? k<3> : m == 4 ? k<4>
+                                                      : m == 5 ? k<5> : m == 6 ? k<6> : k<7>;
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
         long long h[148];
-        double med = 0;
         for (int rep = 0; rep < 5; ++rep) {
             fn<<<148, 256, 65536>>>(f, out, cyc);
             cudaMemcpy(h, cyc, 128 * 8, cudaMemcpyDeviceToHost);
