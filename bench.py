@@ -188,9 +188,12 @@ def paper_config(device: int) -> dict:
     from paper_1302_0120_b200.patterns import make_problem
     p, m = make_problem(800, 50, 7, n_y=600)
     cfg = pm.SolveConfig(max_iters=25, precision=pm.SINGLE, record_every=25, device=device)
-    pp = torch.from_numpy(p.astype(np.float32)).pin_memory().numpy()
-    mm = torch.from_numpy(m[None].astype(np.float32)).pin_memory().numpy()
-    out = torch.empty((1, 600, 800), dtype=torch.float64).pin_memory().numpy()
+    from paper_1302_0120_b200 import host_empty
+    pp = host_empty(p.shape, np.float32)
+    pp[...] = p
+    mm = host_empty((1,) + m.shape, np.float32)
+    mm[0] = m
+    out = host_empty((1, 600, 800), np.float64)
     e2e, dev = [], []
     for i in range(13):
         torch.cuda.synchronize()
@@ -287,9 +290,11 @@ def run_batch(args, world, rank, local):
 
     # end to end through solve_stack: the rank's targets uploaded from pinned
     # memory, the 8-bit SLM levels (what an SLM displays) downloaded
-    p_pin = torch.from_numpy(p.astype(np.float32)).pin_memory().numpy()
-    m_pin = torch.from_numpy(ms).pin_memory().numpy()
-    lv_pin = torch.empty((B, N_PIX, N_PIX), dtype=torch.uint8).pin_memory().numpy()
+    p_pin = pm.host_empty(p.shape, np.float32)          # page-locked by the library's runtime
+    p_pin[...] = p
+    m_pin = pm.host_empty(ms.shape, np.float32)
+    m_pin[...] = ms
+    lv_pin = pm.host_empty((B, N_PIX, N_PIX), np.uint8)
     e2e_ms = []
     for i in range(1 + min(args.steps, 5)):
         torch.cuda.synchronize()
@@ -589,9 +594,11 @@ def main():
     assert iters[0] == ITERS and np.isfinite(gaps[0])
 
     # ---- end to end through the public batch API (host buffers, pinned)
-    p_pin = torch.from_numpy(p.astype(np.float32)).pin_memory().numpy()
-    m_pin = torch.from_numpy(m[None].astype(np.float32)).pin_memory().numpy()
-    out_pin = torch.empty((1, N_PIX, N_PIX), dtype=torch.float64).pin_memory().numpy()
+    p_pin = pm.host_empty(p.shape, np.float32)          # page-locked by the library's runtime
+    p_pin[...] = p
+    m_pin = pm.host_empty((1,) + m.shape, np.float32)
+    m_pin[0] = m
+    out_pin = pm.host_empty((1, N_PIX, N_PIX), np.float64)
     e2e_ms = []
     for i in range(args.warmup + args.steps):
         with torch.cuda.stream(stream):

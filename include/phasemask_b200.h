@@ -324,6 +324,12 @@ int pm_debug_phase_stamps(pm_plan *plan, int enable, unsigned long long *out, in
  * `reps`, for the HBM (bytes >> L2) and L2 (bytes << L2) roofs. */
 int pm_measure_copy(int device, long long bytes, int reps, double *gbs);
 
+/* Page-locked host memory from the library's own CUDA runtime (transfers from
+ * it run at full speed and asynchronously; the host layer's cast and output
+ * buffers). Plumbing: no reference counterpart. */
+int pm_host_alloc(long long bytes, void **out);
+int pm_host_free(void *ptr);
+
 /* L2 roof (SURVEY.md §8(d) "Which roof"): `passes` sweeps over an
  * L2-resident buffer of `bytes` inside one launch, L1 bypassed; mode 0 reads
  * only (bytes read), 1 copies (read + write bytes counted). Best of 4. */

@@ -11,6 +11,7 @@ from __future__ import annotations
 import ctypes as C
 import os
 import threading
+import weakref
 from pathlib import Path
 
 import numpy as np
@@ -117,6 +118,8 @@ SIGNATURES = {
     "pm_time_sweep": (_I, [_VP, _I, _I, _I, C.POINTER(C.c_float)]),
     "pm_measure_copy": (_I, [_I, _LL, _I, C.POINTER(_D)]),
     "pm_measure_l2": (_I, [_I, _LL, _I, _I, C.POINTER(_D)]),
+    "pm_host_alloc": (_I, [_LL, C.POINTER(_VP)]),
+    "pm_host_free": (_I, [_VP]),
     "pm_debug_phase_stamps": (_I, [_VP, _I, _VP, _I]),
 }
 
@@ -378,3 +381,55 @@ def measure_l2(nbytes: int, passes: int = 50, mode: int = 1, device: int = 0) ->
     v = C.c_double(0.0)
     check(load().pm_measure_l2(device, nbytes, passes, mode, C.byref(v)), "pm_measure_l2")
     return v.value
+
+
+class _PinnedPool:
+    """Page-locked host buffers from the library's own CUDA runtime
+    (pm_host_alloc). Memory pinned by another runtime in the process (torch's
+    caching host allocator) is not recognised as pinned by the library's
+    copies, which then run at pageable speed; these buffers are. A dropped
+    array's block returns to a per-size free list (bounded)."""
+
+    MAX_CACHED = 1 << 30
+
+    def __init__(self):
+        self.free: dict[int, list[int]] = {}
+        self.cached = 0
+        self.lock = threading.Lock()
+
+    def _release(self, size: int, ptr: int):
+        with self.lock:
+            if self.cached + size <= self.MAX_CACHED:
+                self.free.setdefault(size, []).append(ptr)
+                self.cached += size
+                return
+        try:
+            load().pm_host_free(C.c_void_p(ptr))
+        except Exception:                        # interpreter shutdown: the process frees it
+            pass
+
+    def empty(self, shape, dtype) -> np.ndarray:
+        dtype = np.dtype(dtype)
+        n = int(np.prod(shape)) * dtype.itemsize
+        size = max(4096, (n + 65535) & ~65535)
+        with self.lock:
+            lst = self.free.get(size)
+            ptr = lst.pop() if lst else None
+            if ptr is not None:
+                self.cached -= size
+        if ptr is None:
+            out = C.c_void_p(0)
+            check(load().pm_host_alloc(size, C.byref(out)), "pm_host_alloc")
+            ptr = out.value
+        buf = (C.c_ubyte * size).from_address(ptr)
+        weakref.finalize(buf, self._release, size, ptr)
+        return np.frombuffer(buf, dtype=np.uint8, count=n).view(dtype).reshape(shape)
+
+
+_pool = _PinnedPool()
+
+
+def host_empty(shape, dtype) -> np.ndarray:
+    """An uninitialised C-contiguous array in page-locked memory the library
+    copies from / to at full speed (pass such arrays to the batch API)."""
+    return _pool.empty(shape, dtype)

@@ -14,6 +14,7 @@
 #include <map>
 #include <mutex>
 #include <atomic>
+#include <chrono>
 #include <cstddef>
 #include <set>
 #include <string>
@@ -589,6 +590,10 @@ struct pm_plan {
     int* hostw_h = nullptr;           // {acknowledged iteration, abort request} host view
     int* hostw_d = nullptr;
     int ring_cap = 0;
+    // page-locked staging of the small per-solve transfers (energies, thresholds,
+    // mask states, histories): pageable cudaMemcpyAsync would synchronise the stream
+    unsigned char* hst = nullptr;
+    size_t hst_bytes = 0;
     int solve_grid = 0;               // CTAs of the persistent kernel (0: not available)
     int solve_grid_tma = 0;           // CTAs of its TMA variant (0: not available)
     int path = 0;                     // 0 auto, 1 persistent, 2 sweep graph
@@ -612,7 +617,6 @@ struct pm_plan {
         void* levels = nullptr;
         void* ustar = nullptr;
         void* vstar = nullptr;
-        std::vector<double> h_tolp, h_thrp, h_thrm, h_thrms, h_en, h_thrx;
         bool energy_on_device = false;
         bool tol_on_device = false;
         bool ring = false;            // decisions streamed to ring_h (pm_solve_async)
@@ -621,6 +625,16 @@ struct pm_plan {
 };
 
 namespace {
+
+// PM_TRACE=1: host wall-clock stamps of the solve's stages on stderr (diagnostics).
+inline void trace(const char* what) {
+    static const bool on = getenv("PM_TRACE") != nullptr;
+    if (!on) return;
+    static thread_local auto t0 = std::chrono::steady_clock::now();
+    const auto t = std::chrono::steady_clock::now();
+    fprintf(stderr, "[pm] %8.1f us  %s\n", std::chrono::duration<double, std::micro>(t - t0).count(), what);
+    t0 = t;
+}
 
 // Run control of the session: the reference's loop parameters plus the
 // record ring of a callback solve (pm_solve_async).
@@ -636,6 +650,22 @@ SolveCtl make_ctl(const pm_plan* pl) {
     c.host = pl->s.ring ? (volatile int*)pl->hostw_d : nullptr;
     c.lockstep = (pl->s.ring && pl->s.lockstep) ? 1 : 0;
     return c;
+}
+
+// The plan's page-locked staging area, at least `bytes` (grows; the stream is
+// idle when it is replaced: callers stage only between solves).
+int host_stage(pm_plan* pl, size_t bytes, unsigned char** out) {
+    if (pl->hst_bytes < bytes) {
+        CK(cudaStreamSynchronize(pl->stream));
+        if (pl->hst) cudaFreeHost(pl->hst);
+        pl->hst = nullptr;
+        pl->hst_bytes = 0;
+        const size_t nb = std::max<size_t>(bytes, 64 << 10);
+        CK(cudaHostAlloc((void**)&pl->hst, nb, cudaHostAllocDefault));
+        pl->hst_bytes = nb;
+    }
+    *out = pl->hst;
+    return PM_OK;
 }
 
 RowCfg row_config(const pm_plan* pl) {
@@ -1531,31 +1561,35 @@ int session_setup(pm_plan* pl, const void* d_p, const void* d_m, int batch, cons
                                              batch, tma_m_box(pl));
     // pinned-free small uploads: stage in the session's host vectors, which
     // must outlive the async copies -> keep them in the plan
-    s.h_en.resize(batch);
-    for (int b = 0; b < batch; ++b) s.h_en[b] = energy ? energy[b] : 0.0;
+    // page-locked uploads: [energy][tolp][thrp][thrm][thrms][thrx], batch doubles each
+    unsigned char* stage = nullptr;
+    CKR(host_stage(pl, 6 * (size_t)batch * sizeof(double), &stage));
+    double* h_en = reinterpret_cast<double*>(stage);
+    for (int b = 0; b < batch; ++b) h_en[b] = energy ? energy[b] : 0.0;
     s.energy_on_device = energy == nullptr;
-    CK(cudaMemcpyAsync(pl->energy, s.h_en.data(), batch * sizeof(double), cudaMemcpyHostToDevice, pl->stream));
+    CK(cudaMemcpyAsync(pl->energy, h_en, batch * sizeof(double), cudaMemcpyHostToDevice, pl->stream));
     if (!tol_p) {
         // tolerances from the device-resident p and m (no host pass over them);
         // their partial maxima live in `red` (sized here, outside any capture)
         s.tol_on_device = true;
         return ensure_red(pl, 2 * kTolBlocks * batch);
     }
-    s.h_tolp.resize(batch);
-    s.h_thrp.resize(batch);
-    s.h_thrm.resize(batch);
-    s.h_thrms.resize(batch);
-    s.h_thrx.resize(batch);
+    double* h_tolp = h_en + batch;
+    double* h_thrp = h_tolp + batch;
+    double* h_thrm = h_thrp + batch;
+    double* h_thrms = h_thrm + batch;
+    double* h_thrx = h_thrms + batch;
     for (int b = 0; b < batch; ++b) {
         const double tp = tol_p[prm->p_per_mask ? b : 0];
-        s.h_tolp[b] = tp;
-        zero_thresholds(tp, tol_m[b], pl->prec == PM_SINGLE, &s.h_thrp[b], &s.h_thrm[b], &s.h_thrx[b]);
+        h_tolp[b] = tp;
+        zero_thresholds(tp, tol_m[b], pl->prec == PM_SINGLE, &h_thrp[b], &h_thrm[b], &h_thrx[b]);
+        h_thrms[b] = 0.0;
     }
-    CK(cudaMemcpyAsync(pl->tolp, s.h_tolp.data(), batch * sizeof(double), cudaMemcpyHostToDevice, pl->stream));
-    CK(cudaMemcpyAsync(pl->thrp, s.h_thrp.data(), batch * sizeof(double), cudaMemcpyHostToDevice, pl->stream));
-    CK(cudaMemcpyAsync(pl->thrm, s.h_thrm.data(), batch * sizeof(double), cudaMemcpyHostToDevice, pl->stream));
-    CK(cudaMemcpyAsync(pl->thrms, s.h_thrms.data(), batch * sizeof(double), cudaMemcpyHostToDevice, pl->stream));
-    CK(cudaMemcpyAsync(pl->thrx, s.h_thrx.data(), batch * sizeof(double), cudaMemcpyHostToDevice, pl->stream));
+    CK(cudaMemcpyAsync(pl->tolp, h_tolp, batch * sizeof(double), cudaMemcpyHostToDevice, pl->stream));
+    CK(cudaMemcpyAsync(pl->thrp, h_thrp, batch * sizeof(double), cudaMemcpyHostToDevice, pl->stream));
+    CK(cudaMemcpyAsync(pl->thrm, h_thrm, batch * sizeof(double), cudaMemcpyHostToDevice, pl->stream));
+    CK(cudaMemcpyAsync(pl->thrms, h_thrms, batch * sizeof(double), cudaMemcpyHostToDevice, pl->stream));
+    CK(cudaMemcpyAsync(pl->thrx, h_thrx, batch * sizeof(double), cudaMemcpyHostToDevice, pl->stream));
     return PM_OK;
 }
 
@@ -2006,6 +2040,7 @@ int pm_plan_destroy(pm_plan* pl) {
     if (pl->stamps) cudaFree(pl->stamps);
     if (pl->ring_h) cudaFreeHost(pl->ring_h);
     if (pl->hostw_h) cudaFreeHost(pl->hostw_h);
+    if (pl->hst) cudaFreeHost(pl->hst);
     if (pl->ev0) cudaEventDestroy(pl->ev0);
     if (pl->ev1) cudaEventDestroy(pl->ev1);
     if (pl->own_stream && pl->stream) cudaStreamDestroy(pl->stream);
@@ -2423,7 +2458,9 @@ static int solve_enqueue(pm_plan* pl, const void* d_p, const void* d_m, const vo
                          const pm_params* prm, const double* tol_p, const double* tol_m,
                          const double* energy, pm_result* res, bool host_io, int ring = 0, int lockstep = 0) {
     if (!tol_p != !tol_m) return set_err(PM_ERR_ARG, "tolerance arrays: pass both or neither");
+    trace("solve: enter");
     CKR(session_setup(pl, d_p, d_m, batch, prm, tol_p, tol_m, energy));
+    trace("session_setup");
     auto& s = pl->s;
     s.ring = ring != 0;
     s.lockstep = ring && lockstep;
@@ -2440,9 +2477,11 @@ static int solve_enqueue(pm_plan* pl, const void* d_p, const void* d_m, const vo
         s.ustar = res ? res->u_star : nullptr;
         s.vstar = res ? res->v_star : nullptr;
     }
+    trace("outputs");
     CK(cudaEventRecord(pl->ev0, pl->stream));
     CKR(enqueue_full_solve(pl));
     CK(cudaEventRecord(pl->ev1, pl->stream));
+    trace("enqueue_full_solve");
     return PM_OK;
 }
 
@@ -2463,10 +2502,12 @@ static int solve_collect(pm_plan* pl, pm_result* res, bool host_io) {
         if (res->v_star)
             CK(cudaMemcpyAsync(res->v_star, pl->vstar, batch * N * pl->csz, cudaMemcpyDeviceToHost, pl->stream));
     }
+    trace("D2H enqueued");
     std::vector<int> iters(batch), div(batch);
     int zero = 0, pair_bad = 0;
     CKR(read_records(pl, 1, prm->max_iters, res ? res->gap : nullptr, res ? res->err_lit : nullptr,
                      res ? res->err_dark : nullptr, iters.data(), div.data(), nullptr, &zero, &pair_bad));
+    trace("read_records (synchronised)");
     if (res) {
         if (res->iters_run) std::copy(iters.begin(), iters.end(), res->iters_run);
         if (res->diverged_iter) std::copy(div.begin(), div.end(), res->diverged_iter);
@@ -2496,10 +2537,39 @@ int pm_solve(pm_plan* pl, const void* p, const void* m, const void* m_init, int 
     std::lock_guard<std::mutex> lk(pl->mu);
     CKR(ensure_capacity(pl, batch, prm->max_iters));
     const size_t N = pl->N;
+    static const bool tr = getenv("PM_TRACE") != nullptr;
+    cudaEvent_t ea = nullptr, ed = nullptr;
+    if (tr) {
+        cudaEventCreate(&ea);
+        cudaEventCreate(&ed);
+        cudaEventRecord(ea, pl->stream);
+        trace("pm_solve: before uploads");
+    }
     CK(cudaMemcpyAsync(pl->pbuf, p, (prm->p_per_mask ? batch : 1) * N * pl->rsz, cudaMemcpyHostToDevice,
                        pl->stream));
     CK(cudaMemcpyAsync(pl->mbuf, m, batch * N * pl->rsz, cudaMemcpyHostToDevice, pl->stream));
-    return solve_core(pl, pl->pbuf, pl->mbuf, m_init, batch, prm, tol_p, tol_m, energy, res, true);
+    if (tr) trace("pm_solve: uploads enqueued");
+    cudaEvent_t eb = nullptr;
+    if (tr) {
+        cudaEventCreate(&eb);
+        cudaEventRecord(eb, pl->stream);
+    }
+    const int rc = solve_core(pl, pl->pbuf, pl->mbuf, m_init, batch, prm, tol_p, tol_m, energy, res, true);
+    if (tr) {
+        cudaEventRecord(ed, pl->stream);
+        cudaEventSynchronize(ed);
+        float a = 0, b = 0, c = 0, h = 0;
+        cudaEventElapsedTime(&h, ea, eb);
+        fprintf(stderr, "[pm] p, m uploads alone %.3f ms\n", h);
+        cudaEventDestroy(eb);
+        cudaEventElapsedTime(&a, ea, pl->ev0);
+        cudaEventElapsedTime(&b, pl->ev0, pl->ev1);
+        cudaEventElapsedTime(&c, pl->ev1, ed);
+        fprintf(stderr, "[pm] device timeline: uploads %.3f ms, solve %.3f ms, downloads + records %.3f ms\n", a, b, c);
+        cudaEventDestroy(ea);
+        cudaEventDestroy(ed);
+    }
+    return rc;
 }
 
 int pm_solve_device(pm_plan* pl, const void* d_p, const void* d_m, const void* d_m_init, int batch,
@@ -2780,6 +2850,23 @@ int pm_measure_copy(int device, long long bytes, int reps, double* gbs) {
     cudaFree(b);
     if (e != cudaSuccess) return cuda_err(e, "copy_kernel");
     *gbs = 2.0 * n4 * 16 / (best * 1e-3) / 1e9;
+    return PM_OK;
+}
+
+int pm_host_alloc(long long bytes, void** out) {
+    if (!out || bytes < 0) return set_err(PM_ERR_ARG, "bad arguments");
+    *out = nullptr;
+    cudaError_t e = cudaHostAlloc(out, (size_t)std::max(bytes, 1LL), cudaHostAllocPortable);
+    if (e == cudaErrorMemoryAllocation) {
+        cudaGetLastError();
+        return set_err(PM_ERR_NOMEM, "cudaHostAlloc: out of page-locked memory");
+    }
+    CK(e);
+    return PM_OK;
+}
+
+int pm_host_free(void* p) {
+    if (p) CK(cudaFreeHost(p));
     return PM_OK;
 }
 
