@@ -1,13 +1,14 @@
 """Benchmark: ms per 1024^2 phase mask (100 GS iterations, fp32) on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 1..5]
 
-Workload (BASELINE.json configs[2]): a 1024x1024 SLM, 50-spot target and
-Gaussian-beam amplitude from the SURVEY.md §8(d) generator (synthetic,
-seeded), 100 Gerchberg-Saxton iterations in fp32, one mask per GPU per step
-(weak scaling across ranks, no collective on the iteration path). Metrics
-are recorded with record_every = iters, as the reference's own bench does
-(src/bench.py:100-102); the GPU computes the gap every iteration anyway.
+Default workload (BASELINE.json configs[2], "config 3"): a 1024x1024 SLM,
+50-spot target and Gaussian-beam amplitude from the SURVEY.md §8(d)
+generator (synthetic, seeded), 100 Gerchberg-Saxton iterations in fp32, one
+mask per GPU per step (weak scaling across ranks, no collective on the
+iteration path). Metrics are recorded with record_every = iters, as the
+reference's own bench does (src/bench.py:100-102), so the gap and the
+physical errors are computed on the first and last iterations only.
 
 value  = device time per mask (inputs resident in HBM, CUDA events on the
          solve's stream, L2 flushed by a 256 MiB write before every step),
@@ -16,8 +17,14 @@ e2e    = the same through the public host API, frame by frame
          (paper_1302_0120_b200.batch.solve_stream): every step uploads p and m
          from pinned memory and downloads the float64 mask and histories; the
          neighbouring frames' copies overlap each solve. e2e.latency = one
-         synchronous solve_stack call per mask (copies not overlapped).
-roofline / cpu_baseline / clocks / gpu_launches: see DESIGN.md §Measurement.
+         synchronous solve_stack call per mask; e2e.dropin = the reference's
+         entry point solve(c, m, cfg) with float64 host grids, SolveResult out.
+roofline = the solve's algorithmic bytes / time against the L2-resident copy
+         bandwidth measured in the same run (the field stays in L2), with the
+         HBM fraction beside it; cpu_baseline / clocks / gpu_launches: see
+         DESIGN.md §8.
+--config 1 / 2 / 4 / 5 measure the other BASELINE configs the same way
+(4: a 256-mask batch sharded over the ranks).
 
 Under torchrun each rank drives cuda:LOCAL_RANK; rank 0 prints one JSON line.
 """
