@@ -79,6 +79,13 @@ __global__ void __launch_bounds__(256, 1) k(const float2* __restrict__ f, float*
             float2* col = g + blk * 8 + c;
 #pragma unroll
             for (int q = 0; q < 32; ++q) __stcg(col + (size_t)(jj + 32 * q) * L, v[q]);
+        } else if (M == 8) {
+            // transposed store straight from the warp-per-row registers: element (row r0 + w,
+            // column j + 32 q) to T[(j + 32 q) * L + r0 + w] (8-byte pieces; the CTA's 8 warps
+            // fill each 64-byte segment)
+            float2* t = g + blk * 8 + w;
+#pragma unroll
+            for (int q = 0; q < 32; ++q) __stcg(t + (size_t)(j + 32 * q) * L, v[q]);
         } else {
             // column block, adjacent columns paired through a shuffle: 16-byte stores
             const int c = threadIdx.x & 7, jj = threadIdx.x >> 3;
@@ -118,10 +125,10 @@ int main() {
     const char* names[] = {"", "M1 rows, warp per row (row sweep today)", "M2 [1024][8] column block, (c,j) mapping (column sweep today)",
                            "M3 tiled row stripe via smem", "M4 tiled column stripe via smem",
                            "S5 store rows, warp per row", "S6 store column block, (c,j), 8-byte",
-                           "S7 store column block, shuffle-paired 16-byte"};
-    for (int m = 1; m <= 7; ++m) {
+                           "S7 store column block, shuffle-paired 16-byte", "S8 transposed store, 8-byte pieces from rows"};
+    for (int m = 1; m <= 8; ++m) {
         void (*fn)(const float2*, float*, long long*) = m == 1 ? k<1> : m == 2 ? k<2> : m == 3 ? k<3> : m == 4 ? k<4>
-                                                      : m == 5 ? k<5> : m == 6 ? k<6> : k<7>;
+                                                      : m == 5 ? k<5> : m == 6 ? k<6> : m == 7 ? k<7> : k<8>;
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
         long long h[148];
         for (int rep = 0; rep < 5; ++rep) {
