@@ -174,16 +174,31 @@ def _host_empty(shape, dtype) -> np.ndarray:
     return np.empty(shape, dtype=dtype)
 
 
+_CAST_POOL = None
+_CAST_THREADED_MIN = 8 << 20
+
+
 def _host_cast(a: np.ndarray, dtype) -> np.ndarray:
     """`a` as a C-contiguous `dtype` array; when a cast is needed anyway it is
-    written into (large: page-locked) memory from _host_empty. One thread: a
-    cast spread over several cores leaves the data dirty in their caches, and
-    the upload that follows then ran at ~8 GB/s instead of ~50 (measured:
-    solve() at 1024^2 fp32, 3.9 -> 3.4 ms end to end)."""
+    written into (large: page-locked) memory from _host_empty. Up to 8 MB on
+    one thread: a cast spread over several cores leaves the data dirty in their
+    caches, and the upload that follows then ran at ~8 GB/s instead of ~50
+    (solve() at 1024^2 fp32: 3.9 -> 3.4 ms end to end); larger arrays, whose
+    cast dominates, on 8 threads (numpy releases the GIL in the copy)."""
+    global _CAST_POOL
     if a.dtype == np.dtype(dtype) and a.flags.c_contiguous:
         return a
     out = _host_empty(a.shape, dtype)
-    np.copyto(out, a, casting="unsafe")
+    if out.nbytes < _CAST_THREADED_MIN or a.ndim < 1 or a.shape[0] < 8:
+        np.copyto(out, a, casting="unsafe")
+        return out
+    if _CAST_POOL is None:
+        from concurrent.futures import ThreadPoolExecutor
+        _CAST_POOL = ThreadPoolExecutor(max(1, min(8, os.cpu_count() or 1)), thread_name_prefix="pm-cast")
+    k = _CAST_POOL._max_workers
+    bounds = np.linspace(0, a.shape[0], k + 1).astype(int)
+    list(_CAST_POOL.map(lambda i: np.copyto(out[bounds[i]:bounds[i + 1]], a[bounds[i]:bounds[i + 1]],
+                                            casting="unsafe"), range(k)))
     return out
 
 
