@@ -4,6 +4,7 @@
 // stand-alone transform / projection / reduction entry points and the
 // measurement helpers used by bench.py.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX ranges (ncu --nvtx / nsys)
 #include <cudaTypedefs.h>
 
 #include <algorithm>
@@ -625,6 +626,13 @@ struct pm_plan {
 };
 
 namespace {
+
+// NVTX range of one entry point (scope-bound).
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangPop_(); }
+    static void nvtxRangPop_() { nvtxRangePop(); }
+};
 
 // PM_TRACE=1: host wall-clock stamps of the solve's stages on stderr (diagnostics).
 inline void trace(const char* what) {
@@ -2108,6 +2116,7 @@ int pm_fft2_device(pm_plan* pl, const void* d_in, void* d_out, int direction, in
 }
 
 int pm_fft2(pm_plan* pl, const void* in, void* out, int direction, int batch) {
+    NvtxRange nvtx_("pm_fft2");
     CKR(check_plan(pl));
     if (direction != PM_FORWARD && direction != PM_INVERSE)
         return set_err(PM_ERR_ARG, "direction must be -1 (forward) or +1 (inverse)");
@@ -2531,6 +2540,7 @@ static int solve_core(pm_plan* pl, const void* d_p, const void* d_m, const void*
 int pm_solve(pm_plan* pl, const void* p, const void* m, const void* m_init, int batch,
              const pm_params* prm, const double* tol_p, const double* tol_m, const double* energy,
              pm_result* res) {
+    NvtxRange nvtx_("pm_solve");
     CKR(check_plan(pl));
     if (!p || !m) return set_err(PM_ERR_ARG, "null p or m");
     CKR(validate_params(prm, batch));
@@ -2575,6 +2585,7 @@ int pm_solve(pm_plan* pl, const void* p, const void* m, const void* m_init, int 
 int pm_solve_device(pm_plan* pl, const void* d_p, const void* d_m, const void* d_m_init, int batch,
                     const pm_params* prm, const double* tol_p, const double* tol_m, const double* energy,
                     pm_result* res) {
+    NvtxRange nvtx_("pm_solve_device");
     CKR(check_plan(pl));
     if (!d_p || !d_m) return set_err(PM_ERR_ARG, "null p or m");
     std::lock_guard<std::mutex> lk(pl->mu);
@@ -2591,6 +2602,7 @@ static_assert(kRecPublished == PM_REC_PUBLISHED && kRecRecorded == PM_REC_RECORD
 int pm_solve_async(pm_plan* pl, const void* p, const void* m, const void* m_init, const pm_params* prm,
                    const double* tol_p, const double* tol_m, const double* energy, int lockstep,
                    pm_result* res) {
+    NvtxRange nvtx_("pm_solve_async");
     CKR(check_plan(pl));
     if (!p || !m) return set_err(PM_ERR_ARG, "null p or m");
     CKR(validate_params(prm, 1));
@@ -2663,6 +2675,7 @@ int pm_solve_answer(pm_plan* pl, int iter, int abort) {
 }
 
 int pm_solve_wait(pm_plan* pl, pm_result* res) {
+    NvtxRange nvtx_("pm_solve_wait");
     CKR(check_plan(pl));
     std::lock_guard<std::mutex> lk(pl->mu);
     if (!pl->s.active || !pl->s.ring) return set_err(PM_ERR_ARG, "no streamed solve in progress (pm_solve_async)");
