@@ -395,7 +395,8 @@ class _PinnedPool:
     def __init__(self):
         self.free: dict[int, list[int]] = {}
         self.cached = 0
-        self.lock = threading.Lock()
+        # re-entrant: a finaliser (returning a block) may run while this thread holds it
+        self.lock = threading.RLock()
 
     def _release(self, size: int, ptr: int):
         with self.lock:
