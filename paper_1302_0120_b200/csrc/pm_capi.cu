@@ -702,11 +702,10 @@ ColCfg col_config(const pm_plan* pl) {
 
 void free_buffers(pm_plan* pl) {
     void* bufs[] = {pl->field, pl->tmp, pl->pbuf, pl->mbuf, pl->phases, pl->levels, pl->ustar,
-                    pl->vstar, pl->st, pl->hist, pl->part, pl->ctr, pl->tolp, pl->thrp,
-                    pl->thrm, pl->thrms, pl->escale, pl->energy, pl->psum};
+                    pl->vstar, pl->st, pl->hist, pl->part, pl->ctr, pl->escale, pl->energy, pl->psum};
     for (void* b : bufs)
         if (b) cudaFree(b);
-    void* rbufs[] = {pl->field2, pl->xbuf, pl->rpart, pl->thrx, pl->mT, pl->ps};
+    void* rbufs[] = {pl->field2, pl->xbuf, pl->rpart, pl->mT, pl->ps};
     for (void* b : rbufs)
         if (b) cudaFree(b);
     pl->field2 = pl->xbuf = pl->mT = pl->ps = nullptr;
@@ -785,13 +784,15 @@ int ensure_capacity(pm_plan* pl, int batch, int max_iters) {
     CK(cudaMalloc((void**)&pl->hist, (size_t)cap * hcap * 4 * sizeof(double)));
     CK(cudaMalloc((void**)&pl->part, (size_t)2 * cap * nb * 3 * sizeof(double)));
     CK(cudaMalloc((void**)&pl->ctr, (size_t)cap * sizeof(unsigned)));
-    CK(cudaMalloc((void**)&pl->tolp, cap * sizeof(double)));
-    CK(cudaMalloc((void**)&pl->thrp, cap * sizeof(double)));
-    CK(cudaMalloc((void**)&pl->thrm, cap * sizeof(double)));
-    CK(cudaMalloc((void**)&pl->thrms, cap * sizeof(double)));
-    CK(cudaMalloc((void**)&pl->thrx, cap * sizeof(double)));
+    // the per-mask scalars in one block, [energy][tolp][thrp][thrm][thrms][thrx] (cap
+    // each): a solve with host tolerances uploads them in one copy (session_setup)
+    CK(cudaMalloc((void**)&pl->energy, 6 * (size_t)cap * sizeof(double)));
+    pl->tolp = pl->energy + cap;
+    pl->thrp = pl->tolp + cap;
+    pl->thrm = pl->thrp + cap;
+    pl->thrms = pl->thrm + cap;
+    pl->thrx = pl->thrms + cap;
     CK(cudaMalloc((void**)&pl->escale, cap * sizeof(double)));
-    CK(cudaMalloc((void**)&pl->energy, cap * sizeof(double)));
     CK(cudaMalloc((void**)&pl->psum, (size_t)2 * cap * 32 * sizeof(double)));
     CK(cudaMemsetAsync(pl->ctr, 0, (size_t)cap * sizeof(unsigned), pl->stream));
     CK(cudaMemsetAsync(pl->st, 0, cap * sizeof(MaskState), pl->stream));
@@ -1565,39 +1566,39 @@ int session_setup(pm_plan* pl, const void* d_p, const void* d_m, int batch, cons
         CKR(ensure_ps(pl, prm->p_per_mask ? batch : 1));
         s.ps = pl->ps;
     }
-    pl->tm_m_ok = !pl->generic && tma_encode(&pl->tm_m, const_cast<void*>(d_m), pl->prec == PM_SINGLE, pl->nx, pl->ny,
-                                             batch, tma_m_box(pl));
+    // (m's tensor map only where the TMA build can run: several column tasks per CTA)
+    pl->tm_m_ok = !pl->generic && tma_wanted(pl) &&
+                  tma_encode(&pl->tm_m, const_cast<void*>(d_m), pl->prec == PM_SINGLE, pl->nx, pl->ny, batch,
+                             tma_m_box(pl));
     // pinned-free small uploads: stage in the session's host vectors, which
     // must outlive the async copies -> keep them in the plan
-    // page-locked uploads: [energy][tolp][thrp][thrm][thrms][thrx], batch doubles each
+    // page-locked uploads mirroring the device block [energy][tolp][thrp][thrm][thrms][thrx]
+    // (cap doubles each): one copy (each small copy costs several microseconds of stream time)
+    const size_t cap = (size_t)pl->cap;
     unsigned char* stage = nullptr;
-    CKR(host_stage(pl, 6 * (size_t)batch * sizeof(double), &stage));
+    CKR(host_stage(pl, 6 * cap * sizeof(double), &stage));
     double* h_en = reinterpret_cast<double*>(stage);
     for (int b = 0; b < batch; ++b) h_en[b] = energy ? energy[b] : 0.0;
     s.energy_on_device = energy == nullptr;
-    CK(cudaMemcpyAsync(pl->energy, h_en, batch * sizeof(double), cudaMemcpyHostToDevice, pl->stream));
     if (!tol_p) {
+        CK(cudaMemcpyAsync(pl->energy, h_en, batch * sizeof(double), cudaMemcpyHostToDevice, pl->stream));
         // tolerances from the device-resident p and m (no host pass over them);
         // their partial maxima live in `red` (sized here, outside any capture)
         s.tol_on_device = true;
         return ensure_red(pl, 2 * kTolBlocks * batch);
     }
-    double* h_tolp = h_en + batch;
-    double* h_thrp = h_tolp + batch;
-    double* h_thrm = h_thrp + batch;
-    double* h_thrms = h_thrm + batch;
-    double* h_thrx = h_thrms + batch;
+    double* h_tolp = h_en + cap;
+    double* h_thrp = h_tolp + cap;
+    double* h_thrm = h_thrp + cap;
+    double* h_thrms = h_thrm + cap;
+    double* h_thrx = h_thrms + cap;
     for (int b = 0; b < batch; ++b) {
         const double tp = tol_p[prm->p_per_mask ? b : 0];
         h_tolp[b] = tp;
         zero_thresholds(tp, tol_m[b], pl->prec == PM_SINGLE, &h_thrp[b], &h_thrm[b], &h_thrx[b]);
         h_thrms[b] = 0.0;
     }
-    CK(cudaMemcpyAsync(pl->tolp, h_tolp, batch * sizeof(double), cudaMemcpyHostToDevice, pl->stream));
-    CK(cudaMemcpyAsync(pl->thrp, h_thrp, batch * sizeof(double), cudaMemcpyHostToDevice, pl->stream));
-    CK(cudaMemcpyAsync(pl->thrm, h_thrm, batch * sizeof(double), cudaMemcpyHostToDevice, pl->stream));
-    CK(cudaMemcpyAsync(pl->thrms, h_thrms, batch * sizeof(double), cudaMemcpyHostToDevice, pl->stream));
-    CK(cudaMemcpyAsync(pl->thrx, h_thrx, batch * sizeof(double), cudaMemcpyHostToDevice, pl->stream));
+    CK(cudaMemcpyAsync(pl->energy, h_en, 6 * cap * sizeof(double), cudaMemcpyHostToDevice, pl->stream));
     return PM_OK;
 }
 
@@ -1851,14 +1852,17 @@ int read_records(pm_plan* pl, int first, int last, double* gap, double* lit, dou
                  int* iters, int* diverged, int* aborted = nullptr, int* zero = nullptr, int* pair_bad = nullptr) {
     auto& s = pl->s;
     const int B = s.batch, K = s.prm.max_iters;
-    std::vector<MaskState> st(B);
-    CK(cudaMemcpyAsync(st.data(), pl->st, B * sizeof(MaskState), cudaMemcpyDeviceToHost, pl->stream));
-    std::vector<double> h;
-    if (gap || lit || dark) {
-        h.resize((size_t)B * pl->hist_cap * 4);
-        CK(cudaMemcpyAsync(h.data(), pl->hist, h.size() * sizeof(double), cudaMemcpyDeviceToHost,
+    // page-locked download area after the uploads' part of the staging buffer
+    const size_t up = 6 * (size_t)pl->cap * sizeof(double);
+    const size_t nh = (gap || lit || dark) ? (size_t)B * pl->hist_cap * 4 : 0;
+    unsigned char* stage = nullptr;
+    CKR(host_stage(pl, up + B * sizeof(MaskState) + nh * sizeof(double) + 16, &stage));
+    MaskState* st = reinterpret_cast<MaskState*>(stage + up);
+    const double* h = reinterpret_cast<const double*>(stage + up + ((B * sizeof(MaskState) + 15) & ~(size_t)15));
+    CK(cudaMemcpyAsync(st, pl->st, B * sizeof(MaskState), cudaMemcpyDeviceToHost, pl->stream));
+    if (nh)
+        CK(cudaMemcpyAsync(const_cast<double*>(h), pl->hist, nh * sizeof(double), cudaMemcpyDeviceToHost,
                            pl->stream));
-    }
     CK(cudaStreamSynchronize(pl->stream));
     if (zero) *zero = 0;
     if (pair_bad) *pair_bad = 0;
@@ -1868,7 +1872,7 @@ int read_records(pm_plan* pl, int first, int last, double* gap, double* lit, dou
         if (iters) iters[b] = st[b].iters_run;
         if (diverged) diverged[b] = st[b].diverged;
         if (aborted) aborted[b] = st[b].aborted;
-        if (!h.empty()) {
+        if (nh) {
             for (int i = first; i <= last && i <= K; ++i) {
                 const double* e = &h[((size_t)b * pl->hist_cap + (i - 1)) * 4];
                 const bool ok = e[3] != 0.0;
