@@ -1313,10 +1313,18 @@ int gen_col_sweep(pm_plan* pl, int u_iter, int metrics_only, int all_masks) {
     const dim3 grid((pl->nx + TC - 1) / TC, pl->s.batch);
     GenSolveArgs g = gen_args(pl);
     g.nblk = (int)grid.x;
+    // does iterate u_iter need its decision in this sweep (see gen_col_sweep_kernel)
+    const pm_params& prm = pl->s.prm;
+    const bool raar = prm.algorithm == PM_ALGO_RAAR;
+    const bool rec = u_iter >= 1 && (u_iter - 1) % prm.record_every == 0;
+    const int need_dec = (metrics_only || all_masks ||
+                          (raar ? rec
+                                : (rec || prm.early_stop_tol >= 0.0 || pl->s.lockstep || u_iter >= prm.max_iters)))
+                             ? 1 : 0;
     CK(cudaLaunchKernelEx(pdl_config(grid, pl->gnt_c, pl->gsm_c, pl->stream).get(), gen_col_sweep_kernel<T>,
                           (cx<T>*)pl->tmp, (const T*)pl->s.m, (const T*)pl->s.mT, (const double*)pl->thrm,
                           (const double*)pl->escale, (const cx<T>*)pl->gtwy, pl->gy, pl->nx, lg_of(TC), g, u_iter,
-                          metrics_only, all_masks, pl->s.prm.algorithm == PM_ALGO_RAAR ? 1 : 0));
+                          metrics_only, all_masks, raar ? 1 : 0, need_dec));
     pl->launches++;
     return PM_OK;
 }

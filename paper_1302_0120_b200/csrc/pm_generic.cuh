@@ -398,7 +398,7 @@ struct GenSolveArgs {
 template <typename T>
 __global__ void gen_col_sweep_kernel(cx<T>* w, const T* m, const T* mT, const double* thr_m, const double* escale,
                                      const cx<T>* __restrict__ tw, GenPlan gp, int nx, int lgTC, GenSolveArgs g,
-                                     int u_iter, int metrics_only, int all_masks, int raar) {
+                                     int u_iter, int metrics_only, int all_masks, int raar, int need_dec) {
     extern __shared__ __align__(16) unsigned char smraw[];
     const int TC = 1 << lgTC, L = gp.L;
     GenSmem<T> sm(smraw, L, TC);
@@ -407,7 +407,11 @@ __global__ void gen_col_sweep_kernel(cx<T>* w, const T* m, const T* mT, const do
     const int b = blockIdx.y;
     MaskState* st = g.st + b;
     if (st->done || (!all_masks && st->stop)) return;
-    const bool dec = u_iter >= 1 && st->decided < u_iter && !st->stop;
+    // need_dec (host): a record, early stopping, a host verdict or max_iters wants
+    // this iterate decided now; otherwise the sweep skips the metrics and the
+    // per-mask ticket (a non-finite iterate's first iteration stays in `bad`
+    // until the next decision)
+    const bool dec = need_dec && u_iter >= 1 && st->decided < u_iter && !st->stop;
     const bool rec = dec && recorded(g.ctl, u_iter);
     // RAAR: only lit / dark here (kept in the mask state); the gap and the
     // decision come from the next row sweep, where x and P_M x meet
