@@ -657,6 +657,7 @@ SolveCtl make_ctl(const pm_plan* pl) {
     c.ring = pl->s.ring ? pl->ring_d : nullptr;
     c.host = pl->s.ring ? (volatile int*)pl->hostw_d : nullptr;
     c.lockstep = (pl->s.ring && pl->s.lockstep) ? 1 : 0;
+    c.decide_all = pl->s.stepping ? 1 : 0;
     return c;
 }
 

@@ -89,6 +89,7 @@ struct SolveCtl {
     RingSlot* ring;     // host-mapped [max_iters] (device view), null: no streaming (single mask)
     volatile int* host; // host-mapped {acknowledged iteration, abort request}
     int lockstep;       // every iteration waits for the host's verdict (should_abort)
+    int decide_all;     // decide every iterate (the stepping API reads state after each step)
 };
 
 // Iterate i needs its gap: recorded, or early stopping is on (src/solver.py:173-174).
@@ -96,6 +97,12 @@ __host__ __device__ __forceinline__ bool gap_needed(const SolveCtl& c, int i) {
     return (i - 1) % c.record_every == 0 || c.early_tol >= 0.0;
 }
 __host__ __device__ __forceinline__ bool recorded(const SolveCtl& c, int i) { return (i - 1) % c.record_every == 0; }
+// Iterate i must be decided when it is reached (record, early stop, a host verdict,
+// max_iters); other iterates' decisions can wait (a non-finite iterate's first
+// iteration stays in MaskState::bad until the next decision).
+__host__ __device__ __forceinline__ bool decision_needed(const SolveCtl& c, int i) {
+    return gap_needed(c, i) || c.lockstep || c.decide_all || i >= c.max_iters;
+}
 
 // Row-sweep modes.
 enum RowMode : int {
@@ -1062,7 +1069,8 @@ __global__ void __launch_bounds__(256) row_iter_kernel(RowArgs<T> a) {
     if (st->stop | st->done) return;
     // RAAR: this sweep measures the gap of x_{it-1}; the last CTA decides it
     const int gi = a.it - 1;
-    const bool dec = a.mode >= kRowRaar && gi >= 1 && st->decided < gi;
+    const bool dec = a.mode >= kRowRaar && gi >= 1 && st->decided < gi &&
+                     (a.mode == kRowProbe || decision_needed(a.ctl, gi));
     const int G = blockDim.x / F::TG;
     const int g = threadIdx.x / F::TG, j = threadIdx.x % F::TG;
     row_task<T, LG_L, LG_R>(a, b, blockIdx.x * G + g, j, reinterpret_cast<cx<T>*>(smraw) + g * F::SM, a.twf,
@@ -1110,6 +1118,7 @@ __global__ void __launch_bounds__(col_max_threads<LG_L, LG_R>()) col_iter_kernel
     col_task<T, LG_L, LG_R, 0>(a, b, blockIdx.x * C, C, reinterpret_cast<cx<T>*>(smraw), a.twf, nullptr, true,
                                acc);
     if (a.mode < 2 || a.u_iter < 1) return;
+    if (!a.raar && !decision_needed(a.ctl, a.u_iter)) return;   // no metrics, no ticket
     double tot[3];
     if (a.raar) {
         // lit/dark of x_{u_iter}, kept for the decision the next row sweep takes
