@@ -1023,6 +1023,11 @@ int launch_solve(pm_plan* pl, int do_init, int it_begin, int it_end, int do_fina
         a.res = (!off && !use_tma && rows_per_cta <= G && col_tasks <= grid) ? 1 : 0;
     }
     a.tma = use_tma ? 1 : 0;
+    {   // z' written back by TMA stores from the exchange buffer (PM_NO_TMA_STORE: st.global)
+        static const bool off = getenv("PM_NO_TMA_STORE") != nullptr;
+        a.tma_out = (use_tma && !off && pl->tm_field_ok) ? 1 : 0;
+        a.tm_out = pl->tm_field;
+    }
     const void* fn = use_tma ? (raar ? k.solve_raar_tma : k.solve_tma) : (raar ? k.solve_raar : k.solve);
     void* args[] = {&a};
     cudaLaunchConfig_t cfg = {};
@@ -2822,14 +2827,14 @@ int pm_time_sweep(pm_plan* pl, int which, int batch, int reps, float* avg_ms) {
 int pm_debug_phase_stamps(pm_plan* pl, int enable, unsigned long long* out, int n) {
     CKR(check_plan(pl));
     if (enable) {
-        const size_t n_st = (size_t)std::max(pl->solve_grid, 1) * kStampsPerCta;
+        const size_t n_st = (size_t)std::max(pl->solve_grid, 1) * 1024;   // fits PM_FINE rows
         if (!pl->stamps) CK(cudaMalloc((void**)&pl->stamps, n_st * sizeof(unsigned long long)));
         CK(cudaMemset(pl->stamps, 0, n_st * sizeof(unsigned long long)));
         return PM_OK;
     }
     if (out && pl->stamps) {
         CK(cudaStreamSynchronize(pl->stream));
-        const size_t n_st = (size_t)std::max(pl->solve_grid, 1) * kStampsPerCta;
+        const size_t n_st = (size_t)std::max(pl->solve_grid, 1) * 1024;   // fits PM_FINE rows
         CK(cudaMemcpy(out, pl->stamps, std::min<size_t>(n, n_st) * sizeof(unsigned long long),
                       cudaMemcpyDeviceToHost));
     }

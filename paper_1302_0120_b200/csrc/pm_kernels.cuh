@@ -467,7 +467,7 @@ __device__ __forceinline__ FineState& fine_state() {
 __device__ __forceinline__ void fine_init(unsigned long long* stamps) {
     if constexpr (PM_FINE) {
         if (threadIdx.x == 0) {
-            fine_state().p = stamps ? stamps + (size_t)blockIdx.x * 256 + 128 : nullptr;
+            fine_state().p = stamps ? stamps + (size_t)blockIdx.x * 1024 + 128 : nullptr;
             fine_state().i = 0;
         }
         __syncthreads();
@@ -477,7 +477,7 @@ __device__ __forceinline__ void fine_stamp(int id) {
     if constexpr (PM_FINE) {
         if (threadIdx.x == 0) {
             FineState& s = fine_state();
-            if (s.p && s.i < 126) {
+            if (s.p && s.i < 894) {
                 s.p[s.i] = id;
                 s.p[s.i + 1] = clock64();
                 s.i += 2;
@@ -491,7 +491,7 @@ __device__ __forceinline__ void fine_stamp_after(V x, int id) {
     if constexpr (PM_FINE) {
         if (threadIdx.x == 0) {
             FineState& s = fine_state();
-            if (s.p && x.x == 1.2345e-30f && x.y == 5.4321e-30f) s.p[127] = 0;
+            if (s.p && x.x == 1.2345e-30f && x.y == 5.4321e-30f) s.p[895] = 0;
         }
         fine_stamp(id);
     }
@@ -558,6 +558,21 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
         "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
         ::"r"(smem_u32(dst)), "l"(map), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
         : "memory");
+}
+
+// TMA tensor store from shared memory (bulk async-group of the issuing thread).
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int x, int y, int z) {
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];"
+                 ::"l"(map), "r"(x), "r"(y), "r"(z), "r"(smem_u32(src)) : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// the issuing thread's stores have read their shared-memory source
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+// ... and are complete in global memory (then ordered before the generic
+// proxy's later accesses: the grid barrier's release publishes them)
+__device__ __forceinline__ void bulk_wait_all() {
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
 // No prefetch: the sweep kernels and single-task phases.
@@ -649,7 +664,7 @@ struct MtStride {
 // groups per task, in commit order: [p of this task] [next task's field],
 // so the projection waits for one group and leaves the prefetch in flight.
 // `xs` (XS, RAAR): this row's slice of x staged with p.
-template <typename T, int LG_L, int LG_R, class Sync, int ALG = -1, bool TS = false, bool PS = false,
+template <typename T, int LG_L, int LG_R, class Sync, int ALG = -1, int TS = 0, bool PS = false,
           class Prefetch = NoPrefetch, bool XS = false>
 __device__ __forceinline__ void row_task(const RowArgs<T>& a, int b, int row, int j, cx<T>* sm,
                                          const twe<T>* tw, T* ps, bool inb_arg, bool live, Sync sync,
@@ -774,7 +789,7 @@ __device__ __forceinline__ void row_task(const RowArgs<T>& a, int b, int row, in
 // Best-approximation pair for one row: v* = P_M u_K = S * RowIFFT(z')
 // = S * conj(RowFFT(conj z')), u* = P_S v*, mask = phases_of(u*, zero_tol_p)
 // (src/solver.py:201-206, src/grid.py:168-176).
-template <typename T, int LG_L, int LG_R, bool TS = false, class Sync>
+template <typename T, int LG_L, int LG_R, int TS = 0, class Sync>
 __device__ __forceinline__ void final_task(const FinalArgs<T>& a, int b, int row, int j, cx<T>* sm,
                                            const twe<T>* tw, bool act, Sync sync) {
     using F = FftShape<LG_L, LG_R>;
@@ -841,9 +856,11 @@ struct TmaTask {
     unsigned long long* bars;     // [0] input, [1] m
     unsigned parity;
     int MC;
+    const CUtensorMap* out;       // the output z' is stored by TMA through the exchange buffer (null: st.global)
+    int ox, oz;                   // its box origin (float column 2*col0, mask)
 };
 
-template <typename T, int LG_L, int LG_R, int NX, bool TS = false, bool PS = false, int CC = 0,
+template <typename T, int LG_L, int LG_R, int NX, int TS = 0, bool PS = false, int CC = 0,
           class Prefetch = NoPrefetch, bool TM = false, class NextF = NoPrefetch, class NextM = NoPrefetch>
 __device__ __forceinline__ void col_task(const ColArgs<T>& a, int b, int col0, int C, cx<T>* smbase,
                                          const twe<T>* tw, T* ms, bool live, double (&acc)[3],
@@ -874,7 +891,9 @@ __device__ __forceinline__ void col_task(const ColArgs<T>& a, int b, int col0, i
         mbar_wait(&tma.bars[0], tma.parity);
 #pragma unroll
         for (int k = 0; k < F::R; ++k) v[k] = tma.ft[(j + F::TG * k) * C + c];
-        __syncthreads();                                                         // tile free
+        fine_stamp_after(v[F::R - 1], 21);                                     // col: tile landed
+        if (tma.out && threadIdx.x == 0) bulk_wait_read();                     // previous task's output read
+        __syncthreads();                                                         // tile free, exchange buffer free
         if (threadIdx.x == 0) next_f();
     } else if (tile) {
         cp_async_wait<0>();
@@ -1010,6 +1029,26 @@ __device__ __forceinline__ void col_task(const ColArgs<T>& a, int b, int col0, i
         else fin = project_regs<true>(v, z, t_of, epi);
         if (act && !fin) first_bad(&a.st[b].bad, a.u_iter + 1);
         acc[0] = act ? g2 : 0.0;
+    }
+    if constexpr (TM) {
+        if (tma.out) {
+            // stage [n_y][C] in the exchange buffer; the tensor accelerator
+            // writes it out while the next task computes
+            if (act) {
+                constexpr int NY = 1 << LG_L, BOXR = NY < 256 ? NY : 256;
+                __syncthreads();                                   // FFT 2's last exchange reads are done
+#pragma unroll
+                for (int k = 0; k < F::R; ++k) smbase[(j + F::TG * k) * C + c] = v[k];
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncthreads();
+                if (threadIdx.x == 0) {
+                    for (int r = 0; r < NY; r += BOXR) tma_store_3d(tma.out, smbase + (size_t)r * C, tma.ox, r, tma.oz);
+                    bulk_commit();
+                }
+            }
+            fine_stamp(25);
+            return;
+        }
     }
     if (act) {
 #pragma unroll
@@ -1196,10 +1235,13 @@ struct SolveArgs {
     int tma;                   // the column phase's TMA maps below are valid
     CUtensorMap tm_in;         // column input w' ([batch][n_y][2 n_x] floats or doubles)
     CUtensorMap tm_m;          // m ([batch][n_y][n_x])
+    int tma_out;               // the column phase stores z' by TMA (tm_out valid)
+    CUtensorMap tm_out;        // z' ([batch][n_y][2 n_x])
 };
 
-// stamps[cta * kStampsPerCta + i] = %globaltimer at the i-th stamp point.
-constexpr int kStampsPerCta = 256;
+// stamps[cta * kStampsPerCta + i] = %globaltimer at the i-th stamp point
+// (PM_FINE builds: a longer row, slots 128.. hold the fine stamps).
+constexpr int kStampsPerCta = PM_FINE ? 1024 : 256;
 __device__ __forceinline__ void stamp(unsigned long long* s, int& i) {
     if (s && threadIdx.x == 0 && i < kStampsPerCta) {
         unsigned long long t;
@@ -1241,7 +1283,10 @@ struct SolveSmem {
     static constexpr int NTAB = 1;                                // forward transforms only (conjugate storage)
     static constexpr int TWR = FR::TW * NTAB;                     // entries
     static constexpr int TWC = SAME ? 0 : FC::TW * NTAB;
-    static constexpr int TWB = up16((TWR + TWC) * (int)sizeof(twe<T>));
+    // compact (c, s) shared twiddles (fp32, 4096 points with TMA tiles: the
+    // 65 KB table would not leave room for the column tile)
+    static constexpr bool TW2 = F32 && TV && LG >= 12;
+    static constexpr int TWB = up16((TWR + TWC) * (TW2 ? 8 : (int)sizeof(twe<T>)));
     static constexpr int TILE = up16((int)sizeof(cx<T>) * ((G > C ? G : C) << LG));   // one task's input
     static constexpr int LIMIT = 225 * 1024;
     // Cross-task prefetch (PM_PF=1) needs the staging, a tile and (measured:
@@ -1284,7 +1329,7 @@ struct SolveSmem {
     static constexpr bool TMA_F = PM_TMA_F && WANT && !TMA_A && BASE0 + FTB + 16 + 128 <= LIMIT;
     static constexpr bool TMA = TMA_A || TMA_B || TMA_C || TMA_F;
     static constexpr bool TMA_M = TMA && !TMA_F;                 // m streamed by TMA too
-    static constexpr bool TS = (TMA_B || TMA_C) ? false : TS0;
+    static constexpr int TS = ((TMA_B || TMA_C) ? false : TS0) ? (TW2 ? 2 : 1) : 0;
     static constexpr bool PS = (TMA_B || TMA_C) ? true : PS0;
     static constexpr int OFF_ST = EX;
     static constexpr int OFF_TILE = EX + (PS ? ST : 0);
@@ -1325,6 +1370,17 @@ __device__ __forceinline__ Tables<T> load_tables(const RowArgs<T>& r, const ColA
     using L = SolveSmem<T, LG, LGR_R, LGR_C, TV>;
     if constexpr (!L::TS) {
         return Tables<T>{r.twf, c.twf};
+    } else if constexpr (L::TS == 2) {
+        float2* t = reinterpret_cast<float2*>(smraw + L::OFF_TW);
+        constexpr int nr = L::FR::TW, nc = L::FC::TW;
+        float2* rf = t;
+        float2* cf = L::SAME ? rf : t + L::TWR;
+        for (int i = threadIdx.x; i < nr; i += blockDim.x) rf[i] = make_float2(r.twf[i].x, r.twf[i].y);
+        if constexpr (!L::SAME) {
+            for (int i = threadIdx.x; i < nc; i += blockDim.x) cf[i] = make_float2(c.twf[i].x, c.twf[i].y);
+        }
+        __syncthreads();
+        return Tables<T>{reinterpret_cast<const twe<T>*>(rf), reinterpret_cast<const twe<T>*>(cf)};
     } else {
         twe<T>* t = reinterpret_cast<twe<T>*>(smraw + L::OFF_TW);
         constexpr int nr = L::FR::TW, nc = L::FC::TW;
@@ -1427,6 +1483,7 @@ struct ColTma {
     const CUtensorMap* in;
     const CUtensorMap* m;
     unsigned* count;              // tile loads completed by this CTA (mbarrier parity)
+    const CUtensorMap* out;       // z' ([batch][n_y][2 n_x]) written by TMA stores (null: st.global)
 };
 
 template <typename T, int LG, int LGR_R, int LGR_C, bool TV = false>
@@ -1490,7 +1547,8 @@ __device__ __forceinline__ void col_phase(const ColArgs<T>& a, int batch, unsign
                 const int tn = t + gridDim.x;
                 auto next_f = [&]() { if (tn < total) issue_f(tn); };
                 auto next_m = [&]() { if (L::TMA_M && tn < total) issue_m(tn); };
-                TmaTask<T> tk{ft, L::TMA_M ? mt + ((tt * C) & (MA - 1)) : nullptr, bars, *ct.count & 1u, L::MC};
+                TmaTask<T> tk{ft, L::TMA_M ? mt + ((tt * C) & (MA - 1)) : nullptr, bars, *ct.count & 1u, L::MC,
+                              ct.out, 2 * tt * C, b};
                 double acc[3];
                 col_task<T, LG, LGR_C, NX, L::TS, L::PS, L::C, NoPrefetch, true, decltype(next_f), decltype(next_m)>(
                     a, b, tt * C, C, smem, tw.cf, ms, act, acc, nullptr, NoPrefetch{}, tk, next_f, next_m);
@@ -1504,6 +1562,7 @@ __device__ __forceinline__ void col_phase(const ColArgs<T>& a, int batch, unsign
                     }
                 }
             }
+            if (ct.out && threadIdx.x == 0) bulk_wait_all();     // z' complete before the grid barrier
             return;
         }
     }
@@ -1595,11 +1654,12 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const __grid_co
     Resident rs{a.res != 0 && (ALG == 1 ? L::RES_RAAR : L::RES_GS), false, false,
                 L::BYTES_T + (ALG == 1 ? L::XSE : 0), L::BYTES_T + (ALG == 1 ? L::XSE : 0) + L::ST};
     unsigned tma_count = 0;
-    ColTma ct{nullptr, nullptr, &tma_count};
+    ColTma ct{nullptr, nullptr, &tma_count, nullptr};
     if constexpr (L::TMA) {
         if (a.tma) {
             ct.in = &a.tm_in;
             ct.m = &a.tm_m;
+            if (a.tma_out) ct.out = &a.tm_out;
             if (threadIdx.x == 0) {
                 unsigned long long* bars = reinterpret_cast<unsigned long long*>(smraw + L::OFF_BAR);
                 mbar_init(&bars[0], 1);

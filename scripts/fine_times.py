@@ -26,9 +26,9 @@ plan = pm.transform.get_plan(spec, prec)
 for rep in range(3):
     plan.lib.pm_debug_phase_stamps(plan.handle, 1, None, 0)
     r = pm.solve(c, mm, cfg)
-st = np.zeros(1184 * 256, dtype=np.uint64)
+st = np.zeros(148 * 1024, dtype=np.uint64)       # PM_FINE rows: 1024 slots per CTA, fine from 128
 plan.lib.pm_debug_phase_stamps(plan.handle, 0, st.ctypes.data_as(_lib.C.c_void_p), st.size)
-S = st.reshape(1184, 256)[:, 128:].astype(np.int64)
+S = st.reshape(148, 1024)[:, 128:].astype(np.int64)
 ncta = int((S[:, 1] > 0).sum())
 trans = collections.defaultdict(list)
 for cta in range(ncta):
