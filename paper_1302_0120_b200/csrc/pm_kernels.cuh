@@ -560,6 +560,19 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
         : "memory");
 }
 
+// Copies completed on each row group's mbarrier (row TMA; their parity),
+// zeroed at kernel start.
+__device__ __forceinline__ unsigned* row_loads() {
+    __shared__ unsigned s[16];
+    return s;
+}
+
+// Contiguous global -> shared copy by the tensor accelerator (bytes % 16 == 0).
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+
 // TMA tensor store from shared memory (bulk async-group of the issuing thread).
 __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int x, int y, int z) {
     asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];"
@@ -669,7 +682,8 @@ template <typename T, int LG_L, int LG_R, class Sync, int ALG = -1, int TS = 0, 
 __device__ __forceinline__ void row_task(const RowArgs<T>& a, int b, int row, int j, cx<T>* sm,
                                          const twe<T>* tw, T* ps, bool inb_arg, bool live, Sync sync,
                                          const cx<T>* tile = nullptr, Prefetch prefetch = Prefetch{},
-                                         cx<T>* xs = nullptr, bool stage_p = true) {
+                                         cx<T>* xs = nullptr, bool stage_p = true,
+                                         unsigned long long* tbar = nullptr, unsigned tpar = 0) {
     using F = FftShape<LG_L, LG_R>;
     const size_t N = (size_t)a.nx * a.ny;
     // whole-warp groups never run out of bounds (the row phase skips them)
@@ -683,7 +697,9 @@ __device__ __forceinline__ void row_task(const RowArgs<T>& a, int b, int row, in
                        : (ALG != 0 && (a.mode == kRowRaar || a.mode == kRowProbe)) ? __ldcg(a.thr_x + b) : 0.0;
     cx<T> v[F::R];
     if (tile) {
-        cp_async_wait<0>();
+        // tbar: the tile was copied by the tensor accelerator (row TMA); else by cp.async (PF)
+        if (tbar) mbar_wait(tbar, tpar);
+        else cp_async_wait<0>();
         sync();
 #pragma unroll
         for (int k = 0; k < F::R; ++k) v[k] = tile[j + F::TG * k];                           // conj(z')
@@ -1339,7 +1355,15 @@ struct SolveSmem {
     static constexpr int OFF_FT = TMA_C ? EX : up128(BYTES);
     static constexpr int OFF_MT = OFF_FT + FTB;
     static constexpr int OFF_BAR = OFF_MT + (TMA_M ? MTB : 0);
-    static constexpr int TMA_END = TMA ? OFF_BAR + 16 : 0;
+    // TMA builds also stream the row phase's rows through the column tile
+    // (idle then), one bulk copy and one mbarrier per row group
+#ifndef PM_ROW_TMA
+#define PM_ROW_TMA 1
+#endif
+    static constexpr bool ROW_TMA = PM_ROW_TMA && TMA && FTB >= (int)sizeof(cx<T>) * (G << LG);
+    static constexpr int NBAR = 2 + (ROW_TMA ? G : 0);
+    static_assert(!ROW_TMA || G <= 16, "row_loads() holds 16 groups");
+    static constexpr int TMA_END = TMA ? OFF_BAR + up16(8 * NBAR) : 0;
     static constexpr int BYTES_T = TMA_END > BYTES ? TMA_END : BYTES;
     static constexpr bool XS = PS && BYTES_T + XSB <= LIMIT;
     static constexpr int OFF_XS = BYTES_T;
@@ -1417,7 +1441,7 @@ struct Resident {
 
 template <typename T, int LG, int LGR_R, int LGR_C, int ALG, bool TV = false>
 __device__ __forceinline__ void row_phase(const RowArgs<T>& a, int batch, unsigned char* smraw,
-                                          const Tables<T>& tw, Resident* rs = nullptr) {
+                                          const Tables<T>& tw, Resident* rs = nullptr, bool tma = false) {
     using L = SolveSmem<T, LG, LGR_R, LGR_C, TV>;
     using F = FftShape<LG, LGR_R>;
     cx<T>* smem = reinterpret_cast<cx<T>*>(smraw);
@@ -1433,6 +1457,19 @@ __device__ __forceinline__ void row_phase(const RowArgs<T>& a, int batch, unsign
     // prefetch the next round's row while this one computes (whole-warp
     // groups, more than one round in this CTA's share)
     const bool pf = L::PF && F::TG >= 32 && count > G;
+    // row TMA (ROW_TMA builds with TMA active): every row of a group arrives in
+    // its slice of the column tile by one bulk copy, issued a round ahead by
+    // the group's first thread; the group's mbarrier completes it
+    const bool rt = L::ROW_TMA && tma && F::TG >= 32;
+    cx<T>* rtile = reinterpret_cast<cx<T>*>(smraw + L::OFF_FT) + ((size_t)g << LG);
+    unsigned long long* rbar = reinterpret_cast<unsigned long long*>(smraw + L::OFF_BAR) + 2 + g;
+    unsigned* s_rloads = row_loads();
+    auto rissue = [&](int rr) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");     // earlier reads of the slice
+        mbar_expect_tx(rbar, (unsigned)(sizeof(cx<T>) * NX));
+        bulk_load(rtile, a.field + (size_t)(start + rr) * NX, (unsigned)(sizeof(cx<T>) * NX), rbar);
+    };
+    if (rt && j == 0 && g < count) rissue(g);
     for (int r0 = 0; r0 < count; r0 += G) {
         const bool inb = r0 + g < count;
         if (F::TG >= 32 && !inb) break;
@@ -1440,15 +1477,23 @@ __device__ __forceinline__ void row_phase(const RowArgs<T>& a, int batch, unsign
         const int b = r >> LG;
         const bool live = inb && mask_live(a.st + b);
         const int rn = r0 + G + g;                 // this group's next row in the share
+        const unsigned rpar = rt ? (s_rloads[g] & 1u) : 0u;
         auto prefetch = [&]() {
-            if (pf && rn < count)
+            if (rt) {
+                if (j == 0) {
+                    s_rloads[g] += 1;
+                    if (rn < count) rissue(rn);
+                }
+            } else if (pf && rn < count) {
                 stage_tile<cx<T>, 1, NX, F::TG>(tile, a.field + (size_t)(start + rn) * NX, 0, j);
+            }
         };
         constexpr bool XS = ALG == 1 && L::XS;
         row_task<T, LG, LGR_R, decltype(group_sync<F::TG>(g)), ALG, L::TS, L::PS, decltype(prefetch), XS>(
             a, b, r & (NX - 1), j, smem + g * F::SM, tw.rf, ps, inb, live, group_sync<F::TG>(g),
-            (pf && r0 > 0) ? tile : nullptr, prefetch,
-            XS ? reinterpret_cast<cx<T>*>(smraw + L::OFF_XS) + ((size_t)g << LG) : nullptr, stage_p);
+            rt ? rtile : ((pf && r0 > 0) ? tile : nullptr), prefetch,
+            XS ? reinterpret_cast<cx<T>*>(smraw + L::OFF_XS) + ((size_t)g << LG) : nullptr, stage_p,
+            rt ? rbar : nullptr, rpar);
     }
     if (res && a.mode != kRowInit) rs->p_ok = true;
 }
@@ -1513,7 +1558,7 @@ __device__ __forceinline__ void col_phase(const ColArgs<T>& a, int batch, unsign
     if constexpr (L::TMA) {
         // CTAs with several tasks in this phase (batches, large grids); a
         // single task is faster with direct loads (measured: 1024^2, 1 mask)
-        if (ct.in && a.mode == 2 && (int)blockIdx.x + (int)gridDim.x < total) {
+        if (ct.in && a.mode == 2 && 2 * (int)gridDim.x <= total) {
             // TMA: tiles for task t are in flight before t starts; each task
             // issues its successor's copies once its own tiles are consumed
             constexpr int BOXR = NX < 256 ? NX : 256;
@@ -1537,6 +1582,9 @@ __device__ __forceinline__ void col_phase(const ColArgs<T>& a, int batch, unsign
                 for (int r = 0; r < NX; r += BOXR)
                     tma_load_3d(mt + (size_t)r * L::MC, ct.m, c0 & ~(MA - 1), r, bt, &bars[1]);
             };
+            // (measured: claiming tasks from a global counter instead of this
+            // static order was slower, 4096^2 275 -> 283 us per iteration:
+            // concurrently running neighbours share sectors of the field)
             if (threadIdx.x == 0 && (int)blockIdx.x < total) {
                 issue_f(blockIdx.x);
                 if constexpr (L::TMA_M) issue_m(blockIdx.x);
@@ -1662,8 +1710,8 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const __grid_co
             if (a.tma_out) ct.out = &a.tm_out;
             if (threadIdx.x == 0) {
                 unsigned long long* bars = reinterpret_cast<unsigned long long*>(smraw + L::OFF_BAR);
-                mbar_init(&bars[0], 1);
-                mbar_init(&bars[1], 1);
+                for (int i = 0; i < L::NBAR; ++i) mbar_init(&bars[i], 1);
+                for (int i = 0; i < 16; ++i) row_loads()[i] = 0;
                 asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
             }
             __syncthreads();
@@ -1677,7 +1725,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const __grid_co
         grid_sync(a.bar, epoch);
         RowArgs<T> r = a.row;
         r.mode = kRowInit;
-        row_phase<T, LG, LGR_R, LGR_C, ALG, TV>(r, B, smraw, tw, &rs);     // u0 row half, w0 (RAAR: and x_0)
+        row_phase<T, LG, LGR_R, LGR_C, ALG, TV>(r, B, smraw, tw, &rs, a.tma != 0);     // u0 row half, w0 (RAAR: and x_0)
         grid_sync(a.bar, epoch);
         c.mode = 2;
         col_phase<T, LG, LGR_R, LGR_C, TV>(c, B, smraw, tw, ct, &rs);      // z1
@@ -1691,7 +1739,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const __grid_co
             RowArgs<T> r = a.row;
             r.mode = kRowRaar;
             r.it = it;
-            row_phase<T, LG, LGR_R, LGR_C, ALG, TV>(r, B, smraw, tw, &rs);   // gap of x_{it-1}, x_it, w_it
+            row_phase<T, LG, LGR_R, LGR_C, ALG, TV>(r, B, smraw, tw, &rs, a.tma != 0);   // gap of x_{it-1}, x_it, w_it
             grid_sync(a.bar, epoch);
             decide_phase_raar<T>(r, B, it - 1);
             if (early || lock) grid_sync(a.bar, epoch);
@@ -1705,7 +1753,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const __grid_co
             RowArgs<T> r = a.row;
             r.mode = kRowProbe;
             r.it = a.it_end;
-            row_phase<T, LG, LGR_R, LGR_C, ALG, TV>(r, B, smraw, tw, &rs);   // gap of x_{it_end-1}
+            row_phase<T, LG, LGR_R, LGR_C, ALG, TV>(r, B, smraw, tw, &rs, a.tma != 0);   // gap of x_{it_end-1}
             grid_sync(a.bar, epoch);
             decide_phase_raar<T>(r, B, a.it_end - 1);
             grid_sync(a.bar, epoch);
@@ -1721,7 +1769,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const __grid_co
             r.mode = kRowGS;
             r.it = it;
             fine_stamp(1);
-            row_phase<T, LG, LGR_R, LGR_C, ALG, TV>(r, B, smraw, tw, &rs);   // u_it, w_it
+            row_phase<T, LG, LGR_R, LGR_C, ALG, TV>(r, B, smraw, tw, &rs, a.tma != 0);   // u_it, w_it
             stamp(a.stamps, si);
             fine_stamp(2);
             grid_sync(a.bar, epoch);
