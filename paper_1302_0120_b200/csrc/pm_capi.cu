@@ -749,14 +749,18 @@ int solve_cols(const pm_plan* pl) {
     return std::max(1, k.solve_threads / std::max(1, k.col.TG));
 }
 
-// [depth][n_y][width] elements of `esize` bytes, boxes [1][min(256, n_y)][box_w].
+// [depth][n_y][width] elements of `esize` bytes viewed as 256-row blocks, boxes [n_y/256][256][box_w].
 bool tma_encode(CUtensorMap* map, void* base, int single, long long width, int n_y, int depth, int box_w) {
     auto fn = tma_encode_fn();
     if (!fn || !base || ((uintptr_t)base & 15)) return false;
     const size_t esz = single ? 4 : 8;
-    cuuint64_t dims[3] = {(cuuint64_t)width, (cuuint64_t)n_y, (cuuint64_t)std::max(depth, 1)};
-    cuuint64_t strides[2] = {(cuuint64_t)(width * esz), (cuuint64_t)(width * esz * n_y)};
-    cuuint32_t box[3] = {(cuuint32_t)box_w, (cuuint32_t)std::min(256, n_y), 1};
+    // rows in blocks of 256: [mask * n_y/256 + block][row][width], so one box
+    // {box_w, 256, n_y/256} is a task's whole [n_y][box_w] tile (one copy
+    // instruction per tile instead of n_y/256)
+    if (n_y % 256 != 0 || n_y / 256 > 256) return false;
+    cuuint64_t dims[3] = {(cuuint64_t)width, 256, (cuuint64_t)(n_y / 256) * std::max(depth, 1)};
+    cuuint64_t strides[2] = {(cuuint64_t)(width * esz), (cuuint64_t)(width * esz * 256)};
+    cuuint32_t box[3] = {(cuuint32_t)box_w, 256, (cuuint32_t)(n_y / 256)};
     cuuint32_t estr[3] = {1, 1, 1};
     if ((box_w * esz) % 16 != 0 || box_w > 256 || strides[0] % 16 != 0) return false;
     CUresult r = fn(map, single ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims,

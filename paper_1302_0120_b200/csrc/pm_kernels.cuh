@@ -1051,14 +1051,14 @@ __device__ __forceinline__ void col_task(const ColArgs<T>& a, int b, int col0, i
             // stage [n_y][C] in the exchange buffer; the tensor accelerator
             // writes it out while the next task computes
             if (act) {
-                constexpr int NY = 1 << LG_L, BOXR = NY < 256 ? NY : 256;
+                constexpr int NY = 1 << LG_L;                      // TMA builds: NY >= 256 (blocked maps)
                 __syncthreads();                                   // FFT 2's last exchange reads are done
 #pragma unroll
                 for (int k = 0; k < F::R; ++k) smbase[(j + F::TG * k) * C + c] = v[k];
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 __syncthreads();
                 if (threadIdx.x == 0) {
-                    for (int r = 0; r < NY; r += BOXR) tma_store_3d(tma.out, smbase + (size_t)r * C, tma.ox, r, tma.oz);
+                    tma_store_3d(tma.out, smbase, tma.ox, 0, tma.oz * (NY / 256));
                     bulk_commit();
                 }
             }
@@ -1523,7 +1523,7 @@ __device__ __forceinline__ void final_phase(const FinalArgs<T>& a, int batch, un
 // part[b][t] so the per-mask total is combined in task order (independent of
 // which CTA ran which task, hence of batch size and grid size).
 // TMA maps of the column phase: its input (w') and m, as [batch][n_y][2 n_x]
-// / [batch][n_y][n_x] tensors with boxes of min(256, n_y) rows (null: no TMA).
+// / [batch][n_y][n_x] tensors in 256-row blocks, one box per task tile (null: no TMA).
 struct ColTma {
     const CUtensorMap* in;
     const CUtensorMap* m;
@@ -1561,7 +1561,7 @@ __device__ __forceinline__ void col_phase(const ColArgs<T>& a, int batch, unsign
         if (ct.in && a.mode == 2 && 2 * (int)gridDim.x <= total) {
             // TMA: tiles for task t are in flight before t starts; each task
             // issues its successor's copies once its own tiles are consumed
-            constexpr int BOXR = NX < 256 ? NX : 256;
+            static_assert(NX >= 256, "blocked TMA maps: whole 256-row blocks");
             cx<T>* ft = reinterpret_cast<cx<T>*>(smraw + L::OFF_FT);
             T* mt = reinterpret_cast<T*>(smraw + L::OFF_MT);
             unsigned long long* bars = reinterpret_cast<unsigned long long*>(smraw + L::OFF_BAR);
@@ -1569,7 +1569,7 @@ __device__ __forceinline__ void col_phase(const ColArgs<T>& a, int batch, unsign
                 const int bt = t / tpm, c0 = (t - bt * tpm) * C;
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // prior reads of the tile
                 mbar_expect_tx(&bars[0], (unsigned)(sizeof(cx<T>) * C * NX));
-                for (int r = 0; r < NX; r += BOXR) tma_load_3d(ft + (size_t)r * C, ct.in, 2 * c0, r, bt, &bars[0]);
+                tma_load_3d(ft, ct.in, 2 * c0, 0, bt * (NX / 256), &bars[0]);
             };
             // a box must start on a 16-byte boundary: when a task is narrower
             // than 16 bytes of m, the box starts at the aligned column below
@@ -1579,8 +1579,7 @@ __device__ __forceinline__ void col_phase(const ColArgs<T>& a, int batch, unsign
                 const int bt = t / tpm, c0 = (t - bt * tpm) * C;
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 mbar_expect_tx(&bars[1], (unsigned)(sizeof(T) * L::MC * NX));
-                for (int r = 0; r < NX; r += BOXR)
-                    tma_load_3d(mt + (size_t)r * L::MC, ct.m, c0 & ~(MA - 1), r, bt, &bars[1]);
+                tma_load_3d(mt, ct.m, c0 & ~(MA - 1), 0, bt * (NX / 256), &bars[1]);
             };
             // (measured: claiming tasks from a global counter instead of this
             // static order was slower, 4096^2 275 -> 283 us per iteration:
