@@ -2,7 +2,7 @@
 # One gpurun call's worth of evidence: GPU tests, smoke, per-size timings,
 # the bench line, the ncu launch list and one full ncu capture of the
 # persistent solve kernel. Usage (from the repo root, under gpurun):
-#   bash scripts/gpu_session.sh [tag] [what...]   what: tests smoke perf bench launches benchfull ref paper full
+#   bash scripts/gpu_session.sh [tag] [what...]   what: tests smoke perf bench launches benchfull ref configs paper full
 set -u
 TAG=${1:-r01}
 shift || true
@@ -32,6 +32,11 @@ for w in $WHAT; do
     ref)
       timeout 900 python bench.py --impl reference > "$OUT/bench_reference.json" 2> "$OUT/bench_reference.err"
       echo "ref rc=$?"; tail -c 1500 "$OUT/bench_reference.json" ;;
+    configs)
+      for c in 1 2 4 5; do
+        timeout 900 python bench.py --config $c > "$OUT/bench_config$c.json" 2> "$OUT/bench_config$c.err"
+        echo "config $c rc=$?"; tail -c 400 "$OUT/bench_config$c.json"
+      done ;;
     paper)
       timeout 300 python scripts/paper_config.py > "$OUT/paper.log" 2>&1; echo "paper rc=$?"; cat "$OUT/paper.log" ;;
     full)
