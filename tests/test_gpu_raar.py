@@ -9,6 +9,8 @@ fp64 field relL2 <= 1e-10 for K <= 20, fp32 <= 1e-4 for K <= 5; gap
 history <= 1e-10 relative (fp64, K <= 50) and <= 1e-2 (fp32, K <= 200).
 """
 
+import os
+
 import numpy as np
 import pytest
 
@@ -72,6 +74,17 @@ def test_raar_fp64_matches_oracle(n, path):
     r = gpu(p, m, "double", path=path, max_iters=K, beta=0.9)
     o = orc.solve(p, m, K, "double", algorithm="raar", beta=0.9)
     check_vs(r, o, "double", 1e-10)
+
+
+@pytest.mark.parametrize("n,tag,K", [(2048, "single", 5), (2048, "double", 6)])
+def test_raar_large_field_tma_build_matches_oracle(n, tag, K):
+    """2048^2 single masks run the persistent kernel's TMA build (column tiles
+    and the z' write-back through the tensor accelerator, rows through the
+    tile): RAAR against the oracle, short horizon."""
+    p, m = make_problem(n, 8, 7)
+    r = gpu(p, m, tag, max_iters=K, beta=0.9)
+    o = orc.solve(p, m, K, tag, algorithm="raar", beta=0.9, workers=os.cpu_count() or 1)
+    check_vs(r, o, tag, 1e-10 if tag == "double" else 1e-5)
 
 
 def test_raar512_survey_anchor():

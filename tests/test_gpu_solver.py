@@ -376,12 +376,15 @@ def test_batch_device_tolerances_match_host_and_reject_zero_inputs():
 
 
 @pytest.mark.parametrize("n,tag,algo,B", [(1024, "single", "gs", 4), (512, "double", "gs", 6), (256, "single", "gs", 24),
-                                          (512, "single", "raar", 5)])
+                                          (512, "single", "raar", 5), (2048, "single", "gs", 2),
+                                          (2048, "single", "raar", 2), (2048, "double", "gs", 2),
+                                          (4096, "single", "gs", 2)])
 def test_tma_batch_variant_is_bitwise_equal_to_single_solves(n, tag, algo, B):
     """Batches large enough to give every CTA several column tasks run the
     persistent kernel's TMA variant (tiles streamed by the tensor memory
     accelerator); each mask must equal its own single-mask solve bitwise,
-    early stopping included."""
+    early stopping included. At 2048^2 / 4096^2 both run the TMA build
+    (one-box column tiles, tensor stores of z', row copies through the tile)."""
     prec = pm.Precision.from_tag(tag)
     p, _ = make_problem(n, 8, 7)
     ms = np.stack([make_problem(n, 8, s)[1] for s in range(20, 20 + B)])
