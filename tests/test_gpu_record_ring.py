@@ -36,7 +36,7 @@ def _with_path(spec, prec, path, fn):
         plan.set_path(0)
 
 
-@pytest.mark.parametrize("n,ny,path", [(256, 256, 1), (256, 256, 2), (120, 90, 0)])
+@pytest.mark.parametrize("n,ny,path", [(256, 256, 1), (256, 256, 2), (120, 90, 0), (2048, 2048, 0)])
 @pytest.mark.parametrize("algo", ["gs", "raar"])
 def test_streamed_records_equal_the_history(n, ny, path, algo):
     spec, c, m = problem(n, ny=ny)
@@ -50,7 +50,7 @@ def test_streamed_records_equal_the_history(n, ny, path, algo):
     assert got.iters_run == 17 and not got.aborted
 
 
-@pytest.mark.parametrize("n,ny,path", [(256, 256, 1), (256, 256, 2), (120, 90, 0)])
+@pytest.mark.parametrize("n,ny,path", [(256, 256, 1), (256, 256, 2), (120, 90, 0), (2048, 2048, 0)])
 @pytest.mark.parametrize("algo", ["gs", "raar"])
 def test_lockstep_abort_lands_on_the_polled_iteration(n, ny, path, algo):
     """should_abort is polled once per iteration, after that iteration's
