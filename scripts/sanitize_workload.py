@@ -53,3 +53,5 @@ run(512, 512, "single", algo="raar", batch=5, K=2)
 run(60, 42, "double", algo="raar", K=4)          # mixed-radix RAAR (alternating iterate buffers)
 run(800, 600, "single", K=2, rand=True)            # mixed radix 16 x 10 x 5 / 12 x 10 x 5, device random start
 run(2048, 2048, "single", K=1)                     # persistent column phase staging m from its transposed copy
+run(4096, 4096, "single", K=1)                     # TMA build: compact shared twiddles, one-box tiles, tensor stores
+run(2048, 2048, "single", algo="raar", K=2)        # TMA build, RAAR (z' stores from the w' input tiles)
