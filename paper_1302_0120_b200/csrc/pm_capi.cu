@@ -336,36 +336,6 @@ __global__ void copy_kernel(const float4* __restrict__ a, float4* __restrict__ b
         b[i] = a[i];
 }
 
-// sum p^2 per amplitude grid (fixed partition) and the reconstructed-
-// intensity scale sum m^2 / sum p^2 per mask (sum |u|^2 = sum p^2 on S).
-template <typename T>
-__global__ void psum_partial_kernel(const T* p, long long n, long long chunk, long long pstride,
-                                    double* part, int nb) {
-    const T* q = p + blockIdx.y * pstride;
-    const long long lo = blockIdx.x * chunk, hi = min(n, lo + chunk);
-    double acc = 0.0;
-    for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) acc += (double)q[i] * (double)q[i];
-    const double s = block_sum(acc);
-    if (threadIdx.x == 0) part[blockIdx.y * nb + blockIdx.x] = s;
-}
-
-// escale[b] = energy[b] / sum p^2; with msum != null the energy sum m^2 is
-// itself reduced on the device (fixed order) from msum[b][0..nb).
-__global__ void escale_kernel(const double* part, int nb, int per_mask, double* energy, const double* msum,
-                              double* escale, int batch) {
-    const int b = blockIdx.x * blockDim.x + threadIdx.x;
-    if (b >= batch) return;
-    const double* q = part + (per_mask ? b : 0) * nb;
-    double s = 0.0;
-    for (int i = 0; i < nb; ++i) s += q[i];
-    if (msum) {
-        double e = 0.0;
-        for (int i = 0; i < nb; ++i) e += msum[b * nb + i];
-        energy[b] = e;
-    }
-    escale[b] = energy[b] / s;
-}
-
 // Decision tolerances of one mask (host and device): the reference's zero_tol
 // as the precision's float (src/projections.py:49-53 compares float32 mag with
 // the Python-float tolerance in float32, NEP 50). Every projection decides on
@@ -379,63 +349,144 @@ __host__ __device__ inline void zero_thresholds(double tp, double tm, bool singl
     *thrx = qp;
 }
 
-// S p into `out` (the P_S target of the GS row sweeps: they write S u).
-template <typename T>
-__global__ void scale_grid_kernel(const T* in, T* out, long long n, T s) {
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
-        out[i] = in[i] * s;
-}
+// The per-solve prologue in ONE launch (it was eight stream operations: two
+// memsets, the tolerance maxima and their combine, sum p^2, sum m^2, the
+// escale combine, S p): block (x, b) covers [x*chunk, (x+1)*chunk) of mask b,
+// a fixed partition of the grid (independent of batch), and leaves
+// {max p, max m, sum p^2, sum m^2} of its chunk in part[b][x]; with a shared
+// p only mask 0's blocks read it. The last block to finish (ticket) clears
+// the mask states and combines the partials in index order: the zero
+// tolerances 1024 eps max(.) and their thresholds (src/projections.py:41-43,
+// src/grid.py:21,33-34) when they are reduced on the device (an identically
+// zero p or all-dark m marks the mask done, reported as the reference's
+// ValueError), the energy sum m^2 when not given, and the reconstructed-
+// intensity scale escale = sum m^2 / sum p^2 (sum |u|^2 = sum p^2 on S).
+// S p is the P_S target of the GS row sweeps (they write S u). Every block
+// helps clear the histories.
+struct ProArgs {
+    const void* p;
+    const void* m;
+    void* ps;                 // S p (GS sweeps), or null
+    double S;
+    long long n, chunk;
+    int nb, batch, per_mask, single;
+    int do_tol, do_msum;
+    double* part;             // [batch][nb][4]
+    MaskState* st;
+    double* hist;
+    long long hist_n;         // doubles to clear
+    double *tolp, *thrp, *thrm, *thrx, *energy, *escale;
+    unsigned* ticket;
+};
 
-// Per-mask zero tolerances 1024 eps max (src/grid.py:21,33-34) and the
-// decision thresholds derived from them, from the device-resident p and m
-// (the host's session_setup formulas); an identically zero p or all-dark m
-// marks the mask done and is reported as the reference's ValueError.
-// Stage 1: block maxima over fixed chunks (max is order-independent).
 template <typename T>
-__global__ void tol_max_kernel(const T* p, long long p_stride, const T* m, long long n, long long chunk,
-                               double* part, int nb) {
-    const int b = blockIdx.y;
-    const T* pb = p + b * p_stride;
-    const T* mb = m + b * n;
-    const long long lo = blockIdx.x * chunk, hi = min(n, lo + chunk);
+__global__ void __launch_bounds__(256) prologue_kernel(ProArgs a) {
+    const int b = blockIdx.y, x = blockIdx.x;
+    const bool do_p = a.per_mask || b == 0;
+    const T* pb = static_cast<const T*>(a.p) + (a.per_mask ? (long long)b * a.n : 0);
+    const T* mb = static_cast<const T*>(a.m) + (long long)b * a.n;
+    T* psb = a.ps ? static_cast<T*>(a.ps) + (a.per_mask ? (long long)b * a.n : 0) : nullptr;
+    const long long lo = x * a.chunk, hi = min(a.n, lo + a.chunk);
+    const bool do_m = a.do_tol || a.do_msum;
     T pmx = T(0), mmx = T(0);
-    for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-        pmx = max(pmx, pb[i]);
-        mmx = max(mmx, mb[i]);
+    double p2 = 0.0, m2 = 0.0;
+    // eight loads in flight per thread (amplitudes are >= 0: the zero padding
+    // past the chunk changes neither the maxima nor the sums)
+    constexpr int U = 8;
+    for (long long base = lo + threadIdx.x; base < hi; base += U * blockDim.x) {
+        T v[U], w[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            const long long i = base + (long long)k * blockDim.x;
+            v[k] = (do_p && i < hi) ? pb[i] : T(0);
+            w[k] = (do_m && i < hi) ? mb[i] : T(0);
+        }
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            const long long i = base + (long long)k * blockDim.x;
+            pmx = max(pmx, v[k]);
+            p2 += (double)v[k] * (double)v[k];
+            mmx = max(mmx, w[k]);
+            m2 += (double)w[k] * (double)w[k];
+            if (psb && do_p && i < hi) psb[i] = v[k] * T(a.S);
+        }
     }
-    __shared__ T sp[32], sm2[32];
+    // fixed-order block reduction of the four values
+    __shared__ double red[4][8];
+    __shared__ int last;
+    double v4[4] = {(double)pmx, (double)mmx, p2, m2};
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) {
-        pmx = max(pmx, __shfl_xor_sync(0xffffffffu, pmx, o));
-        mmx = max(mmx, __shfl_xor_sync(0xffffffffu, mmx, o));
+        v4[0] = fmax(v4[0], __shfl_xor_sync(0xffffffffu, v4[0], o));
+        v4[1] = fmax(v4[1], __shfl_xor_sync(0xffffffffu, v4[1], o));
+        v4[2] += __shfl_xor_sync(0xffffffffu, v4[2], o);
+        v4[3] += __shfl_xor_sync(0xffffffffu, v4[3], o);
     }
-    if ((threadIdx.x & 31) == 0) { sp[threadIdx.x >> 5] = pmx; sm2[threadIdx.x >> 5] = mmx; }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0)
+        for (int k = 0; k < 4; ++k) red[k][warp] = v4[k];
+    // the histories: cleared by every block, grid-stride
+    const long long nblk = (long long)gridDim.x * gridDim.y, bid = (long long)b * gridDim.x + x;
+    for (long long i = bid * blockDim.x + threadIdx.x; i < a.hist_n; i += nblk * blockDim.x) a.hist[i] = 0.0;
     __syncthreads();
-    if (threadIdx.x != 0) return;
-    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) { pmx = max(pmx, sp[w]); mmx = max(mmx, sm2[w]); }
-    part[((size_t)b * nb + blockIdx.x) * 2 + 0] = (double)pmx;
-    part[((size_t)b * nb + blockIdx.x) * 2 + 1] = (double)mmx;
-}
-
-// Stage 2: one thread per mask.
-__global__ void tol_final_kernel(const double* part, int nb, int batch, int single, double nn, double* tolp,
-                                 double* thrp, double* thrm, double* thrms, double* thrx, MaskState* st) {
-    const int b = blockIdx.x * blockDim.x + threadIdx.x;
-    if (b >= batch) return;
-    double pmx = 0.0, mmx = 0.0;
-    for (int i = 0; i < nb; ++i) {
-        pmx = fmax(pmx, part[((size_t)b * nb + i) * 2 + 0]);
-        mmx = fmax(mmx, part[((size_t)b * nb + i) * 2 + 1]);
+    if (threadIdx.x == 0) {
+        double t[4] = {red[0][0], red[1][0], red[2][0], red[3][0]};
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+            t[0] = fmax(t[0], red[0][w]);
+            t[1] = fmax(t[1], red[1][w]);
+            t[2] += red[2][w];
+            t[3] += red[3][w];
+        }
+        double* q = a.part + ((size_t)b * a.nb + x) * 4;
+        for (int k = 0; k < 4; ++k) q[k] = t[k];
+        __threadfence();
+        last = atomicAdd(a.ticket, 1u) == (unsigned)(nblk - 1);
     }
-    const double eps = single ? 1.1920928955078125e-07 : 2.220446049250313e-16;
-    const double tp = 1024.0 * eps * pmx, tm = 1024.0 * eps * mmx;
-    tolp[b] = tp;
-    zero_thresholds(tp, tm, single, thrp + b, thrm + b, thrx + b);
-    const int z = (pmx == 0.0 ? 1 : 0) | (mmx == 0.0 ? 2 : 0);
-    if (z) {
-        st[b].zero = z;
-        st[b].done = 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    // mask states cleared before the zero flags are set
+    unsigned* sw = reinterpret_cast<unsigned*>(a.st);
+    const int words = a.batch * (int)(sizeof(MaskState) / sizeof(unsigned));
+    for (int i = threadIdx.x; i < words; i += blockDim.x) sw[i] = 0u;
+    __syncthreads();
+    // one warp per mask: each lane folds the partials lane, lane + 32, ... in
+    // order, then a fixed xor tree (deterministic; one round of loads in flight
+    // instead of nb dependent ones)
+    for (int k = warp; k < a.batch; k += (int)(blockDim.x >> 5)) {
+        const double* qp = a.part + (size_t)(a.per_mask ? k : 0) * a.nb * 4;
+        const double* qm = a.part + (size_t)k * a.nb * 4;
+        double pmax = 0.0, mmax = 0.0, sp = 0.0, sm = 0.0;
+#pragma unroll 5
+        for (int i = lane; i < a.nb; i += 32) {
+            pmax = fmax(pmax, __ldcg(qp + 4 * i + 0));
+            mmax = fmax(mmax, __ldcg(qm + 4 * i + 1));
+            sp += __ldcg(qp + 4 * i + 2);
+            sm += __ldcg(qm + 4 * i + 3);
+        }
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) {
+            pmax = fmax(pmax, __shfl_xor_sync(0xffffffffu, pmax, o));
+            mmax = fmax(mmax, __shfl_xor_sync(0xffffffffu, mmax, o));
+            sp += __shfl_xor_sync(0xffffffffu, sp, o);
+            sm += __shfl_xor_sync(0xffffffffu, sm, o);
+        }
+        if (lane != 0) continue;
+        if (a.do_tol) {
+            const double eps = a.single ? 1.1920928955078125e-07 : 2.220446049250313e-16;
+            const double tp = 1024.0 * eps * pmax, tm = 1024.0 * eps * mmax;
+            a.tolp[k] = tp;
+            zero_thresholds(tp, tm, a.single, a.thrp + k, a.thrm + k, a.thrx + k);
+            const int z = (pmax == 0.0 ? 1 : 0) | (mmax == 0.0 ? 2 : 0);
+            if (z) {
+                a.st[k].zero = z;
+                a.st[k].done = 1;
+            }
+        }
+        if (a.do_msum) a.energy[k] = sm;
+        a.escale[k] = a.energy[k] / sp;
     }
+    if (threadIdx.x == 0) *a.ticket = 0u;        // ready for the next launch (graph replays too)
 }
 
 // Host abort (should_abort -> True): the current iterate becomes the last.
@@ -578,7 +629,7 @@ struct pm_plan {
     double* thrms = nullptr;          // cap: column thresholds on the unscaled transform
     double* escale = nullptr;         // cap: sum m^2 / sum p^2
     double* energy = nullptr;         // cap: sum m^2 (host-provided)
-    double* psum = nullptr;           // cap * kPsumBlocks partial sums of p^2
+    double* psum = nullptr;           // (unused since the fused prologue)
     double* red = nullptr;            // reduction scratch
     int red_cap = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -788,7 +839,7 @@ int ensure_capacity(pm_plan* pl, int batch, int max_iters) {
     CK(cudaMalloc((void**)&pl->st, cap * sizeof(MaskState)));
     CK(cudaMalloc((void**)&pl->hist, (size_t)cap * hcap * 4 * sizeof(double)));
     CK(cudaMalloc((void**)&pl->part, (size_t)2 * cap * nb * 3 * sizeof(double)));
-    CK(cudaMalloc((void**)&pl->ctr, (size_t)cap * sizeof(unsigned)));
+    CK(cudaMalloc((void**)&pl->ctr, ((size_t)cap + 1) * sizeof(unsigned)));   // + the prologue's ticket
     // the per-mask scalars in one block, [energy][tolp][thrp][thrm][thrms][thrx] (cap
     // each): a solve with host tolerances uploads them in one copy (session_setup)
     CK(cudaMalloc((void**)&pl->energy, 6 * (size_t)cap * sizeof(double)));
@@ -799,7 +850,7 @@ int ensure_capacity(pm_plan* pl, int batch, int max_iters) {
     pl->thrx = pl->thrms + cap;
     CK(cudaMalloc((void**)&pl->escale, cap * sizeof(double)));
     CK(cudaMalloc((void**)&pl->psum, (size_t)2 * cap * 32 * sizeof(double)));
-    CK(cudaMemsetAsync(pl->ctr, 0, (size_t)cap * sizeof(unsigned), pl->stream));
+    CK(cudaMemsetAsync(pl->ctr, 0, ((size_t)cap + 1) * sizeof(unsigned), pl->stream));
     CK(cudaMemsetAsync(pl->st, 0, cap * sizeof(MaskState), pl->stream));
     pl->cap = cap;
     pl->hist_cap = hcap;
@@ -861,7 +912,7 @@ RowArgs<T> row_args(pm_plan* pl, int mode, int it) {
     RowArgs<T> a;
     a.field = (cx<T>*)pl->field;
     a.out = raar ? (cx<T>*)pl->field2 : a.field;
-    a.p = (const T*)(raar ? pl->s.p : pl->s.ps);   // GS: S p (see scale_grid_kernel); RAAR: p
+    a.p = (const T*)(raar ? pl->s.p : pl->s.ps);   // GS: S p (see prologue_kernel); RAAR: p
     a.p_stride = pl->s.p_stride;
     a.twf = (const twe<T>*)pl->tw_row;
     a.twi = (const twe<T>*)pl->tw_row_i;
@@ -1560,7 +1611,9 @@ int ensure_red(pm_plan* pl, int nb) {
     pl->red_cap = nb + 1;
     return PM_OK;
 }
-constexpr int kTolBlocks = 64;
+// Blocks per mask of the prologue: a fixed function of the grid size.
+int prologue_blocks(long long n) { return (int)std::max<long long>(1, std::min<long long>(148, (n + 4095) / 4096)); }
+
 
 // Upload per-mask scalars and reset state; point the session at p/m.
 int session_setup(pm_plan* pl, const void* d_p, const void* d_m, int batch, const pm_params* prm,
@@ -1598,12 +1651,13 @@ int session_setup(pm_plan* pl, const void* d_p, const void* d_m, int batch, cons
     double* h_en = reinterpret_cast<double*>(stage);
     for (int b = 0; b < batch; ++b) h_en[b] = energy ? energy[b] : 0.0;
     s.energy_on_device = energy == nullptr;
+    CKR(ensure_red(pl, 4 * prologue_blocks((long long)pl->N) * batch));   // the prologue's partials
     if (!tol_p) {
         CK(cudaMemcpyAsync(pl->energy, h_en, batch * sizeof(double), cudaMemcpyHostToDevice, pl->stream));
         // tolerances from the device-resident p and m (no host pass over them);
         // their partial maxima live in `red` (sized here, outside any capture)
         s.tol_on_device = true;
-        return ensure_red(pl, 2 * kTolBlocks * batch);
+        return PM_OK;
     }
     double* h_tolp = h_en + cap;
     double* h_thrp = h_tolp + cap;
@@ -1617,63 +1671,6 @@ int session_setup(pm_plan* pl, const void* d_p, const void* d_m, int batch, cons
         h_thrms[b] = 0.0;
     }
     CK(cudaMemcpyAsync(pl->energy, h_en, 6 * cap * sizeof(double), cudaMemcpyHostToDevice, pl->stream));
-    return PM_OK;
-}
-
-// Device-side tolerances (after the mask state is cleared, before the solve).
-
-int enqueue_tolerances(pm_plan* pl) {
-    auto& s = pl->s;
-    if (!s.tol_on_device) return PM_OK;
-    const int single = pl->prec == PM_SINGLE;
-    const long long n = (long long)pl->N;
-    const int nb = (int)std::min<long long>(kTolBlocks, (n + 255) / 256);
-    const long long chunk = (n + nb - 1) / nb;
-    const dim3 grid(nb, s.batch);
-    if (single)
-        tol_max_kernel<float><<<grid, 256, 0, pl->stream>>>((const float*)s.p, s.p_stride, (const float*)s.m, n,
-                                                            chunk, pl->red, nb);
-    else
-        tol_max_kernel<double><<<grid, 256, 0, pl->stream>>>((const double*)s.p, s.p_stride, (const double*)s.m, n,
-                                                             chunk, pl->red, nb);
-    tol_final_kernel<<<(s.batch + 127) / 128, 128, 0, pl->stream>>>(pl->red, nb, s.batch, single, (double)pl->N,
-                                                                     pl->tolp, pl->thrp, pl->thrm, pl->thrms,
-                                                                     pl->thrx, pl->st);
-    CK(cudaGetLastError());
-    pl->launches += 2;
-    return PM_OK;
-}
-
-constexpr int kPsumBlocks = 32;
-
-int enqueue_escale(pm_plan* pl) {
-    auto& s = pl->s;
-    const long long n = (long long)pl->N;
-    const long long chunk = (n + kPsumBlocks - 1) / kPsumBlocks;
-    const int npg = s.prm.p_per_mask ? s.batch : 1;
-    const dim3 grid(kPsumBlocks, npg);
-    if (pl->prec == PM_SINGLE)
-        psum_partial_kernel<float><<<grid, 256, 0, pl->stream>>>((const float*)s.p, n, chunk, s.p_stride,
-                                                                  pl->psum, kPsumBlocks);
-    else
-        psum_partial_kernel<double><<<grid, 256, 0, pl->stream>>>((const double*)s.p, n, chunk, s.p_stride,
-                                                                   pl->psum, kPsumBlocks);
-    double* msum = nullptr;
-    if (s.energy_on_device) {
-        msum = pl->psum + (size_t)pl->cap * kPsumBlocks;
-        const dim3 gm(kPsumBlocks, s.batch);
-        if (pl->prec == PM_SINGLE)
-            psum_partial_kernel<float><<<gm, 256, 0, pl->stream>>>((const float*)s.m, n, chunk, (long long)pl->N,
-                                                                    msum, kPsumBlocks);
-        else
-            psum_partial_kernel<double><<<gm, 256, 0, pl->stream>>>((const double*)s.m, n, chunk, (long long)pl->N,
-                                                                     msum, kPsumBlocks);
-        pl->launches++;
-    }
-    escale_kernel<<<(s.batch + 127) / 128, 128, 0, pl->stream>>>(pl->psum, kPsumBlocks, s.prm.p_per_mask,
-                                                                  pl->energy, msum, pl->escale, s.batch);
-    CK(cudaGetLastError());
-    pl->launches += 2;
     return PM_OK;
 }
 
@@ -1703,21 +1700,6 @@ int ensure_ps(pm_plan* pl, int grids) {
     pl->ps_bytes = 0;
     CK(cudaMalloc(&pl->ps, bytes));
     pl->ps_bytes = bytes;
-    return PM_OK;
-}
-
-int enqueue_ps(pm_plan* pl) {
-    auto& s = pl->s;
-    if (!s.ps) return PM_OK;
-    const long long n = (long long)(s.prm.p_per_mask ? s.batch : 1) * (long long)pl->N;
-    const int blocks = (int)std::min<long long>((n + 255) / 256, 148 * 8);
-    const double S = 1.0 / std::sqrt((double)pl->N);
-    if (pl->prec == PM_SINGLE)
-        scale_grid_kernel<float><<<blocks, 256, 0, pl->stream>>>((const float*)s.p, (float*)pl->ps, n, (float)S);
-    else
-        scale_grid_kernel<double><<<blocks, 256, 0, pl->stream>>>((const double*)s.p, (double*)pl->ps, n, S);
-    CK(cudaGetLastError());
-    pl->launches++;
     return PM_OK;
 }
 
@@ -1757,14 +1739,47 @@ int enqueue_mT(pm_plan* pl) {
     return launch_transpose_m(pl);
 }
 
+int enqueue_prologue(pm_plan* pl) {
+    auto& s = pl->s;
+    const long long n = (long long)pl->N;
+    ProArgs a{};
+    a.p = s.p;
+    a.m = s.m;
+    a.ps = const_cast<void*>(s.ps);
+    a.S = 1.0 / std::sqrt((double)pl->N);
+    a.n = n;
+    a.nb = prologue_blocks(n);
+    a.chunk = (n + a.nb - 1) / a.nb;
+    a.batch = s.batch;
+    a.per_mask = s.prm.p_per_mask ? 1 : 0;
+    a.single = pl->prec == PM_SINGLE;
+    a.do_tol = s.tol_on_device ? 1 : 0;
+    a.do_msum = s.energy_on_device ? 1 : 0;
+    a.part = pl->red;
+    a.st = pl->st;
+    a.hist = pl->hist;
+    a.hist_n = (long long)s.batch * pl->hist_cap * 4;
+    a.tolp = pl->tolp;
+    a.thrp = pl->thrp;
+    a.thrm = pl->thrm;
+    a.thrx = pl->thrx;
+    a.energy = pl->energy;
+    a.escale = pl->escale;
+    a.ticket = pl->ctr + pl->cap;
+    const dim3 grid(a.nb, s.batch);
+    if (a.single)
+        prologue_kernel<float><<<grid, 256, 0, pl->stream>>>(a);
+    else
+        prologue_kernel<double><<<grid, 256, 0, pl->stream>>>(a);
+    CK(cudaGetLastError());
+    pl->launches++;
+    return PM_OK;
+}
+
 int enqueue_begin(pm_plan* pl) {
     auto& s = pl->s;
-    CK(cudaMemsetAsync(pl->st, 0, s.batch * sizeof(MaskState), pl->stream));
-    CK(cudaMemsetAsync(pl->hist, 0, (size_t)s.batch * pl->hist_cap * 4 * sizeof(double), pl->stream));
-    CKR(enqueue_tolerances(pl));
-    CKR(enqueue_escale(pl));
+    CKR(enqueue_prologue(pl));
     if (pl->generic) return gen_begin(pl);
-    CKR(enqueue_ps(pl));
     if (persistent(pl)) {
         CKR(enqueue_mT(pl));
         return solve_launch(pl, 1, 1, 1, 0);
@@ -1822,11 +1837,7 @@ int enqueue_full_solve(pm_plan* pl) {
     auto& s = pl->s;
     if (persistent(pl)) {
         // one cooperative launch: initial iterate, all iterations, final pair
-        CK(cudaMemsetAsync(pl->st, 0, s.batch * sizeof(MaskState), pl->stream));
-        CK(cudaMemsetAsync(pl->hist, 0, (size_t)s.batch * pl->hist_cap * 4 * sizeof(double), pl->stream));
-        CKR(enqueue_tolerances(pl));
-        CKR(enqueue_escale(pl));
-        CKR(enqueue_ps(pl));
+        CKR(enqueue_prologue(pl));
         CKR(enqueue_mT(pl));
         s.it = s.prm.max_iters;
         return solve_launch(pl, 1, 1, s.prm.max_iters + 1, 1);

@@ -258,7 +258,11 @@ __device__ __forceinline__ bool reduce_ticket(double (&acc)[NV], double* part, u
 // Phase of the complex128-cast value, np.mod(., 2pi) semantics, >= 2pi -> 0
 // (src/grid.py:168-176).
 __device__ __forceinline__ double phase_of(double re, double im) {
+#if PM_EXP_NOATAN
+    double th = im - re;          // experiment only: the cost of atan2 in the final pass
+#else
     double th = atan2(im, re);
+#endif
     if (th < 0.0) th = th + kTwoPi;
     else th = th + 0.0;                 // -0 -> +0 as np.mod does
     if (th >= kTwoPi) th = 0.0;
