@@ -842,6 +842,36 @@ __device__ __forceinline__ void final_task(const FinalArgs<T>& a, int b, int row
     }
     if (!act) return;
     const T tol = T(a.tol_p[b]);
+    if constexpr (F::TG <= 32 && F::SM >= F::L && F::R >= 8) {
+        // warp-synchronous rows: the epilogue (u*, the fp64 phase) rolled over
+        // the row through the group's exchange buffer, four elements in flight
+        // per thread. One copy of its code instead of R: fully unrolled, the
+        // fp64 atan2 made the final pass most of the kernel's cold instruction
+        // footprint (fetched from HBM after an L2 flush; profiles/r02_startup_times.txt).
+        sync();
+#pragma unroll
+        for (int k = 0; k < F::R; ++k) sm[j + F::TG * k] = v[k];
+        sync();
+#pragma unroll 1
+        for (int k0 = 0; k0 < F::R; k0 += 4) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int k = k0 + q;
+                const size_t x = o + F::TG * k;
+                const cx<T> vs = sm[j + F::TG * k];
+                if (a.v_star) a.v_star[x] = vs;
+                const cx<T> us = replace_mod_exact<T>(vs, p[F::TG * k], tol);
+                if (a.u_star) a.u_star[x] = us;
+                if (a.phases || a.levels) {
+                    double th = phase_of((double)us.x, (double)us.y);
+                    if (tol > T(0) && np_cabs(us) < tol) th = 0.0;        // np.abs(u*) < zero_tol
+                    if (a.phases) a.phases[x] = th;
+                    if (a.levels) a.levels[x] = level_of(th);
+                }
+            }
+        }
+        return;
+    }
 #pragma unroll
     for (int k = 0; k < F::R; ++k) {
         const size_t x = o + F::TG * k;
