@@ -1612,7 +1612,9 @@ int ensure_red(pm_plan* pl, int nb) {
     return PM_OK;
 }
 // Blocks per mask of the prologue: a fixed function of the grid size.
-int prologue_blocks(long long n) { return (int)std::max<long long>(1, std::min<long long>(148, (n + 4095) / 4096)); }
+// (8192 elements per block, up to 8 blocks per SM: enough loads in flight for
+// HBM-resident grids; the last block combines them one warp per mask)
+int prologue_blocks(long long n) { return (int)std::max<long long>(1, std::min<long long>(8 * 148, (n + 8191) / 8192)); }
 
 
 // Upload per-mask scalars and reset state; point the session at p/m.

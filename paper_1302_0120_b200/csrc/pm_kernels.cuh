@@ -1756,13 +1756,9 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const __grid_co
         c.u_iter = 0;
         col_phase<T, LG, LGR_R, LGR_C, TV>(c, B, smraw, tw);          // u0 column half
         grid_sync(a.bar, epoch);
-    }
-    if (ALG == 1 && a.do_init) {
-        ColArgs<T> c = a.col;
-        c.u_iter = 0;
         RowArgs<T> r = a.row;
         r.mode = kRowInit;
-        row_phase<T, LG, LGR_R, LGR_C, ALG, TV>(r, B, smraw, tw, &rs, a.tma != 0);     // u0 row half, w0 and x_0
+        row_phase<T, LG, LGR_R, LGR_C, ALG, TV>(r, B, smraw, tw, &rs, a.tma != 0);     // u0 row half, w0 (RAAR: and x_0)
         grid_sync(a.bar, epoch);
         c.mode = 2;
         col_phase<T, LG, LGR_R, LGR_C, TV>(c, B, smraw, tw, ct, &rs);      // z1
@@ -1801,30 +1797,24 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const __grid_co
             decide_phase_raar<T>(a.row, B, a.fin.ctl.max_iters);
         }
     } else {
-        // it = 0 (a launch that initialises) is the initial iterate's row half
-        // and z1 through the same row / column call sites as the iterations:
-        // one inlined copy of each phase's code instead of two (a smaller cold
-        // instruction footprint after an L2 flush)
-        for (int it = a.do_init ? 0 : a.it_begin; it < a.it_end; ++it) {
-            const bool step = it > 0;
+        for (int it = a.it_begin; it < a.it_end; ++it) {
             RowArgs<T> r = a.row;
-            r.mode = step ? kRowGS : kRowInit;
+            r.mode = kRowGS;
             r.it = it;
-            if (step) fine_stamp(1);
-            row_phase<T, LG, LGR_R, LGR_C, ALG, TV>(r, B, smraw, tw, &rs, a.tma != 0);   // u_it, w_it (u0, w0)
-            if (step) stamp(a.stamps, si);
-            if (step) fine_stamp(2);
+            fine_stamp(1);
+            row_phase<T, LG, LGR_R, LGR_C, ALG, TV>(r, B, smraw, tw, &rs, a.tma != 0);   // u_it, w_it
+            stamp(a.stamps, si);
+            fine_stamp(2);
             grid_sync(a.bar, epoch);
-            if (step) stamp(a.stamps, si);
-            if (step) fine_stamp(3);
+            stamp(a.stamps, si);
+            fine_stamp(3);
             ColArgs<T> c = a.col;
             c.mode = 2;
             c.u_iter = it;
             col_phase<T, LG, LGR_R, LGR_C, TV>(c, B, smraw, tw, ct, &rs);    // metrics of u_it, z_{it+1}
-            if (step) stamp(a.stamps, si);
-            if (step) fine_stamp(4);
+            stamp(a.stamps, si);
+            fine_stamp(4);
             grid_sync(a.bar, epoch);
-            if (!step) continue;
             stamp(a.stamps, si);
             fine_stamp(5);
             // decisions: records, early stop, max_iters, and the last iterate
